@@ -1,0 +1,417 @@
+"""Benchmark: TC-GS forward render on B200 (BASELINE.json metric, config 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+
+One step = one full frame of the hot path (K1 preprocess -> K2-K6 binning ->
+K7 tensor-core alpha + blend) for the config-2 workload: 1M synthetic
+Gaussians with SH degree 3 at 1920x1080, inputs resident in HBM (the 236 MB
+scene exceeds the 126 MB L2, so no flush is needed between frames).  N > 1
+shards camera views across ranks (one process per GPU, no collective on the
+data path; weak scaling: every rank renders K frames).
+
+The JSON line carries the device-timed throughput (`value`), the end-to-end
+throughput through the public API with host buffers (`e2e`), the roofline of
+the dominant kernel (K7), the CPU baseline (the oracle's C port of the
+reference renderer on this host's cores), clocks and the kernel-launch count.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/sec at 1080p (1M Gaussians) and alpha-blend ms/frame; TC/MUFU % of peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--scale", type=float, default=1.0, help="scene-size multiplier (testing only)")
+    ap.add_argument("--impl", default="tcgs", choices=["tcgs", "reference"])
+    ap.add_argument("--backend", default="tcgs")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def view_cameras(base, n):
+    """Views of the config scene: yaw steps of 0.5 mrad about the camera centre (view sharding)."""
+    from paper_2505_24796_b200.synthetic import CameraSpec
+
+    cams = []
+    for k in range(n):
+        th = 0.0005 * k
+        c, s = math.cos(th), math.sin(th)
+        v = np.array(base.view, dtype=np.float64).copy()
+        R = np.array([[c, 0.0, s], [0.0, 1.0, 0.0], [-s, 0.0, c]])
+        v[:3, :3] = R @ v[:3, :3]
+        v[:3, 3] = R @ v[:3, 3]
+        cams.append(CameraSpec(v, base.fx, base.fy, base.cx, base.cy, base.width, base.height, base.near))
+    return cams
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons (NVML) while the timed region runs."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.pynvml = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception:  # noqa: BLE001 - clocks are best effort
+            self.pynvml = None
+        return self
+
+    def _sample(self):
+        p = self.pynvml
+        self.samples.append(p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM))
+        r = p.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+            "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+        }
+        for k, bit in names.items():
+            if r & bit:
+                self.reasons.add(k)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                break
+            time.sleep(0.02)
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        if self.pynvml and not self.samples:
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                pass
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        busy = [s for s in self.samples]
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(busy)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def profile_traffic():
+    """K7 DRAM bytes per launch from the committed ncu --set full capture summary, if present."""
+    p = os.path.join(ROOT, "profiles", "k7_ncu_summary.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
+def launches_per_frame(P, cam, band_rows=None):
+    """Kernels libtcgs.so launches per frame (fixed schedule, see csrc/binning.cu)."""
+    tiles_x = (cam.width + 15) // 16
+    tiles_y = (cam.height + 15) // 16 if band_rows is None else band_rows
+    nt = tiles_x * tiles_y
+    bits = max(1, math.ceil(math.log2(max(nt, 2))))
+    tile_passes = math.ceil(bits / 8)
+    depth_passes = 8
+    k = 1 + 1  # init_counters, preprocess
+    if P > 0:
+        k += 1 + 3 * depth_passes  # depth_key_fix + (upsweep, scan, downsweep) per pass
+    k += 3  # count_upsweep, count_scan, duplicate_keys
+    k += 3 * tile_passes + 1  # tile sort + ranges
+    k += 1  # render
+    return k
+
+
+# ------------------------------------------------------------------------------------------ CPU side
+
+def cpu_reference_frame(scene, cam, rows):
+    """The oracle's C port of the reference renderer (project, build_tiles, blend) on host cores.
+    Blend runs on a band of `rows` tile rows and is extrapolated to the frame."""
+    import oracle
+
+    t0 = time.perf_counter()
+    colors = scene["colors"]
+    if scene.get("sh_degree", 0) > 0:
+        colors = oracle.sh_color(scene["means"], scene["features"], scene["sh_degree"], cam.view)
+    proj = oracle.project(scene["means"], scene["scales"], scene["rotations"], cam)
+    t1 = time.perf_counter()
+    off, ids = oracle.build_tiles(proj, cam)
+    t2 = time.perf_counter()
+    tiles_y = (cam.height + 15) // 16
+    r0 = max(0, tiles_y // 2 - rows // 2)
+    r1 = min(tiles_y, r0 + rows)
+    oracle.blend(proj, off, ids, scene["opacities"], colors, cam, band=(r0, r1))
+    t3 = time.perf_counter()
+    frame_s = (t1 - t0) + (t2 - t1) + (t3 - t2) * tiles_y / (r1 - r0)
+    return frame_s, {"preprocess_s": t1 - t0, "sort_s": t2 - t1, "blend_band_s": t3 - t2,
+                     "band_rows": r1 - r0, "tile_rows": tiles_y}
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2505_24796_b200 import synthetic
+
+    os.environ.setdefault("OMP_NUM_THREADS", str(cpu_threads()))
+    scene, cams = synthetic.config_scene(args.config, args.scale)
+    cam = cams[0]
+    rows = 2
+    for _ in range(max(args.warmup, 0)):
+        cpu_reference_frame(scene, cam, rows)
+    times = []
+    detail = None
+    for _ in range(args.steps):
+        s, detail = cpu_reference_frame(scene, cam, rows)
+        times.append(s)
+    mean_s = sum(times) / len(times)
+    fps = 1.0 / mean_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: " + synthetic.CONFIGS[args.config], "P": int(scene["means"].shape[0]),
+                   "width": cam.width, "height": cam.height},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
+                         "kind": "port",
+                         "sample": f"oracle C port (float64 restatement of tilesplat.render 'reference'): full "
+                                   f"project + build_tiles, blend on {detail['band_rows']} of {detail['tile_rows']} "
+                                   f"tile rows extrapolated to the frame"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "detail": detail,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ GPU side
+
+def run_tcgs(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_24796_b200 as tcgs
+    from paper_2505_24796_b200 import synthetic
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    scene, cams = synthetic.config_scene(args.config, args.scale)
+    base = cams[0]
+    n_views = world * (args.steps + args.warmup)
+    views = view_cameras(base, n_views)
+    my_views = views[rank::world]
+
+    cloud = tcgs.GaussianCloud.from_arrays(scene, dev)
+    r = tcgs.Renderer(dev, args.backend)
+    first = r.render_frame(cloud, base)  # sizes the workspace; stats of the base view
+    st0 = first.stats
+    stream = torch.cuda.current_stream(dev)
+
+    def frame(cam, ev=None):
+        return r.launch(cloud, cam, timers=ev)
+
+    for k in range(args.warmup):
+        frame(my_views[k])
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region: K frames, inputs resident in HBM
+    k7_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for k in range(args.steps):
+            frame(my_views[args.warmup + k], k7_ev[k])
+        stop.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(stop)
+    blend_ms = [e[2].elapsed_time(e[3]) for e in k7_ev]
+    pre_ms = [e[0].elapsed_time(e[1]) for e in k7_ev]
+    bin_ms = [e[1].elapsed_time(e[2]) for e in k7_ev]
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # per-frame stats of the last timed view (device counters)
+    rc, st_last = r.read_stats(cloud.P)
+
+    # ---- end to end through the public API: host scene -> device, render, image -> host
+    e2e = None
+    if not args.no_e2e:
+        host = {k: torch.as_tensor(np.ascontiguousarray(scene[k])).pin_memory()
+                for k in ("means", "scales", "rotations", "opacities", "features" if scene["sh_degree"] > 0 else "colors")}
+        feats_key = "features" if scene["sh_degree"] > 0 else "colors"
+        dev_bufs = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
+        out_host = torch.empty((base.height, base.width, 3), dtype=torch.float32).pin_memory()
+        stats_bytes = 9 * 8
+        h2d = sum(v.numel() * v.element_size() for v in host.values())
+        d2h = out_host.numel() * 4 + stats_bytes
+        e2e_steps = max(3, min(args.steps, 20))
+
+        def e2e_frame(cam):
+            for k, v in host.items():
+                dev_bufs[k].copy_(v, non_blocking=True)
+            c = tcgs.GaussianCloud(dev_bufs["means"], dev_bufs["scales"], dev_bufs["rotations"],
+                                   dev_bufs["opacities"], dev_bufs[feats_key],
+                                   scene["sh_degree"] if scene["sh_degree"] > 0 else -1)
+            rgb, T, cnt = r.launch(c, cam)
+            out_host.copy_(rgb, non_blocking=True)
+            r.read_stats(c.P)  # D2H of the frame's FragmentStats (synchronises the stream)
+
+        for k in range(2):
+            e2e_frame(my_views[k])
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for k in range(e2e_steps):
+            e2e_frame(my_views[k % len(my_views)])
+        torch.cuda.synchronize(dev)
+        e2e_s = time.perf_counter() - t0
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * e2e_steps / float(te.item()), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": e2e_steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    frames = world * args.steps
+    value = frames / (ms_max / 1e3)
+    blend_avg = sum(blend_ms) / len(blend_ms)
+    peaks, peak_kind = measured_peaks()
+    # K7 algorithmic work: F_alpha = f_blend + f_cull + pixels_terminated fragments, 16 flops each
+    # (length-8 dot = 2*8 flops, src/tilesplat/tensor_path.py:40,53); ex2 = f_blend + terminated.
+    F_alpha = st_last.f_blend + st_last.f_cull + st_last.pixels_terminated
+    tc_tflops = 16.0 * F_alpha / (blend_avg * 1e-3) / 1e12
+    ex2_rate = (st_last.f_blend + st_last.pixels_terminated) / (blend_avg * 1e-3)
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    ex2_peak = 148 * 16 * sm_mhz * 1e6  # MUFU: 16 ex2/clk/SM (nominal)
+    clocks = clk.summary()
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        threads = cpu_threads()
+        os.environ["OMP_NUM_THREADS"] = str(threads)
+        s, det = cpu_reference_frame(scene, base, rows=2)
+        cpu = {"value": 1.0 / s, "unit": "frames/s", "cores": threads, "kind": "port",
+               "sample": f"oracle C port of tilesplat.render 'reference' (float64), view 0: full project + "
+                         f"build_tiles, blend on {det['band_rows']}/{det['tile_rows']} tile rows extrapolated",
+               "detail": det}
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "frames/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64 preprocess / fp16-hi-lo tcgen05 alpha, fp32 blend",
+        "data": "synthetic (generator G, seed 2; SURVEY.md Appendix B)",
+        "config": {"workload": f"{args.config}: " + synthetic.CONFIGS[args.config],
+                   "P": cloud.P, "sh_degree": scene["sh_degree"], "width": base.width, "height": base.height,
+                   "parallelism": f"views x{world}" if world > 1 else "single view",
+                   "l2": "no flush: per-frame inputs (%.0f MB) exceed the 126 MB L2" % (
+                       sum(np.asarray(scene[k]).nbytes for k in ("means", "scales", "rotations", "opacities",
+                                                                  "features" if scene["sh_degree"] > 0 else "colors"))
+                       / 1e6),
+                   "backend": args.backend},
+        "alpha_blend_ms": blend_avg,
+        "stage_ms": {"preprocess": sum(pre_ms) / len(pre_ms), "binning": sum(bin_ms) / len(bin_ms),
+                     "blend": blend_avg},
+        "frame_stats": {**st_last.to_dict(), "n_visible": st_last.n_visible},
+        "roofline": {"kernel": "K7 render_kernel (alpha + blend)", "bound": "tensor", "achieved": tc_tflops,
+                     "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": tc_tflops / peaks["bf16_tflops"],
+                     "traffic": profile_traffic(), "peak_kind": peak_kind,
+                     "work": "16 flops x F_alpha (F_alpha = f_blend + f_cull + pixels_terminated)",
+                     "mufu": {"achieved_ex2_per_s": ex2_rate, "peak_ex2_per_s": ex2_peak,
+                              "frac": ex2_rate / ex2_peak, "peak_kind": "nominal 16/clk/SM"}},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches_per_frame(cloud.P, base) * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_tcgs(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,152 @@
+/*
+ * tcgs.h -- C ABI of libtcgs.so, the B200 (sm_100a) TC-GS forward renderer.
+ *
+ * Drop-in boundary for the reference's render entry point
+ *     tilesplat.render(scene, cam, backend) -> (ImageBuffer, FragmentStats)
+ *     (/root/reference/pkg/src/tilesplat/raster.py:161-201)
+ * whose stages are
+ *     project_scene  (src/tilesplat/projection.py:119-134)   -> tcgs_preprocess
+ *     build_tiles    (src/tilesplat/tiling.py:46-59)          -> tcgs_bin
+ *     per-tile backend.tile_evaluator + blend_tile
+ *                    (src/tilesplat/raster.py:102-146,
+ *                     src/tilesplat/tensor_path.py:117-194)   -> tcgs_blend
+ * and whose per-fragment plugin protocol (evaluator.fragment(j, active),
+ * src/tilesplat/raster.py:86-94) is NOT crossed: the whole tile loop runs on
+ * the GPU.  tcgs_blend_lists replays caller-given projected records and tile
+ * lists through the same blend kernel (debug / KAT entry).
+ *
+ * Conventions
+ *   - every pointer argument marked (device) is CUDA device memory owned by the
+ *     caller; the library allocates nothing on the hot path and keeps no
+ *     global mutable state except a thread-local last-error string;
+ *   - `stream` is a cudaStream_t passed as void*; every call is stream-ordered
+ *     and asynchronous except tcgs_read_stats (synchronises `stream`);
+ *   - return value 0 = success, negative = error code (tcgs_error_string).
+ */
+#ifndef TCGS_H_
+#define TCGS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TCGS_TILE_SIZE 16 /* src/tilesplat/tiling.py:11 */
+
+enum tcgs_status {
+    TCGS_OK = 0,
+    TCGS_ERR_INVALID_ARG = -1, /* wrapper raises ValueError (src/tilesplat/raster.py:157) */
+    TCGS_ERR_CUDA = -2,        /* wrapper raises RuntimeError */
+    TCGS_ERR_CAPACITY = -3,    /* splat count exceeded max_splats; tcgs_read_stats reports the need */
+    TCGS_ERR_DEVICE = -4,      /* not an sm_100 device */
+    TCGS_ERR_WORKSPACE = -5    /* workspace smaller than tcgs_workspace_size() */
+};
+
+/* Alpha-evaluation modes: compile-time instantiations of the same blend kernel. */
+enum tcgs_alpha_mode {
+    TCGS_ALPHA_TC_HILO = 0, /* tcgen05 fp16 K=16: hi/lo split Gaussian vector (default) */
+    TCGS_ALPHA_TC_K8 = 1,   /* tcgen05 fp16, the paper's length-8 vector (src/tilesplat/tensor_path.py:25-40) */
+    TCGS_ALPHA_FFMA = 2     /* CUDA-core FP32 quadratic form, no tensor cores (ablation baseline) */
+};
+
+enum tcgs_dtype { TCGS_F32 = 0, TCGS_F64 = 1 };
+
+/* World-space Gaussians, SoA (src/tilesplat/scene.py:24-47).  All arrays (device). */
+typedef struct tcgs_scene {
+    int64_t P;
+    int32_t sh_degree;     /* -1: `features` holds RGB in [0,1] [P,3] (Gaussian3D.color);
+                              0..3: SH coefficients [P,(d+1)^2,3] (3DGS convention) */
+    int32_t dtype;         /* enum tcgs_dtype, for every array below */
+    const void *means;     /* [P,3] */
+    const void *scales;    /* [P,3], activated (> 0) */
+    const void *rotations; /* [P,4] unit quaternion (w, x, y, z) */
+    const void *opacities; /* [P] in (0, 1] */
+    const void *features;  /* [P,3] or [P,(d+1)^2,3] */
+} tcgs_scene;
+
+/* Pinhole camera (src/tilesplat/scene.py:50-68). */
+typedef struct tcgs_camera {
+    double view[16]; /* world -> camera, row-major 4x4; +z forward, +y down */
+    double fx, fy, cx, cy;
+    double near_plane; /* cull when z <= near (src/tilesplat/projection.py:77) */
+    int32_t width, height;
+} tcgs_camera;
+
+typedef struct tcgs_opts {
+    int32_t tile_row_begin; /* render tile rows [begin, end); end <= 0 means all rows */
+    int32_t tile_row_end;
+    int32_t alpha_mode;     /* enum tcgs_alpha_mode */
+    int32_t early_cull;     /* exp_calls accounting: 1 = EarlyCull (tensor_path.py:148-154), 0 = reference (raster.py:94) */
+    int32_t debug;          /* 1: K1 also stores float64 conic/depth for tcgs_copy_projection */
+} tcgs_opts;
+
+/* FragmentStats (src/tilesplat/raster.py:19-49) plus extras. */
+typedef struct tcgs_stats {
+    int64_t n_splats;          /* N = total tile-list entries (band) */
+    int64_t dropped;           /* near-culled Gaussians */
+    int64_t f_blend, f_cull, f_skip, exp_calls, pixels_terminated;
+    int64_t n_visible;         /* Gaussians touching at least one tile of the band */
+    int64_t max_splats_needed; /* == n_splats; > max_splats on TCGS_ERR_CAPACITY */
+} tcgs_stats;
+
+/* Bytes of device workspace for P Gaussians, a width x height frame and at most max_splats splats. */
+size_t tcgs_workspace_size(int64_t P, int32_t width, int32_t height, int64_t max_splats);
+
+/* K1: EWA projection in float64 + SH colour + tile rectangle per Gaussian
+ * (replaces project/project_scene, src/tilesplat/projection.py:68-134). */
+int tcgs_preprocess(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts *opts, void *ws,
+                    size_t ws_bytes, int64_t max_splats, void *stream);
+
+/* K2-K6: depth-rank sort, duplicate-with-keys, tile radix sort, tile ranges
+ * (replaces build_tiles, src/tilesplat/tiling.py:46-59). */
+int tcgs_bin(int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes,
+             int64_t max_splats, void *stream);
+
+/* K7: tensor-core alpha + conditional blend per tile (replaces the tile loop of
+ * render + blend_tile, src/tilesplat/raster.py:110-146,177-193).
+ * Outputs (device, full frame, rows outside the band untouched):
+ *   rgb [H,W,3] f32, T [H,W] f32 (final transmittance), n_contrib [H,W] i32. */
+int tcgs_blend(int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes,
+               int64_t max_splats, float *rgb, float *T, int32_t *n_contrib, void *stream);
+
+/* K1 + K2-K6 + K7 in one call. */
+int tcgs_render(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts *opts, void *ws,
+                size_t ws_bytes, int64_t max_splats, float *rgb, float *T, int32_t *n_contrib, void *stream);
+
+/* Synchronises `stream` and reads the frame's FragmentStats. Returns TCGS_ERR_CAPACITY if the
+ * frame overflowed max_splats (stats->max_splats_needed then says how many are needed). */
+int tcgs_read_stats(const void *ws, int64_t P, const tcgs_opts *opts, tcgs_stats *stats, void *stream);
+
+/* Debug/KAT entry: blend caller-given projected records through K7.
+ *   mean2d [P,2] f64, conic [P,3] f64 (s11,s12,s22), opacity [P] f64, rgb [P,3] f32 (device);
+ *   tile lists as CSR: offsets [n_tiles+1] i64, ids [N] i32 (device), row-major tiles. */
+int tcgs_blend_lists(int64_t P, const double *mean2d, const double *conic, const double *opacity,
+                     const float *colors, const int64_t *offsets, const int32_t *ids, const tcgs_camera *cam,
+                     const tcgs_opts *opts, void *ws, size_t ws_bytes, float *rgb, float *T, int32_t *n_contrib,
+                     void *stream);
+
+/* Debug: copy the binned splat lists (tile-major Gaussian ids) and per-tile [start,end) ranges
+ * out of the workspace (device -> device). ranges has (band tiles) entries of 2 x i32. */
+int tcgs_copy_lists(const void *ws, int64_t P, const tcgs_camera *cam, const tcgs_opts *opts,
+                    int64_t max_splats, int32_t *ids_out, int32_t *ranges_out, void *stream);
+
+/* Debug: copy per-Gaussian projection results (device -> device): visible u8 [P], mean2d [P,2] f64,
+ * conic [P,3] f64, depth [P] f64, radius [P] i32, rgb [P,3] f32. */
+int tcgs_copy_projection(const void *ws, int64_t P, const tcgs_camera *cam, int64_t max_splats,
+                         uint8_t *visible, double *mean2d, double *conic, double *depth, int32_t *radius,
+                         float *rgb, void *stream);
+
+/* 0 if the current device is sm_100 (B200); TCGS_ERR_DEVICE otherwise. */
+int tcgs_device_check(void);
+
+const char *tcgs_error_string(int code);
+const char *tcgs_last_error(void);
+int tcgs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TCGS_H_ */

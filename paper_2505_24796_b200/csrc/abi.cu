@@ -1,0 +1,238 @@
+// abi.cu -- the extern "C" boundary of libtcgs.so (include/tcgs.h).
+#include <stdio.h>
+#include <string.h>
+
+#include "tcgs_internal.cuh"
+
+using namespace tcgs;
+
+namespace {
+
+thread_local char g_last_error[512] = "";
+
+int fail(int code, const char *msg) {
+    snprintf(g_last_error, sizeof(g_last_error), "%s", msg);
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *where) {
+    snprintf(g_last_error, sizeof(g_last_error), "%s: %s", where, cudaGetErrorString(e));
+    return TCGS_ERR_CUDA;
+}
+
+__global__ void init_counters(DevCounters *c) {
+    DevCounters z;
+    memset(&z, 0, sizeof(z));
+    z.key_min = ~0ull;
+    *c = z;
+}
+
+int check_common(const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes, int64_t P,
+                 int64_t max_splats) {
+    if (!cam || !ws) return fail(TCGS_ERR_INVALID_ARG, "null camera or workspace");
+    if (cam->width <= 0 || cam->height <= 0) return fail(TCGS_ERR_INVALID_ARG, "image dimensions must be positive");
+    if (!(cam->fx > 0) || !(cam->fy > 0)) return fail(TCGS_ERR_INVALID_ARG, "focal lengths must be positive");
+    if (!(cam->near_plane > 0)) return fail(TCGS_ERR_INVALID_ARG, "near clip must be positive");
+    if (P < 0 || P >= (int64_t)1 << 32) return fail(TCGS_ERR_INVALID_ARG, "P out of range");
+    if (max_splats < 1 || max_splats >= (int64_t)1 << 32) return fail(TCGS_ERR_INVALID_ARG, "max_splats out of range");
+    const int tx = (cam->width + TILE - 1) / TILE, ty = (cam->height + TILE - 1) / TILE;
+    if (tx > 32767 || ty > 32767) return fail(TCGS_ERR_INVALID_ARG, "image too large");
+    if (opts) {
+        if (opts->alpha_mode < 0 || opts->alpha_mode > TCGS_ALPHA_FFMA)
+            return fail(TCGS_ERR_INVALID_ARG, "unknown alpha mode");
+        if (opts->tile_row_end > 0 && (opts->tile_row_begin < 0 || opts->tile_row_begin >= opts->tile_row_end ||
+                                       opts->tile_row_end > ty))
+            return fail(TCGS_ERR_INVALID_ARG, "invalid tile-row band");
+    }
+    if (ws_bytes < Layout::make(P, cam->width, cam->height, max_splats).total)
+        return fail(TCGS_ERR_WORKSPACE, "workspace smaller than tcgs_workspace_size()");
+    return TCGS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tcgs_version(void) { return 1; }
+
+const char *tcgs_last_error(void) { return g_last_error; }
+
+const char *tcgs_error_string(int code) {
+    switch (code) {
+        case TCGS_OK: return "ok";
+        case TCGS_ERR_INVALID_ARG: return "invalid argument";
+        case TCGS_ERR_CUDA: return "CUDA error";
+        case TCGS_ERR_CAPACITY: return "splat capacity exceeded";
+        case TCGS_ERR_DEVICE: return "unsupported device (sm_100a required)";
+        case TCGS_ERR_WORKSPACE: return "workspace too small";
+        default: return "unknown error";
+    }
+}
+
+int tcgs_device_check(void) {
+    int dev = 0, major = 0, minor = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (major != 10 || minor != 0) {
+        snprintf(g_last_error, sizeof(g_last_error), "libtcgs.so is built for sm_100a; device is sm_%d%d", major, minor);
+        return TCGS_ERR_DEVICE;
+    }
+    return TCGS_OK;
+}
+
+size_t tcgs_workspace_size(int64_t P, int32_t width, int32_t height, int64_t max_splats) {
+    return Layout::make(P, width, height, max_splats).total;
+}
+
+int tcgs_preprocess(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts *opts, void *ws,
+                    size_t ws_bytes, int64_t max_splats, void *stream) {
+    if (!scene) return fail(TCGS_ERR_INVALID_ARG, "null scene");
+    int rc = check_common(cam, opts, ws, ws_bytes, scene->P, max_splats);
+    if (rc) return rc;
+    if (scene->sh_degree < -1 || scene->sh_degree > 3) return fail(TCGS_ERR_INVALID_ARG, "sh_degree must be -1..3");
+    if (scene->dtype != TCGS_F32 && scene->dtype != TCGS_F64) return fail(TCGS_ERR_INVALID_ARG, "dtype");
+    if (scene->P > 0 && (!scene->means || !scene->scales || !scene->rotations || !scene->opacities || !scene->features))
+        return fail(TCGS_ERR_INVALID_ARG, "null scene array");
+    cudaStream_t st = (cudaStream_t)stream;
+    const Layout L = Layout::make(scene->P, cam->width, cam->height, max_splats);
+    init_counters<<<1, 1, 0, st>>>(at<DevCounters>(ws, L.counters));
+    cudaError_t e = launch_preprocess(*scene, *cam, make_band(*cam, opts), opts ? opts->debug : 0, ws, L, st);
+    if (e != cudaSuccess) return cuda_fail(e, "preprocess");
+    return TCGS_OK;
+}
+
+int tcgs_bin(int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes,
+             int64_t max_splats, void *stream) {
+    int rc = check_common(cam, opts, ws, ws_bytes, P, max_splats);
+    if (rc) return rc;
+    const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
+    cudaError_t e = launch_bin(P, make_band(*cam, opts), ws, L, max_splats, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "bin");
+    return TCGS_OK;
+}
+
+int tcgs_blend(int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes,
+               int64_t max_splats, float *rgb, float *T, int32_t *n_contrib, void *stream) {
+    int rc = check_common(cam, opts, ws, ws_bytes, P, max_splats);
+    if (rc) return rc;
+    if (!rgb || !T || !n_contrib) return fail(TCGS_ERR_INVALID_ARG, "null output");
+    const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
+    cudaError_t e = launch_render(opts ? opts->alpha_mode : 0, *cam, make_band(*cam, opts), nullptr, ws, L, rgb, T,
+                                  n_contrib, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "render");
+    return TCGS_OK;
+}
+
+int tcgs_render(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes,
+                int64_t max_splats, float *rgb, float *T, int32_t *n_contrib, void *stream) {
+    int rc = tcgs_preprocess(scene, cam, opts, ws, ws_bytes, max_splats, stream);
+    if (rc) return rc;
+    rc = tcgs_bin(scene->P, cam, opts, ws, ws_bytes, max_splats, stream);
+    if (rc) return rc;
+    return tcgs_blend(scene->P, cam, opts, ws, ws_bytes, max_splats, rgb, T, n_contrib, stream);
+}
+
+int tcgs_read_stats(const void *ws, int64_t P, const tcgs_opts *opts, tcgs_stats *stats, void *stream) {
+    if (!ws || !stats) return fail(TCGS_ERR_INVALID_ARG, "null workspace or stats");
+    (void)P;
+    DevCounters c;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyAsync(&c, ws, sizeof(c), cudaMemcpyDeviceToHost, st);  // counters sit at offset 0
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "read_stats");
+    memset(stats, 0, sizeof(*stats));
+    stats->n_splats = (int64_t)c.n_splats;
+    stats->max_splats_needed = (int64_t)c.n_splats;
+    stats->dropped = (int64_t)c.dropped;
+    stats->n_visible = (int64_t)c.n_visible;
+    stats->f_blend = (int64_t)c.f_blend;
+    stats->f_cull = (int64_t)c.f_cull;
+    stats->pixels_terminated = (int64_t)c.pixels_terminated;
+    // every in-image (pixel, splat) pair is exactly one of blend / cull / skip (src/tilesplat/raster.py:124-145)
+    stats->f_skip = (int64_t)c.pairs - stats->f_blend - stats->f_cull;
+    const int early = opts ? opts->early_cull : 1;
+    stats->exp_calls = early ? stats->f_blend + stats->pixels_terminated
+                             : stats->f_blend + stats->f_cull + stats->pixels_terminated;
+    if (c.overflow) return fail(TCGS_ERR_CAPACITY, "splat count exceeded max_splats");
+    return TCGS_OK;
+}
+
+int tcgs_blend_lists(int64_t P, const double *mean2d, const double *conic, const double *opacity, const float *colors,
+                     const int64_t *offsets, const int32_t *ids, const tcgs_camera *cam, const tcgs_opts *opts,
+                     void *ws, size_t ws_bytes, float *rgb, float *T, int32_t *n_contrib, void *stream) {
+    int rc = check_common(cam, opts, ws, ws_bytes, P, 1);
+    if (rc) return rc;
+    if (P > 0 && (!mean2d || !conic || !opacity || !colors)) return fail(TCGS_ERR_INVALID_ARG, "null records");
+    if (!offsets || !rgb || !T || !n_contrib) return fail(TCGS_ERR_INVALID_ARG, "null list/output");
+    cudaStream_t st = (cudaStream_t)stream;
+    const Layout L = Layout::make(P, cam->width, cam->height, 1);
+    const Band band = make_band(*cam, opts);
+    init_counters<<<1, 1, 0, st>>>(at<DevCounters>(ws, L.counters));
+    cudaError_t e = launch_pack_lists(P, mean2d, conic, opacity, colors, offsets, band, ws, L, st);
+    if (e != cudaSuccess) return cuda_fail(e, "pack_lists");
+    e = launch_render(opts ? opts->alpha_mode : 0, *cam, band, reinterpret_cast<const uint32_t *>(ids), ws, L, rgb, T,
+                      n_contrib, st);
+    if (e != cudaSuccess) return cuda_fail(e, "render");
+    return TCGS_OK;
+}
+
+int tcgs_copy_lists(const void *ws, int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, int64_t max_splats,
+                    int32_t *ids_out, int32_t *ranges_out, void *stream) {
+    if (!ws || !cam || !ids_out || !ranges_out) return fail(TCGS_ERR_INVALID_ARG, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
+    DevCounters c;
+    cudaError_t e = cudaMemcpyAsync(&c, ws, sizeof(c), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "copy_lists");
+    const int64_t n = (int64_t)c.n_splats < max_splats ? (int64_t)c.n_splats : max_splats;
+    const uint32_t *src = at<uint32_t>(ws, c.tile_cur ? L.tval[1] : L.tval[0]);
+    if (n > 0) e = cudaMemcpyAsync(ids_out, src, sizeof(uint32_t) * (size_t)n, cudaMemcpyDeviceToDevice, st);
+    const Band band = make_band(*cam, opts);
+    if (e == cudaSuccess && band.n_tiles() > 0)
+        e = cudaMemcpyAsync(ranges_out, at<uint2>(ws, L.ranges), sizeof(uint2) * (size_t)band.n_tiles(),
+                            cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "copy_lists");
+    return TCGS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void copy_projection_kernel(int64_t P, const int32_t *radius, const Rec *rec, const double *dconic,
+                                       const double *ddepth, uint8_t *visible, double *mean2d, double *conic,
+                                       double *depth, int32_t *rad_out, float *rgb) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P) return;
+    const int32_t r = radius[i];
+    visible[i] = r >= 0;
+    rad_out[i] = r;
+    conic[3 * i] = dconic[3 * i];
+    conic[3 * i + 1] = dconic[3 * i + 1];
+    conic[3 * i + 2] = dconic[3 * i + 2];
+    depth[i] = ddepth[i];
+    const Rec q = rec[i];
+    mean2d[2 * i] = q.mx;
+    mean2d[2 * i + 1] = q.my;
+    rgb[3 * i] = q.r;
+    rgb[3 * i + 1] = q.g;
+    rgb[3 * i + 2] = q.b;
+}
+}  // namespace
+
+extern "C" int tcgs_copy_projection(const void *ws, int64_t P, const tcgs_camera *cam, int64_t max_splats,
+                                    uint8_t *visible, double *mean2d, double *conic, double *depth, int32_t *radius,
+                                    float *rgb, void *stream) {
+    if (!ws || !cam || !visible || !mean2d || !conic || !depth || !radius || !rgb)
+        return fail(TCGS_ERR_INVALID_ARG, "null argument");
+    if (P <= 0) return TCGS_OK;
+    const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
+    copy_projection_kernel<<<(unsigned)((P + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        P, at<int32_t>(ws, L.radius), at<Rec>(ws, L.rec), at<double>(ws, L.dbg_conic), at<double>(ws, L.dbg_depth),
+        visible, mean2d, conic, depth, radius, rgb);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "copy_projection");
+    return TCGS_OK;
+}

@@ -1,0 +1,361 @@
+// preprocess.cu -- K1: EWA projection of every Gaussian in float64 (sm_100a).
+//
+// Replaces tilesplat.projection.project / project_scene
+// (/root/reference/pkg/src/tilesplat/projection.py:68-134), covariance_of
+// (src/tilesplat/scene.py:83-101) and tiling.covered_tiles
+// (src/tilesplat/tiling.py:34-43).  One thread per Gaussian; HBM-bound
+// (reads 56 B of geometry + 12*(d+1)^2 B of SH, writes a 48 B render record,
+// an 8 B tile rectangle, a 4 B tile count and an 8 B depth key).
+//
+// Bit-exactness: this translation unit is compiled with --fmad=false so every
+// a*b+c below is two IEEE roundings exactly as numpy evaluates it; the
+// explicit fma() calls reproduce OpenBLAS's dgemm/dgemv operation order
+// for the reference's small matmuls (measured: DESIGN.md "bit-exact
+// preprocess"), and py_hypot() restates CPython's math.hypot.  Radius, tile
+// rectangles, mean2d and depth therefore equal the reference's bit for bit,
+// which the binning parity test checks.
+#include <float.h>
+
+#include "tcgs_internal.cuh"
+
+namespace tcgs {
+
+namespace {
+
+struct dl {
+    double hi, lo;
+};
+__device__ __forceinline__ dl dl_mul(double x, double y) {
+    dl r;
+    r.hi = x * y;
+    r.lo = fma(x, y, -r.hi);
+    return r;
+}
+__device__ __forceinline__ dl dl_fast_sum(double a, double b) {
+    dl r;
+    r.hi = a + b;
+    double z = r.hi - a;
+    r.lo = b - z;
+    return r;
+}
+
+// CPython 3.12 math.hypot for two arguments (vector_norm with differential correction).
+__device__ double py_hypot(double x, double y) {
+    x = fabs(x);
+    y = fabs(y);
+    double mx = x > y ? x : y;
+    if (isinf(mx)) return mx;
+    if (isnan(x) || isnan(y)) return __longlong_as_double(0x7ff8000000000000ll);
+    if (mx == 0.0) return mx;
+    int max_e;
+    frexp(mx, &max_e);
+    double pre = 1.0;
+    if (max_e < -1023) {  // subnormal inputs: rescale (never hit by projected covariances)
+        x /= DBL_MIN;
+        y /= DBL_MIN;
+        mx /= DBL_MIN;
+        pre = DBL_MIN;
+        frexp(mx, &max_e);
+    }
+    double scale = ldexp(1.0, -max_e);
+    double csum = 1.0, frac1 = 0.0, frac2 = 0.0;
+    double v[2] = {x, y};
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+        double t = v[i] * scale;
+        dl pr = dl_mul(t, t);
+        dl sm = dl_fast_sum(csum, pr.hi);
+        csum = sm.hi;
+        frac1 += pr.lo;
+        frac2 += sm.lo;
+    }
+    double h = sqrt(csum - 1.0 + (frac1 + frac2));
+    dl pr = dl_mul(-h, h);
+    dl sm = dl_fast_sum(csum, pr.hi);
+    csum = sm.hi;
+    frac1 += pr.lo;
+    frac2 += sm.lo;
+    double xx = csum - 1.0 + (frac1 + frac2);
+    h += xx / (2.0 * h);
+    return pre * (h / scale);
+}
+
+// OpenBLAS dgemm / dgemv entry order for K = 3.
+__device__ __forceinline__ double dot3_gemm(double a0, double a1, double a2, double b0, double b1, double b2) {
+    return fma(a2, b2, fma(a1, b1, a0 * b0));
+}
+__device__ __forceinline__ double dot3_gemv(double a0, double a1, double a2, double b0, double b1, double b2) {
+    return fma(a2, b2, fma(a0, b0, a1 * b1));
+}
+
+template <typename T>
+__device__ __forceinline__ double ld(const T *p, int64_t i) {
+    return static_cast<double>(__ldg(p + i));
+}
+
+__constant__ double SH_C1 = 0.4886025119029199;
+__constant__ double SH_C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005, -1.0925484305920792,
+                                0.5462742152960396};
+__constant__ double SH_C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
+                                -0.4570457994644658, 1.445305721320277, -0.5900435899266435};
+
+// 3DGS spherical-harmonics colour (degree <= 3), float64; NOT in the reference (parity unpinned,
+// SURVEY.md Appendix E).  Same operation order as oracle/tcgs_oracle.c:oracle_sh_color.
+template <typename T>
+__device__ void sh_color(const T *sh, int deg, double x, double y, double z, float out[3]) {
+    const double C0 = 0.28209479177387814;
+    for (int ch = 0; ch < 3; ch++) {
+        double r = C0 * ld(sh, 0 * 3 + ch);
+        if (deg >= 1) r += -SH_C1 * y * ld(sh, 1 * 3 + ch) + SH_C1 * z * ld(sh, 2 * 3 + ch) - SH_C1 * x * ld(sh, 3 * 3 + ch);
+        if (deg >= 2) {
+            double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+            r += SH_C2[0] * xy * ld(sh, 4 * 3 + ch) + SH_C2[1] * yz * ld(sh, 5 * 3 + ch) +
+                 SH_C2[2] * (2.0 * zz - xx - yy) * ld(sh, 6 * 3 + ch) + SH_C2[3] * xz * ld(sh, 7 * 3 + ch) +
+                 SH_C2[4] * (xx - yy) * ld(sh, 8 * 3 + ch);
+            if (deg >= 3) {
+                r += SH_C3[0] * y * (3.0 * xx - yy) * ld(sh, 9 * 3 + ch) + SH_C3[1] * xy * z * ld(sh, 10 * 3 + ch) +
+                     SH_C3[2] * y * (4.0 * zz - xx - yy) * ld(sh, 11 * 3 + ch) +
+                     SH_C3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy) * ld(sh, 12 * 3 + ch) +
+                     SH_C3[4] * x * (4.0 * zz - xx - yy) * ld(sh, 13 * 3 + ch) +
+                     SH_C3[5] * z * (xx - yy) * ld(sh, 14 * 3 + ch) + SH_C3[6] * x * (xx - 3.0 * yy) * ld(sh, 15 * 3 + ch);
+            }
+        }
+        r += 0.5;
+        out[ch] = (float)(r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r));
+    }
+}
+
+struct PreArgs {
+    tcgs_camera cam;
+    double campos[3];
+    int64_t P;
+    int sh_degree;
+    int tiles_x, tiles_y, band_y0, band_y1;
+    int debug;
+    Rec *rec;
+    short4 *rect;
+    uint32_t *touched;
+    unsigned long long *keys;
+    uint32_t *idx;
+    int32_t *radius;
+    double *dbg_conic;
+    double *dbg_depth;
+    DevCounters *ctr;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__restrict__ means,
+                                                         const T *__restrict__ scales, const T *__restrict__ rots,
+                                                         const T *__restrict__ opac, const T *__restrict__ feats) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool in_range = i < a.P;
+    unsigned long long key = ~0ull;  // "touches nothing": rewritten by depth_key_fix
+    uint32_t touched = 0;
+    bool dropped = false;
+    if (in_range) {
+        const double *V = a.cam.view;
+        const double m0 = ld(means, 3 * i), m1 = ld(means, 3 * i + 1), m2 = ld(means, 3 * i + 2);
+        double t[3];
+#pragma unroll
+        for (int k = 0; k < 3; k++) t[k] = dot3_gemv(V[4 * k + 0], V[4 * k + 1], V[4 * k + 2], m0, m1, m2) + V[4 * k + 3];
+        const double tz = t[2];
+        a.radius[i] = -1;
+        if (!(tz > a.cam.near_plane)) {  // src/tilesplat/projection.py:76-78 (tz <= near culls)
+            dropped = true;
+        } else {
+            const double fx = a.cam.fx, fy = a.cam.fy;
+            const double mx = fx * t[0] / tz + a.cam.cx;
+            const double my = fy * t[1] / tz + a.cam.cy;
+            const double jac[2][3] = {{fx / tz, 0.0, -fx * t[0] / (tz * tz)}, {0.0, fy / tz, -fy * t[1] / (tz * tz)}};
+            // covariance_of (src/tilesplat/scene.py:83-101)
+            const double w = ld(rots, 4 * i), x = ld(rots, 4 * i + 1), y = ld(rots, 4 * i + 2), z = ld(rots, 4 * i + 3);
+            const double r[3][3] = {
+                {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
+                {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
+                {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)},
+            };
+            const double s0 = ld(scales, 3 * i), s1 = ld(scales, 3 * i + 1), s2 = ld(scales, 3 * i + 2);
+            const double sq[3] = {s0 * s0, s1 * s1, s2 * s2};
+            double mm[3][3], c[3][3], cov[3][3];
+#pragma unroll
+            for (int p = 0; p < 3; p++)
+#pragma unroll
+                for (int q = 0; q < 3; q++) mm[p][q] = r[p][q] * sq[q];
+#pragma unroll
+            for (int p = 0; p < 3; p++)
+#pragma unroll
+                for (int q = 0; q < 3; q++) c[p][q] = dot3_gemm(mm[p][0], mm[p][1], mm[p][2], r[q][0], r[q][1], r[q][2]);
+#pragma unroll
+            for (int p = 0; p < 3; p++)
+#pragma unroll
+                for (int q = 0; q < 3; q++) cov[p][q] = (c[p][q] + c[q][p]) / 2.0;
+            // sigma = (J W) Sigma (J W)^T  (src/tilesplat/projection.py:88-96)
+            double m[2][3], mc[2][3], sg[2][2];
+#pragma unroll
+            for (int p = 0; p < 2; p++)
+#pragma unroll
+                for (int q = 0; q < 3; q++) m[p][q] = dot3_gemm(jac[p][0], jac[p][1], jac[p][2], V[q], V[4 + q], V[8 + q]);
+#pragma unroll
+            for (int p = 0; p < 2; p++)
+#pragma unroll
+                for (int q = 0; q < 3; q++) mc[p][q] = dot3_gemm(m[p][0], m[p][1], m[p][2], cov[0][q], cov[1][q], cov[2][q]);
+#pragma unroll
+            for (int p = 0; p < 2; p++)
+#pragma unroll
+                for (int q = 0; q < 2; q++) sg[p][q] = dot3_gemm(mc[p][0], mc[p][1], mc[p][2], m[q][0], m[q][1], m[q][2]);
+            double sa = (sg[0][0] + sg[0][0]) / 2.0;
+            double sb = (sg[0][1] + sg[1][0]) / 2.0;
+            double sc = (sg[1][1] + sg[1][1]) / 2.0;
+            sa += 0.3;  // COV_DILATION, src/tilesplat/projection.py:14
+            sc += 0.3;
+            {  // _clamp_eigenvalues(sigma, 0.5), src/tilesplat/projection.py:45-65
+                const double mid = (sa + sc) / 2.0;
+                const double half = py_hypot((sa - sc) / 2.0, sb);
+                const double lo = mid - half, hi = mid + half;
+                if (!(lo >= 0.5)) {
+                    const double lo_c = lo > 0.5 ? lo : 0.5, hi_c = hi > 0.5 ? hi : 0.5;
+                    if (half == 0.0) {
+                        sa = lo_c;
+                        sb = 0.0;
+                        sc = lo_c;
+                    } else {
+                        double v0, v1;
+                        if (fabs(sb) > 1e-300) {
+                            v0 = sb;
+                            v1 = hi - sa;
+                        } else if (sa >= sc) {
+                            v0 = 1.0;
+                            v1 = 0.0;
+                        } else {
+                            v0 = 0.0;
+                            v1 = 1.0;
+                        }
+                        const double nrm = sqrt(fma(v1, v1, v0 * v0));
+                        v0 = v0 / nrm;
+                        v1 = v1 / nrm;
+                        const double u0 = -v1, u1 = v0;
+                        sa = hi_c * (v0 * v0) + lo_c * (u0 * u0);
+                        sb = hi_c * (v0 * v1) + lo_c * (u0 * u1);
+                        sc = hi_c * (v1 * v1) + lo_c * (u1 * u1);
+                    }
+                }
+            }
+            const double mid = (sa + sc) / 2.0;
+            const double lam_max = mid + py_hypot((sa - sc) / 2.0, sb);
+            const int32_t rad = (int32_t)ceil(3.0 * sqrt(lam_max));
+            const double det = sa * sc - sb * sb;
+            if (!(det > 0.0)) {  // invert_cov2 raises -> project returns None (projection.py:104-107)
+                dropped = true;
+            } else {
+                const double s11 = sc / det, s12 = -sb / det, s22 = sa / det;
+                a.radius[i] = rad;
+                if (a.debug) {
+                    a.dbg_conic[3 * i] = s11;
+                    a.dbg_conic[3 * i + 1] = s12;
+                    a.dbg_conic[3 * i + 2] = s22;
+                    a.dbg_depth[i] = tz;
+                }
+                // covered_tiles (src/tilesplat/tiling.py:34-43), clipped to the grid and the band
+                double fx0 = floor((mx - rad) / TILE), fx1 = floor((mx + rad) / TILE);
+                double fy0 = floor((my - rad) / TILE), fy1 = floor((my + rad) / TILE);
+                fx0 = fmax(fx0, 0.0);
+                fy0 = fmax(fy0, (double)a.band_y0);
+                fx1 = fmin(fx1, (double)(a.tiles_x - 1));
+                fy1 = fmin(fy1, (double)(a.band_y1 - 1));
+                if (fx0 <= fx1 && fy0 <= fy1) {
+                    const int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
+                    touched = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
+                    a.rect[i] = make_short4((short)x0, (short)y0, (short)x1, (short)y1);
+                    key = (unsigned long long)__double_as_longlong(tz);  // tz > 0: bit order == value order
+                    Rec rc;
+                    rc.mx = mx;
+                    rc.my = my;
+                    rc.s11 = (float)s11;
+                    rc.s12 = (float)s12;
+                    rc.s22 = (float)s22;
+                    const double o = ld(opac, i);
+                    rc.ln_o = (float)log(o);
+                    rc.opacity = (float)o;
+                    float col[3];
+                    if (a.sh_degree < 0) {
+                        col[0] = (float)ld(feats, 3 * i);
+                        col[1] = (float)ld(feats, 3 * i + 1);
+                        col[2] = (float)ld(feats, 3 * i + 2);
+                    } else {
+                        const int K = (a.sh_degree + 1) * (a.sh_degree + 1);
+                        const double dx = m0 - a.campos[0], dy = m1 - a.campos[1], dz = m2 - a.campos[2];
+                        const double nn = sqrt(dx * dx + dy * dy + dz * dz);
+                        sh_color(feats + (size_t)i * K * 3, a.sh_degree, dx / nn, dy / nn, dz / nn, col);
+                    }
+                    rc.r = col[0];
+                    rc.g = col[1];
+                    rc.b = col[2];
+                    a.rec[i] = rc;
+                }
+            }
+        }
+        a.touched[i] = touched;
+        a.keys[i] = key;
+        a.idx[i] = (uint32_t)i;
+    }
+    // warp-aggregated counters
+    const unsigned full = 0xffffffffu;
+    const unsigned n_drop = __popc(__ballot_sync(full, dropped));
+    const unsigned n_vis = __popc(__ballot_sync(full, touched > 0));
+    unsigned long long kmin = touched > 0 ? key : ~0ull, kmax = touched > 0 ? key : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long omin = __shfl_xor_sync(full, kmin, o), omax = __shfl_xor_sync(full, kmax, o);
+        kmin = omin < kmin ? omin : kmin;
+        kmax = omax > kmax ? omax : kmax;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (n_drop) atomicAdd(&a.ctr->dropped, (unsigned long long)n_drop);
+        if (n_vis) {
+            atomicAdd(&a.ctr->n_visible, (unsigned long long)n_vis);
+            atomicMin(&a.ctr->key_min, kmin);
+            atomicMax(&a.ctr->key_max, kmax);
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug,
+                              void *ws, const Layout &L, cudaStream_t st) {
+    PreArgs a;
+    a.cam = cam;
+    const double *V = cam.view;
+    // camera centre -R^T t (row-major view)
+    for (int k = 0; k < 3; k++) a.campos[k] = -(V[0 * 4 + k] * V[3] + V[1 * 4 + k] * V[7] + V[2 * 4 + k] * V[11]);
+    a.P = scene.P;
+    a.sh_degree = scene.sh_degree;
+    a.tiles_x = band.tiles_x;
+    a.tiles_y = band.tiles_y;
+    a.band_y0 = band.y0;
+    a.band_y1 = band.y1;
+    a.debug = debug;
+    a.rec = at<Rec>(ws, L.rec);
+    a.rect = at<short4>(ws, L.rect);
+    a.touched = at<uint32_t>(ws, L.touched);
+    a.keys = at<unsigned long long>(ws, L.key64[0]);
+    a.idx = at<uint32_t>(ws, L.idx[0]);
+    a.radius = at<int32_t>(ws, L.radius);
+    a.dbg_conic = at<double>(ws, L.dbg_conic);
+    a.dbg_depth = at<double>(ws, L.dbg_depth);
+    a.ctr = at<DevCounters>(ws, L.counters);
+    if (scene.P <= 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((scene.P + 255) / 256);
+    if (scene.dtype == TCGS_F64) {
+        preprocess_kernel<double><<<blocks, 256, 0, st>>>(
+            a, (const double *)scene.means, (const double *)scene.scales, (const double *)scene.rotations,
+            (const double *)scene.opacities, (const double *)scene.features);
+    } else {
+        preprocess_kernel<float><<<blocks, 256, 0, st>>>(
+            a, (const float *)scene.means, (const float *)scene.scales, (const float *)scene.rotations,
+            (const float *)scene.opacities, (const float *)scene.features);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace tcgs

@@ -1,0 +1,132 @@
+// tcgs_internal.cuh -- shared definitions of libtcgs.so (sm_100a only).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tcgs.h"
+
+namespace tcgs {
+
+constexpr int TILE = 16;              // src/tilesplat/tiling.py:11
+constexpr int RADIX_BITS = 8;
+constexpr int RADIX = 1 << RADIX_BITS;
+constexpr int SORT_BLOCKS = 296;      // 2 x 148 SMs: fixed grid, chunks sized from the device-side count
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_WARPS = SORT_THREADS / 32;
+constexpr int SORT_IPT = 16;          // items per thread per tile in the downsweep
+constexpr int SCAN_BLOCKS = 296;
+constexpr int SCAN_THREADS = 256;
+constexpr int MAX_PASSES = 8;         // depth key: <= 64 bits
+constexpr int TILE_PASS_SLOT = 8;     // pass bookkeeping slots 8.. are the tile-key passes
+
+constexpr int K7_THREADS = 256;       // one pixel per thread, 16x16 tile
+constexpr int K7_BATCH = 64;          // Gaussians per tcgen05 batch (MMA N)
+constexpr int K7_TMEM_COLS = 256;     // 2 buffers x 2 pixel halves x 64 columns
+constexpr int K7_CTAS_PER_SM = 2;
+
+// Per-Gaussian record consumed by the blend kernel (48 B, three 16 B loads).
+struct __align__(16) Rec {
+    double mx, my;             // float64 mean2d (src/tilesplat/projection.py:80-82)
+    float s11, s12, s22, ln_o; // conic (rounded from float64) and log opacity
+    float r, g, b, opacity;    // colour (SH evaluated) and opacity
+};
+
+// Device-side counters and sort bookkeeping (zeroed at the start of each frame).
+struct DevCounters {
+    unsigned long long dropped, n_visible, n_splats, overflow;
+    unsigned long long f_blend, f_cull, pixels_terminated, pairs;
+    unsigned long long key_min, key_max, key_range;
+    unsigned int tile_queue;
+    int depth_cur, tile_cur;
+    int pass_in[16];
+    int pass_do[16];
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+    size_t counters, rec, rect, touched, key64[2], idx[2], radius, dbg_conic, dbg_depth;
+    size_t hist, blocksum, tkey[2], tval[2], ranges, total;
+    static Layout make(int64_t P, int W, int H, int64_t cap) {
+        Layout L;
+        size_t o = 0;
+        size_t Pn = (size_t)(P > 0 ? P : 1), cn = (size_t)(cap > 0 ? cap : 1);
+        size_t nt = (size_t)((W + TILE - 1) / TILE) * (size_t)((H + TILE - 1) / TILE);
+        auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+        L.counters = take(sizeof(DevCounters));
+        L.rec = take(sizeof(Rec) * Pn);
+        L.rect = take(sizeof(short4) * Pn);
+        L.touched = take(sizeof(uint32_t) * Pn);
+        L.key64[0] = take(sizeof(uint64_t) * Pn);
+        L.key64[1] = take(sizeof(uint64_t) * Pn);
+        L.idx[0] = take(sizeof(uint32_t) * Pn);
+        L.idx[1] = take(sizeof(uint32_t) * Pn);
+        L.radius = take(sizeof(int32_t) * Pn);
+        L.dbg_conic = take(sizeof(double) * 3 * Pn);
+        L.dbg_depth = take(sizeof(double) * Pn);
+        L.hist = take(sizeof(uint32_t) * RADIX * SORT_BLOCKS);
+        L.blocksum = take(sizeof(unsigned long long) * SCAN_BLOCKS);
+        L.tkey[0] = take(sizeof(uint32_t) * cn);
+        L.tkey[1] = take(sizeof(uint32_t) * cn);
+        L.tval[0] = take(sizeof(uint32_t) * cn);
+        L.tval[1] = take(sizeof(uint32_t) * cn);
+        L.ranges = take(sizeof(uint2) * (nt ? nt : 1));
+        L.total = o;
+        return L;
+    }
+};
+
+template <typename T>
+inline T *at(void *ws, size_t off) { return reinterpret_cast<T *>(static_cast<char *>(ws) + off); }
+template <typename T>
+inline const T *at(const void *ws, size_t off) { return reinterpret_cast<const T *>(static_cast<const char *>(ws) + off); }
+
+struct Band {
+    int tiles_x, tiles_y, y0, y1;  // tile rows [y0, y1)
+    int n_tiles() const { return tiles_x * (y1 - y0); }
+};
+
+inline Band make_band(const tcgs_camera &cam, const tcgs_opts *o) {
+    Band b;
+    b.tiles_x = (cam.width + TILE - 1) / TILE;
+    b.tiles_y = (cam.height + TILE - 1) / TILE;
+    b.y0 = 0;
+    b.y1 = b.tiles_y;
+    if (o && o->tile_row_end > 0) {
+        b.y0 = o->tile_row_begin < 0 ? 0 : o->tile_row_begin;
+        b.y1 = o->tile_row_end > b.tiles_y ? b.tiles_y : o->tile_row_end;
+    }
+    return b;
+}
+
+// ------------------------------------------------------------------ launchers
+cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug,
+                              void *ws, const Layout &L, cudaStream_t st);
+cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st);
+cudaError_t launch_render(int alpha_mode, const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
+                          void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st);
+cudaError_t launch_pack_lists(int64_t P, const double *mean2d, const double *conic, const double *opacity,
+                              const float *colors, const int64_t *offsets, const Band &band, void *ws,
+                              const Layout &L, cudaStream_t st);
+int tile_key_bits(const Band &band);
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+}  // namespace tcgs

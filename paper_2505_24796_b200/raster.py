@@ -1,0 +1,448 @@
+"""Host side of the B200 TC-GS renderer: the reference's render entry point,
+re-implemented over libtcgs.so.
+
+Mirrors tilesplat.raster (/root/reference/pkg/src/tilesplat/raster.py):
+``render(scene, cam, backend) -> (ImageBuffer, FragmentStats)`` (:161-201),
+``make_backend`` (:149-158), ``FragmentStats`` (:19-49), ``ImageBuffer``
+(:52-64), ``computation_model`` (:204-208) and the module constants
+(:15-16).  Scenes and cameras are duck-typed against tilesplat.scene
+(Scene/Gaussian3D/Camera, src/tilesplat/scene.py:24-80), so the reference's own
+objects are accepted unchanged.
+
+There is exactly one implementation behind it (sm_100a CUDA through the C
+ABI); the backend string only selects a compile-time alpha mode of the same
+blend kernel.  Nothing here computes pixels on the CPU.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _abi
+
+ALPHA_CULL_THRESHOLD = 1.0 / 255.0  # src/tilesplat/raster.py:15
+TERMINATION_THRESHOLD = 0.0001      # src/tilesplat/raster.py:16
+TILE_SIZE = 16                      # src/tilesplat/tiling.py:11
+
+
+@dataclass
+class FragmentStats:
+    """Counts of blended, culled, and skipped fragments plus exp calls (src/tilesplat/raster.py:19-49)."""
+
+    f_blend: int = 0
+    f_cull: int = 0
+    f_skip: int = 0
+    exp_calls: int = 0
+    n_splats: int = 0
+    dropped: int = 0
+    pixels_terminated: int = 0
+    stage_ms: dict = field(default_factory=dict)
+    n_visible: int = 0
+
+    @property
+    def total_fragments(self) -> int:
+        return self.f_blend + self.f_cull + self.f_skip
+
+    def counts(self) -> tuple[int, int, int, int]:
+        return (self.f_blend, self.f_cull, self.f_skip, self.exp_calls)
+
+    def to_dict(self) -> dict:
+        return {
+            "f_blend": self.f_blend,
+            "f_cull": self.f_cull,
+            "f_skip": self.f_skip,
+            "exp_calls": self.exp_calls,
+            "N": self.n_splats,
+            "dropped": self.dropped,
+            "pixels_terminated": self.pixels_terminated,
+            "stage_ms": dict(self.stage_ms),
+        }
+
+
+@dataclass
+class ImageBuffer:
+    """Row-major float RGB image in [0, 1] (src/tilesplat/raster.py:52-64), plus the final
+    transmittance ``T`` and per-pixel contributor counts ``n_contrib``."""
+
+    rgb: np.ndarray  # (height, width, 3) float64
+    T: np.ndarray | None = None
+    n_contrib: np.ndarray | None = None
+
+    @property
+    def width(self) -> int:
+        return self.rgb.shape[1]
+
+    @property
+    def height(self) -> int:
+        return self.rgb.shape[0]
+
+
+@dataclass(frozen=True)
+class Backend:
+    """Selects the alpha mode of the single B200 blend kernel."""
+
+    name: str
+    alpha_mode: int
+    early_cull: bool = True
+
+    def tile_evaluator(self, *a, **k):  # the per-fragment protocol (raster.py:86-107) is not crossed
+        raise NotImplementedError("the B200 renderer blends whole tiles on the GPU; use render()")
+
+
+_SPECS = {
+    # spec: (alpha mode, EarlyCull accounting)
+    "tcgs": (_abi.ALPHA_TC_HILO, True),
+    "tcgs-hilo": (_abi.ALPHA_TC_HILO, True),
+    "tcgs-fp16": (_abi.ALPHA_TC_K8, True),
+    "tcgs-k8": (_abi.ALPHA_TC_K8, True),
+    "tcgs-ffma": (_abi.ALPHA_FFMA, True),
+    # reference spellings (src/tilesplat/raster.py:149-158, src/tilesplat/cli.py:15)
+    "reference": (_abi.ALPHA_FFMA, False),
+    "frag2mat": (_abi.ALPHA_TC_HILO, True),
+    "frag2mat-fp16": (_abi.ALPHA_TC_K8, True),
+}
+
+
+def make_backend(spec: str = "tcgs", coords: str = "local", batch_width: int = 64,
+                 use_early_cull: bool = True) -> Backend:
+    """Backend factory mirroring src/tilesplat/raster.py:149-158 (ValueError on unknown specs)."""
+    if spec not in _SPECS:
+        raise ValueError(f"unknown backend {spec!r}")
+    if coords != "local":
+        raise ValueError(f"coordinate mode {coords!r}: the B200 kernel evaluates in tile-local coordinates only")
+    if batch_width < 1:
+        raise ValueError("batch width must be positive")
+    mode, early = _SPECS[spec]
+    return Backend(spec, mode, early and use_early_cull)
+
+
+def computation_model(stats: FragmentStats, k_alpha: float, k_cull: float, k_blend: float) -> float:
+    """Fragment-cost model (src/tilesplat/raster.py:204-208)."""
+    if k_alpha < 0 or k_cull < 0 or k_blend < 0:
+        raise ValueError("cost constants must be non-negative")
+    return k_blend * stats.f_blend + (k_cull + k_alpha) * (stats.f_blend + stats.f_cull)
+
+
+# ----------------------------------------------------------------------------- scene / camera packing
+
+@dataclass
+class GaussianCloud:
+    """Device-resident SoA Gaussians (the layout libtcgs.so consumes).
+
+    ``features`` is RGB [P,3] when ``sh_degree == -1`` (the reference's
+    Gaussian3D.color) or SH coefficients [P,(d+1)^2,3] for degree d.
+    """
+
+    means: torch.Tensor
+    scales: torch.Tensor
+    rotations: torch.Tensor
+    opacities: torch.Tensor
+    features: torch.Tensor
+    sh_degree: int = -1
+
+    @property
+    def P(self) -> int:
+        return int(self.means.shape[0])
+
+    @property
+    def dtype_code(self) -> int:
+        return _abi.F64 if self.means.dtype == torch.float64 else _abi.F32
+
+    @classmethod
+    def from_arrays(cls, d: dict, device=None, dtype=None) -> "GaussianCloud":
+        """From a dict of arrays (paper_2505_24796_b200.synthetic scenes)."""
+        device = torch.device(device or "cuda")
+        sh = int(d.get("sh_degree", 0))
+        feats = d["features"] if (sh > 0 and "features" in d) else d["colors"]
+        sh_code = sh if (sh > 0 and "features" in d) else -1
+        if dtype is None:
+            dtype = torch.float64 if np.asarray(d["means"]).dtype == np.float64 else torch.float32
+
+        def t(x):
+            return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype).to(device).contiguous()
+
+        return cls(t(d["means"]), t(d["scales"]), t(d["rotations"]), t(np.asarray(d["opacities"]).reshape(-1)),
+                   t(feats), sh_code)
+
+    @classmethod
+    def from_scene(cls, scene, device=None) -> "GaussianCloud":
+        """From a reference ``tilesplat.Scene`` (float64, colours used directly)."""
+        g = tuple(scene.gaussians)
+        if len(g) == 0:
+            z = np.zeros((0, 3))
+            return cls.from_arrays({"means": z, "scales": z, "rotations": np.zeros((0, 4)),
+                                    "opacities": np.zeros(0), "colors": z}, device, torch.float64)
+        arr = {
+            "means": np.array([x.mean for x in g], np.float64),
+            "scales": np.array([x.scale for x in g], np.float64),
+            "rotations": np.array([x.rotation for x in g], np.float64),
+            "opacities": np.array([x.opacity for x in g], np.float64),
+            "colors": np.array([x.color for x in g], np.float64),
+        }
+        return cls.from_arrays(arr, device, torch.float64)
+
+    def _c(self) -> _abi.Scene:
+        s = _abi.Scene()
+        s.P = self.P
+        s.sh_degree = self.sh_degree
+        s.dtype = self.dtype_code
+        for name in ("means", "scales", "rotations", "opacities", "features"):
+            t = getattr(self, name)
+            if not t.is_contiguous():
+                raise ValueError(f"{name} must be contiguous")
+            if t.dtype != self.means.dtype:
+                raise ValueError("all Gaussian arrays must share one dtype")
+            setattr(s, name, t.data_ptr() if t.numel() else 0)
+        return s
+
+
+def camera_struct(cam) -> _abi.Camera:
+    """Pack a tilesplat.Camera-like object (src/tilesplat/scene.py:50-68)."""
+    c = _abi.Camera()
+    v = np.asarray(cam.view, dtype=np.float64).reshape(16)
+    for i in range(16):
+        c.view[i] = float(v[i])
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    c.near_plane = float(getattr(cam, "near", 0.2))
+    c.width, c.height = int(cam.width), int(cam.height)
+    if c.width <= 0 or c.height <= 0:
+        raise ValueError("image dimensions must be positive")
+    if not (c.fx > 0 and c.fy > 0):
+        raise ValueError("focal lengths must be positive")
+    if not c.near_plane > 0:
+        raise ValueError("near clip must be positive")
+    return c
+
+
+# ----------------------------------------------------------------------------- the renderer
+
+@dataclass
+class Frame:
+    rgb: torch.Tensor        # [H,W,3] f32 (device)
+    T: torch.Tensor          # [H,W]   f32 (device)
+    n_contrib: torch.Tensor  # [H,W]   i32 (device)
+    stats: FragmentStats | None
+
+
+class Renderer:
+    """Owns the device workspace and the output buffers; renders frames stream-ordered.
+
+    The library allocates nothing: the workspace is a torch uint8 tensor sized by
+    tcgs_workspace_size and grown (with one re-render) when a frame overflows
+    the splat capacity.
+    """
+
+    def __init__(self, device=None, backend="tcgs", max_splats: int | None = None):
+        self.lib = _abi.load()
+        self.device = torch.device(device or "cuda")
+        if self.device.type != "cuda":
+            raise ValueError("the B200 renderer needs a CUDA device")
+        with torch.cuda.device(self.device):
+            _abi.check(self.lib.tcgs_device_check(), "device check")
+        self.backend = backend if isinstance(backend, Backend) else make_backend(backend)
+        self.max_splats = max_splats
+        self.ws = None
+        self.ws_key = None
+        self._out = {}
+
+    def _opts(self, band=None, debug=False) -> _abi.Opts:
+        o = _abi.Opts()
+        o.tile_row_begin, o.tile_row_end = (band if band is not None else (0, 0))
+        o.alpha_mode = self.backend.alpha_mode
+        o.early_cull = 1 if self.backend.early_cull else 0
+        o.debug = 1 if debug else 0
+        return o
+
+    def workspace(self, P: int, W: int, H: int, cap: int) -> torch.Tensor:
+        need = int(self.lib.tcgs_workspace_size(P, W, H, cap))
+        if self.ws is None or self.ws.numel() < need:
+            self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        self.ws_key = (P, W, H, cap)
+        return self.ws
+
+    def outputs(self, W: int, H: int):
+        key = (W, H)
+        if key not in self._out:
+            self._out[key] = (torch.zeros((H, W, 3), dtype=torch.float32, device=self.device),
+                              torch.ones((H, W), dtype=torch.float32, device=self.device),
+                              torch.zeros((H, W), dtype=torch.int32, device=self.device))
+        return self._out[key]
+
+    def capacity(self, P: int) -> int:
+        if self.max_splats is None:
+            self.max_splats = max(1 << 16, 16 * P)
+        return self.max_splats
+
+    def launch(self, cloud: GaussianCloud, cam, band=None, debug=False, outputs=None, timers=None):
+        """Enqueue K1..K7 on the current stream (no host synchronisation)."""
+        c = camera_struct(cam)
+        cap = self.capacity(cloud.P)
+        ws = self.workspace(cloud.P, c.width, c.height, cap)
+        rgb, T, cnt = outputs if outputs is not None else self.outputs(c.width, c.height)
+        o = self._opts(band, debug)
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        s = cloud._c()
+        lib = self.lib
+        ev = timers
+        if ev:
+            ev[0].record()
+        _abi.check(lib.tcgs_preprocess(s, c, o, ws.data_ptr(), ws.numel(), cap, st), "tcgs_preprocess")
+        if ev:
+            ev[1].record()
+        _abi.check(lib.tcgs_bin(cloud.P, c, o, ws.data_ptr(), ws.numel(), cap, st), "tcgs_bin")
+        if ev:
+            ev[2].record()
+        _abi.check(lib.tcgs_blend(cloud.P, c, o, ws.data_ptr(), ws.numel(), cap, rgb.data_ptr(), T.data_ptr(),
+                                  cnt.data_ptr(), st), "tcgs_blend")
+        if ev:
+            ev[3].record()
+        return rgb, T, cnt
+
+    def read_stats(self, P: int, band=None) -> tuple[int, FragmentStats]:
+        st_ = _abi.Stats()
+        o = self._opts(band)
+        rc = self.lib.tcgs_read_stats(self.ws.data_ptr(), P, o, st_, torch.cuda.current_stream(self.device).cuda_stream)
+        fs = FragmentStats(f_blend=st_.f_blend, f_cull=st_.f_cull, f_skip=st_.f_skip, exp_calls=st_.exp_calls,
+                           n_splats=st_.n_splats, dropped=st_.dropped, pixels_terminated=st_.pixels_terminated,
+                           n_visible=st_.n_visible)
+        return rc, fs
+
+    def render_frame(self, cloud: GaussianCloud, cam, band=None, debug=False, timed=True) -> Frame:
+        with torch.cuda.device(self.device):
+            for _attempt in range(3):
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timed else None
+                rgb, T, cnt = self.launch(cloud, cam, band, debug, timers=ev)
+                rc, fs = self.read_stats(cloud.P, band)
+                if rc == _abi.TCGS_ERR_CAPACITY:
+                    self.max_splats = int(fs.n_splats * 1.25) + 1024
+                    continue
+                _abi.check(rc, "tcgs_read_stats")
+                if ev:
+                    fs.stage_ms = {"preprocess": ev[0].elapsed_time(ev[1]), "sorting": ev[1].elapsed_time(ev[2]),
+                                   "blending": ev[2].elapsed_time(ev[3])}
+                return Frame(rgb, T, cnt, fs)
+        raise RuntimeError("splat capacity could not be satisfied")
+
+    # -- debug accessors (tests) ------------------------------------------------------------
+    def tile_lists(self, P: int, cam, band=None):
+        """(offsets int64 [n_tiles+1], ids int32 [N]) of the last frame, as numpy (CSR, row-major tiles)."""
+        c = camera_struct(cam)
+        o = self._opts(band)
+        rc, fs = self.read_stats(P, band)
+        _abi.check(rc, "tcgs_read_stats")
+        n = fs.n_splats
+        ids = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        ty0, ty1 = band if band is not None else (0, (c.height + 15) // 16)
+        nt = ((c.width + 15) // 16) * (ty1 - ty0)
+        ranges = torch.empty((max(nt, 1), 2), dtype=torch.int32, device=self.device)
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        _abi.check(self.lib.tcgs_copy_lists(self.ws.data_ptr(), P, c, o, self.max_splats, ids.data_ptr(),
+                                            ranges.data_ptr(), st), "tcgs_copy_lists")
+        r = ranges[:nt].cpu().numpy().astype(np.int64)
+        counts = np.where(r[:, 1] > r[:, 0], r[:, 1] - r[:, 0], 0)
+        offsets = np.zeros(nt + 1, np.int64)
+        np.cumsum(counts, out=offsets[1:])
+        ids_np = ids[:n].cpu().numpy()
+        # ranges are contiguous and ordered, so CSR offsets index ids directly
+        assert all(r[t, 0] == offsets[t] for t in range(nt) if counts[t] > 0)
+        return offsets, ids_np
+
+    def projection(self, P: int, cam):
+        c = camera_struct(cam)
+        d = self.device
+        vis = torch.empty(max(P, 1), dtype=torch.uint8, device=d)
+        m2 = torch.empty((max(P, 1), 2), dtype=torch.float64, device=d)
+        con = torch.empty((max(P, 1), 3), dtype=torch.float64, device=d)
+        dep = torch.empty(max(P, 1), dtype=torch.float64, device=d)
+        rad = torch.empty(max(P, 1), dtype=torch.int32, device=d)
+        rgb = torch.empty((max(P, 1), 3), dtype=torch.float32, device=d)
+        st = torch.cuda.current_stream(d).cuda_stream
+        _abi.check(self.lib.tcgs_copy_projection(self.ws.data_ptr(), P, c, self.max_splats, vis.data_ptr(),
+                                                 m2.data_ptr(), con.data_ptr(), dep.data_ptr(), rad.data_ptr(),
+                                                 rgb.data_ptr(), st), "tcgs_copy_projection")
+        torch.cuda.synchronize(d)
+        return {k: v[:P].cpu().numpy() for k, v in
+                dict(visible=vis, mean2d=m2, inv_cov=con, depth=dep, radius=rad, rgb=rgb).items()}
+
+    def blend_lists(self, mean2d, conic, opacity, colors, offsets, ids, cam, band=None):
+        """K7 alone on caller-given projected records and CSR tile lists (tests/KATs)."""
+        d = self.device
+        c = camera_struct(cam)
+        P = int(np.asarray(mean2d).reshape(-1, 2).shape[0])
+
+        def t(x, dt):
+            return torch.as_tensor(np.ascontiguousarray(x), dtype=dt, device=d).contiguous()
+
+        m2 = t(np.asarray(mean2d, np.float64).reshape(-1, 2), torch.float64)
+        con = t(np.asarray(conic, np.float64).reshape(-1, 3), torch.float64)
+        op = t(np.asarray(opacity, np.float64).reshape(-1), torch.float64)
+        col = t(np.asarray(colors, np.float32).reshape(-1, 3), torch.float32)
+        off = t(np.asarray(offsets, np.int64), torch.int64)
+        idt = t(np.asarray(ids, np.int32).reshape(-1) if np.size(ids) else np.zeros(1, np.int32), torch.int32)
+        ws = self.workspace(P, c.width, c.height, 1)
+        rgb = torch.zeros((c.height, c.width, 3), dtype=torch.float32, device=d)
+        T = torch.ones((c.height, c.width), dtype=torch.float32, device=d)
+        cnt = torch.zeros((c.height, c.width), dtype=torch.int32, device=d)
+        o = self._opts(band)
+        st = torch.cuda.current_stream(d).cuda_stream
+        with torch.cuda.device(d):
+            _abi.check(self.lib.tcgs_blend_lists(P, m2.data_ptr(), con.data_ptr(), op.data_ptr(), col.data_ptr(),
+                                                 off.data_ptr(), idt.data_ptr(), c, o, ws.data_ptr(), ws.numel(),
+                                                 rgb.data_ptr(), T.data_ptr(), cnt.data_ptr(), st), "tcgs_blend_lists")
+            rc, fs = self.read_stats(P, band)
+            _abi.check(rc, "tcgs_read_stats")
+        return Frame(rgb, T, cnt, fs)
+
+
+_DEFAULT = {}
+
+
+def _renderer(device, backend) -> Renderer:
+    key = (str(device), backend.name if isinstance(backend, Backend) else backend)
+    if key not in _DEFAULT:
+        _DEFAULT[key] = Renderer(device, backend)
+    return _DEFAULT[key]
+
+
+def render(scene, cam, backend="tcgs", device=None) -> tuple[ImageBuffer, FragmentStats]:
+    """Drop-in for ``tilesplat.render(scene, cam, backend)`` (src/tilesplat/raster.py:161-201).
+
+    ``scene`` is a reference ``Scene`` (or a ``GaussianCloud``); background is
+    black; boundary tiles are full 16x16 tiles with out-of-image pixels masked.
+    Returns float64 RGB like the reference plus ``T``/``n_contrib`` extras.
+    """
+    if isinstance(backend, str):
+        backend = make_backend(backend)
+    device = torch.device(device or "cuda")
+    t0 = time.perf_counter()
+    cloud = scene if isinstance(scene, GaussianCloud) else GaussianCloud.from_scene(scene, device)
+    r = _renderer(device, backend)
+    frame = r.render_frame(cloud, cam)
+    img = ImageBuffer(frame.rgb.double().cpu().numpy(), frame.T.double().cpu().numpy(),
+                      frame.n_contrib.cpu().numpy())
+    frame.stats.stage_ms["total_wall"] = (time.perf_counter() - t0) * 1e3
+    return img, frame.stats
+
+
+def rasterize(means, scales, rotations, opacities, features, sh_degree: int, cameras, backend="tcgs",
+              band=None, renderer: Renderer | None = None) -> dict:
+    """Batched entry: render every camera of ``cameras`` from device tensors.
+
+    Returns ``rgb [V,H,W,3] f32``, ``T [V,H,W] f32``, ``n_contrib [V,H,W] i32``
+    (device tensors) and per-view FragmentStats.
+    """
+    cloud = GaussianCloud(means.contiguous(), scales.contiguous(), rotations.contiguous(),
+                          opacities.reshape(-1).contiguous(), features.contiguous(), int(sh_degree))
+    r = renderer or Renderer(means.device, backend)
+    out_rgb, out_T, out_n, stats = [], [], [], []
+    for cam in cameras:
+        f = r.render_frame(cloud, cam, band=band)
+        out_rgb.append(f.rgb.clone())
+        out_T.append(f.T.clone())
+        out_n.append(f.n_contrib.clone())
+        stats.append(f.stats)
+    return {"rgb": torch.stack(out_rgb), "T": torch.stack(out_T), "n_contrib": torch.stack(out_n), "stats": stats}

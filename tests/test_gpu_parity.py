@@ -1,0 +1,277 @@
+"""GPU parity: libtcgs.so (through the C ABI) against the reference's outputs.
+
+Bar (BASELINE.json north_star):
+  * tile keys, sorted order and per-tile ranges: bit-exact;
+  * RGB and final transmittance: max abs error <= 2/255 and PSNR >= 45 dB;
+  * per-pixel contributor counts: identical except where alpha lies within
+    fp16 error of the cutoff (explained pixel by pixel, tests/parity_util.py).
+The reference side is the golden fixtures the reference itself produced
+(tests/golden/make_golden.py) and, for sizes without fixtures, the CPU
+oracle (oracle/, pinned to those fixtures by test_oracle_golden.py).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from conftest import GoldenCam, load_golden, GOLDEN_NAMES  # noqa: E402
+from parity_util import explain_count_mismatches, psnr  # noqa: E402
+
+import paper_2505_24796_b200 as tcgs  # noqa: E402
+from paper_2505_24796_b200 import synthetic  # noqa: E402
+
+RGB_TOL = 2.0 / 255.0
+PSNR_MIN = 45.0
+MODES = {"tcgs": "hilo", "tcgs-fp16": "k8", "tcgs-ffma": "ffma"}
+
+
+@pytest.fixture(scope="module")
+def renderers():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return {spec: tcgs.Renderer("cuda", spec) for spec in MODES}
+
+
+def cloud_of(g):
+    d = {k: g[k] for k in ("means", "scales", "rotations", "opacities", "colors")}
+    return tcgs.GaussianCloud.from_arrays(d, "cuda")
+
+
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+def test_projection_bit_exact(renderers, name):
+    g = load_golden(name)
+    cam = GoldenCam(g)
+    r = renderers["tcgs"]
+    cloud = cloud_of(g)
+    f = r.render_frame(cloud, cam, debug=True)
+    pr = r.projection(cloud.P, cam)
+    surv = np.nonzero(pr["visible"])[0]
+    assert np.array_equal(surv, g["surv"])
+    assert f.stats.dropped == int(g["stats"][5])
+    # src/tilesplat/projection.py:68-116 -- the float64 preprocess reproduces numpy/OpenBLAS bit for bit
+    assert np.array_equal(pr["radius"][surv], g["radius"])
+    assert np.array_equal(pr["mean2d"][surv], g["mean2d"])
+    assert np.array_equal(pr["depth"][surv], g["depth"])
+    assert np.array_equal(pr["inv_cov"][surv], g["inv_cov"])
+
+
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+def test_tile_lists_bit_exact(renderers, name):
+    g = load_golden(name)
+    cam = GoldenCam(g)
+    r = renderers["tcgs"]
+    cloud = cloud_of(g)
+    f = r.render_frame(cloud, cam)
+    assert f.stats.n_splats == int(g["stats"][4])
+    offsets, ids = r.tile_lists(cloud.P, cam)
+    assert np.array_equal(offsets, g["offsets"])  # per-tile ranges
+    assert np.array_equal(ids, g["ids"])          # keys + depth order, ties by index
+
+
+def _check_frame(name, g, rgb, T, cnt, stats, mode):
+    ref_rgb, ref_T, ref_cnt = g["rgb"], g["T"], g["counts"]
+    d_rgb = float(np.max(np.abs(rgb - ref_rgb))) if rgb.size else 0.0
+    d_T = float(np.max(np.abs(T - ref_T))) if T.size else 0.0
+    assert d_rgb <= RGB_TOL, (name, d_rgb * 255)
+    assert d_T <= RGB_TOL, (name, d_T * 255)
+    assert psnr(rgb, ref_rgb) >= PSNR_MIN, name
+    assert psnr(T, ref_T) >= PSNR_MIN, name
+    proj_m2 = np.zeros((g["means"].shape[0], 2))
+    proj_ic = np.zeros((g["means"].shape[0], 3))
+    proj_m2[g["surv"]] = g["mean2d"]
+    proj_ic[g["surv"]] = g["inv_cov"]
+    n_mis, unexplained = explain_count_mismatches(cnt, ref_cnt, g["offsets"], g["ids"], proj_m2, proj_ic,
+                                                  np.asarray(g["opacities"], np.float64), int(g["size"][0]), mode)
+    assert not unexplained, (name, n_mis, unexplained[:5])
+    # fragment accounting closure: every in-image (pixel, splat) pair is blend, cull or skip
+    st = g["stats"]
+    total_ref = int(st[0] + st[1] + st[2])
+    assert stats.f_blend + stats.f_cull + stats.f_skip == total_ref
+    assert int(cnt.sum()) == stats.f_blend
+    if n_mis == 0:
+        assert (stats.f_blend, stats.f_cull, stats.f_skip) == tuple(int(x) for x in st[:3])
+        assert stats.pixels_terminated == int(st[6])
+    return n_mis
+
+
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+@pytest.mark.parametrize("spec", list(MODES))
+def test_blend_lists_against_reference(renderers, name, spec):
+    """K7 alone, fed the reference's own projection records and tile lists."""
+    g = load_golden(name)
+    cam = GoldenCam(g)
+    P = g["means"].shape[0]
+    m2 = np.zeros((P, 2))
+    ic = np.zeros((P, 3))
+    m2[g["surv"]] = g["mean2d"]
+    ic[g["surv"]] = g["inv_cov"]
+    f = renderers[spec].blend_lists(m2, ic, g["opacities"], g["colors"], g["offsets"], g["ids"], cam)
+    _check_frame(name, g, f.rgb.double().cpu().numpy(), f.T.double().cpu().numpy(), f.n_contrib.cpu().numpy(),
+                 f.stats, MODES[spec])
+
+
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+@pytest.mark.parametrize("spec", list(MODES))
+def test_full_render_against_reference(renderers, name, spec):
+    """K1..K7 end to end through the C ABI."""
+    g = load_golden(name)
+    cam = GoldenCam(g)
+    f = renderers[spec].render_frame(cloud_of(g), cam)
+    _check_frame(name, g, f.rgb.double().cpu().numpy(), f.T.double().cpu().numpy(), f.n_contrib.cpu().numpy(),
+                 f.stats, MODES[spec])
+    assert f.stats.n_splats == int(g["stats"][4])
+    if spec != "tcgs-ffma":  # EarlyCull accounting (src/tilesplat/tensor_path.py:148-154)
+        assert f.stats.exp_calls == f.stats.f_blend + f.stats.pixels_terminated
+
+
+def test_reference_backend_accounting(renderers):
+    g = load_golden("c1")
+    img, st = tcgs.render(_RefScene(g), GoldenCam(g), backend="reference")
+    assert st.exp_calls == st.f_blend + st.f_cull + st.pixels_terminated
+    assert st.to_dict()["N"] == int(g["stats"][4])
+    assert set(st.stage_ms) >= {"preprocess", "sorting", "blending"}
+    assert float(np.max(np.abs(img.rgb - g["rgb"]))) <= RGB_TOL
+
+
+class _G:
+    def __init__(self, mean, scale, rotation, opacity, color):
+        self.mean, self.scale, self.rotation, self.opacity, self.color = mean, scale, rotation, opacity, color
+
+
+class _RefScene:
+    """Duck-typed tilesplat.Scene built from a fixture."""
+
+    def __init__(self, g):
+        self.gaussians = tuple(_G(g["means"][i], g["scales"][i], g["rotations"][i], float(g["opacities"][i]),
+                                  g["colors"][i]) for i in range(g["means"].shape[0]))
+
+
+# ---- blend KATs (tests/test_raster.py:37-80 of the reference) through K7 -------------------------
+
+def _const_alpha_tile(renderers, alphas, colors, spec="tcgs"):
+    """One 16x16 tile; splat j has zero conic so alpha_j = opacity_j at every pixel."""
+    n = len(alphas)
+    cam = synthetic.make_camera(16, 16)
+    f = renderers[spec].blend_lists(np.full((n, 2), 8.0), np.zeros((n, 3)), np.asarray(alphas, np.float64),
+                                    np.asarray(colors, np.float64), np.array([0, n]), np.arange(n), cam)
+    return f.rgb.double().cpu().numpy().reshape(256, 3), f.T.double().cpu().numpy().reshape(256), f.stats
+
+
+@pytest.mark.parametrize("spec", list(MODES))
+def test_kat_two_half_alpha_splats(renderers, spec):
+    c, t, st = _const_alpha_tile(renderers, [0.5, 0.5], [[1, 0, 0], [0, 1, 0]], spec)
+    assert np.allclose(c, [0.5, 0.25, 0.0], atol=2e-6) and np.allclose(t, 0.25, atol=2e-6)
+    assert st.f_blend == 512 and st.f_cull == 0 and st.f_skip == 0
+
+
+@pytest.mark.parametrize("spec", list(MODES))
+def test_kat_culls_tiny_alpha(renderers, spec):
+    c, t, st = _const_alpha_tile(renderers, [1.0 / 512.0], [[1, 1, 1]], spec)
+    assert np.all(c == 0.0) and np.all(t == 1.0) and st.f_cull == 256 and st.f_blend == 0
+
+
+@pytest.mark.parametrize("spec", list(MODES))
+def test_kat_opaque_terminates_before_compositing(renderers, spec):
+    c, t, st = _const_alpha_tile(renderers, [1.0, 0.5], np.ones((2, 3)), spec)
+    assert np.all(c == 0.0) and np.all(t == 1.0)
+    assert st.pixels_terminated == 256 and st.f_blend == 0 and st.f_skip == 512
+
+
+@pytest.mark.parametrize("spec", list(MODES))
+def test_kat_skip_accounting(renderers, spec):
+    c, t, st = _const_alpha_tile(renderers, [0.5, 1.0, 0.5], np.ones((3, 3)), spec)
+    assert st.f_blend == 256 and st.pixels_terminated == 256 and st.f_skip == 512
+    assert st.total_fragments == 3 * 256
+
+
+def test_long_lists_cross_batches(renderers):
+    """200 splats in one tile (several 64-wide batches): batch boundaries must not change the result."""
+    rng = np.random.default_rng(3)
+    n = 200
+    alphas = rng.uniform(0.001, 0.05, n)
+    cols = rng.uniform(0, 1, (n, 3))
+    c, t, st = _const_alpha_tile(renderers, alphas, cols)
+    rc, rt, _, (fb, fc, fs, pt) = oracle.blend_const_alpha(alphas, cols)
+    assert np.max(np.abs(c - rc)) <= 1e-5 and np.max(np.abs(t - rt)) <= 1e-5
+    assert (st.f_blend, st.f_cull, st.f_skip) == (fb, fc, fs)
+
+
+# ---- edge cases ------------------------------------------------------------------------------
+
+def test_empty_scene_renders_black(renderers):
+    cam = synthetic.make_camera(48, 48)
+    z = np.zeros((0, 3))
+    d = {"means": z, "scales": z, "rotations": np.zeros((0, 4)), "opacities": np.zeros(0), "colors": z}
+    f = renderers["tcgs"].render_frame(tcgs.GaussianCloud.from_arrays(d, "cuda"), cam)
+    assert float(f.rgb.abs().max()) == 0.0 and float(f.T.min()) == 1.0
+    assert f.stats.counts() == (0, 0, 0, 0) and f.stats.n_splats == 0
+
+
+def test_all_behind_camera(renderers):
+    cam = synthetic.make_camera(64, 64)
+    s = synthetic.make_scene(4, 50, depth_range=(-5.0, 0.2))
+    f = renderers["tcgs"].render_frame(tcgs.GaussianCloud.from_arrays(s, "cuda"), cam)
+    assert f.stats.dropped == 50 and f.stats.n_splats == 0 and float(f.rgb.abs().max()) == 0.0
+
+
+def test_single_huge_gaussian(renderers):
+    cam = synthetic.make_camera(200, 120)
+    d = {"means": np.array([[0.0, 0.0, 2.0]]), "scales": np.array([[3.0, 2.0, 1.0]]),
+         "rotations": np.array([[1.0, 0.0, 0.0, 0.0]]), "opacities": np.array([0.9]),
+         "colors": np.array([[0.2, 0.5, 0.8]])}
+    f = renderers["tcgs"].render_frame(tcgs.GaussianCloud.from_arrays(d, "cuda"), cam)
+    ref = oracle.render(d["means"], d["scales"], d["rotations"], d["opacities"], d["colors"], cam)
+    assert f.stats.n_splats == ref.stats.n_splats
+    assert float(np.max(np.abs(f.rgb.double().cpu().numpy() - ref.rgb))) <= RGB_TOL
+
+
+@pytest.mark.parametrize("band", [(0, 1), (2, 5), (4, 8)])
+def test_tile_band_matches_full_frame(renderers, band):
+    g = load_golden("f32gen")
+    cam = GoldenCam(g)
+    r = renderers["tcgs"]
+    cloud = cloud_of(g)
+    full = r.render_frame(cloud, cam)
+    full_rgb = full.rgb.clone()
+    full_cnt = full.n_contrib.clone()
+    fb = r.render_frame(cloud, cam, band=band)
+    y0, y1 = band[0] * 16, min(band[1] * 16, cam.height)
+    assert torch.equal(fb.rgb[y0:y1], full_rgb[y0:y1])  # same kernel, same inputs: bit-identical
+    assert torch.equal(fb.n_contrib[y0:y1], full_cnt[y0:y1])
+
+
+# ---- full-size parity (BASELINE config shapes) against the oracle ---------------------------------
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg,scale,rows", [("c2", 1.0, (30, 34)), ("c5", 0.25, (30, 32)), ("c4", 0.5, (30, 33))])
+def test_full_size_lists_and_band_pixels(renderers, cfg, scale, rows):
+    """Config-sized scenes: whole-frame tile lists bit-exact vs the oracle, pixels on a tile-row band."""
+    scene, cams = synthetic.config_scene(cfg, scale)
+    cam = cams[0] if cfg != "c4" else cams[37]
+    r = renderers["tcgs"]
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    f = r.render_frame(cloud, cam)
+    offsets, ids = r.tile_lists(cloud.P, cam)
+    # oracle colours: SH evaluated in float64 (parity of SH itself is unpinned by the reference)
+    colors = oracle.sh_color(scene["means"], scene["features"], scene["sh_degree"], cam.view)
+    proj = oracle.project(scene["means"], scene["scales"], scene["rotations"], cam)
+    o_off, o_ids = oracle.build_tiles(proj, cam)
+    assert np.array_equal(offsets, o_off) and np.array_equal(ids, o_ids)
+    rgb, T, cnt, st = oracle.blend(proj, o_off, o_ids, scene["opacities"], colors, cam, band=rows)
+    y0, y1 = rows[0] * 16, min(rows[1] * 16, cam.height)
+    g_rgb = f.rgb.double().cpu().numpy()[y0:y1]
+    assert float(np.max(np.abs(g_rgb - rgb[y0:y1]))) <= RGB_TOL
+    assert psnr(g_rgb, rgb[y0:y1]) >= PSNR_MIN
+    assert float(np.max(np.abs(f.T.double().cpu().numpy()[y0:y1] - T[y0:y1]))) <= RGB_TOL
+    g_cnt = f.n_contrib.cpu().numpy().copy()
+    g_cnt[:y0] = cnt[:y0]
+    g_cnt[y1:] = cnt[y1:]
+    n_mis, unexplained = explain_count_mismatches(g_cnt, cnt, o_off, o_ids, proj.mean2d, proj.inv_cov,
+                                                  np.asarray(scene["opacities"], np.float64), cam.width, "hilo")
+    assert not unexplained, (cfg, n_mis, unexplained[:5])

@@ -202,7 +202,7 @@ int tcgs_copy_lists(const void *ws, int64_t P, const tcgs_camera *cam, const tcg
 
 namespace {
 __global__ void copy_projection_kernel(int64_t P, const int32_t *radius, const Rec *rec, const double *dconic,
-                                       const double *ddepth, uint8_t *visible, double *mean2d, double *conic,
+                                       const double *ddepth, const double *dmean2d, uint8_t *visible, double *mean2d, double *conic,
                                        double *depth, int32_t *rad_out, float *rgb) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P) return;
@@ -213,9 +213,9 @@ __global__ void copy_projection_kernel(int64_t P, const int32_t *radius, const R
     conic[3 * i + 1] = dconic[3 * i + 1];
     conic[3 * i + 2] = dconic[3 * i + 2];
     depth[i] = ddepth[i];
-    const Rec q = rec[i];
-    mean2d[2 * i] = q.mx;
-    mean2d[2 * i + 1] = q.my;
+    const Rec q = rec[i];  // colour is only defined for Gaussians that touch a tile
+    mean2d[2 * i] = dmean2d[2 * i];
+    mean2d[2 * i + 1] = dmean2d[2 * i + 1];
     rgb[3 * i] = q.r;
     rgb[3 * i + 1] = q.g;
     rgb[3 * i + 2] = q.b;
@@ -231,7 +231,7 @@ extern "C" int tcgs_copy_projection(const void *ws, int64_t P, const tcgs_camera
     const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
     copy_projection_kernel<<<(unsigned)((P + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         P, at<int32_t>(ws, L.radius), at<Rec>(ws, L.rec), at<double>(ws, L.dbg_conic), at<double>(ws, L.dbg_depth),
-        visible, mean2d, conic, depth, radius, rgb);
+        at<double>(ws, L.dbg_mean2d), visible, mean2d, conic, depth, radius, rgb);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "copy_projection");
     return TCGS_OK;

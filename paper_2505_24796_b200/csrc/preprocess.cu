@@ -140,6 +140,7 @@ struct PreArgs {
     int32_t *radius;
     double *dbg_conic;
     double *dbg_depth;
+    double *dbg_mean2d;
     DevCounters *ctr;
 };
 
@@ -254,6 +255,8 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
                     a.dbg_conic[3 * i + 1] = s12;
                     a.dbg_conic[3 * i + 2] = s22;
                     a.dbg_depth[i] = tz;
+                    a.dbg_mean2d[2 * i] = mx;
+                    a.dbg_mean2d[2 * i + 1] = my;
                 }
                 // covered_tiles (src/tilesplat/tiling.py:34-43), clipped to the grid and the band
                 double fx0 = floor((mx - rad) / TILE), fx1 = floor((mx + rad) / TILE);
@@ -343,6 +346,7 @@ cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, c
     a.radius = at<int32_t>(ws, L.radius);
     a.dbg_conic = at<double>(ws, L.dbg_conic);
     a.dbg_depth = at<double>(ws, L.dbg_depth);
+    a.dbg_mean2d = at<double>(ws, L.dbg_mean2d);
     a.ctr = at<DevCounters>(ws, L.counters);
     if (scene.P <= 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((scene.P + 255) / 256);

@@ -1,28 +1,37 @@
 // render.cu -- K7: tensor-core alpha (Frag2Mat + G2L + EarlyCull) and conditional
-// blending, one 16x16 tile per CTA iteration (sm_100a, tcgen05 + TMEM).
+// blending for 16x16 tiles (sm_100a: tcgen05.mma, TMEM, mbarrier pipelines).
 //
 // Replaces the tile loop of tilesplat.raster.render and blend_tile
 // (/root/reference/pkg/src/tilesplat/raster.py:110-146,177-193) with the
 // Frag2Mat evaluator (src/tilesplat/tensor_path.py:25-163):
 //
-//   beta[p, j] = U[p, :] . V[j, :]       (256 pixels x 64 Gaussians per batch)
+//   beta[p, j] = U[p, :] . V[j, :]       (256 pixels x 32 Gaussians per batch)
 //
 // U holds each pixel's tile-local monomials [1, ux, uy, ux^2, ux*uy, uy^2]
-// (G2L: ux, uy in [-8, 7], tile centre origin, src/tilesplat/tensor_path.py:
-// 21-22,92-100) -- exact in fp16 and identical for every tile, so it is built
-// once per CTA in shared memory.  V holds each Gaussian's coefficients
-// (gaussian_vector, tensor_path.py:25-40) pre-scaled by log2(e) and split
-// into fp16 hi + lo parts so the K = 16 of tcgen05.mma.kind::f16 carries ~22
-// significant bits (TCGS_ALPHA_TC_K8 keeps the paper's length-8 fp16 vector).
-// Two MMAs (pixel halves, M = 128 each, N = 64, K = 16) accumulate in fp32 in
-// TMEM; each thread (= one pixel = one TMEM lane) reads its 64 betas with
-// tcgen05.ld and runs Algorithm 1: EarlyCull (beta < -log2 255 culls without
-// an exponential), alpha = ex2(beta), termination test before compositing
-// (T - alpha T < 1e-4), C += alpha T c, T -= alpha T.  The CTA retires the
-// tile when every in-image pixel has terminated (__syncthreads_or).
+// (G2L: ux, uy in [-8, 7] about the tile centre, src/tilesplat/tensor_path.py:
+// 21-22,92-100) -- exact in fp16 and the same for every tile, so it is built
+// once per CTA.  V holds each Gaussian's coefficients (gaussian_vector,
+// tensor_path.py:25-40) pre-scaled by log2(e) and split into fp16 hi + lo
+// parts so the K = 16 of tcgen05.mma.kind::f16 carries ~22 significant bits
+// (TCGS_ALPHA_TC_K8 keeps the paper's length-8 fp16 vector for ablation).
 //
-// Pipeline: double-buffered V stages and TMEM accumulators -- the MMA of
-// batch k+1 runs while the threads blend batch k.
+// CTA = 8 consumer warps (one pixel per thread; warp w owns an 8x4 pixel block
+// = TMEM lanes 32(w%4).. of pixel half w/4) + 1 producer warp.
+//   producer: takes tiles from a global queue, gathers each list entry's
+//     projected record, drops Gaussians whose EarlyCull test fails at every
+//     pixel of the tile (exact box minimum of the quadratic form -- these are
+//     culls the reference would count, and are counted), compacts the live
+//     ones 32 at a time into a shared-memory stage (fp16 hi/lo V rows,
+//     colours, dead-before counts), and issues two M=128 x N=32 x K=16 MMAs
+//     per stage into a TMEM accumulator buffer (commit -> mbarrier);
+//   consumers: tcgen05.ld their 32 betas, build the pass mask of EarlyCull
+//     (beta' < -log2 255 culls without an exponential), then walk the warp's
+//     union of passing columns in order: alpha = ex2(beta'), the termination
+//     test before compositing (T - alpha T < 1e-4, src/tilesplat/raster.py:
+//     136-145), C += alpha T c, T -= alpha T.  A warp whose pixels have all
+//     terminated stops working; when all 8 have, the producer retires the tile.
+// Stages (4) and TMEM buffers (2) are ring buffers guarded by full/empty and
+// mma_done/tmem_empty mbarriers, so gathers, MMAs and blending overlap.
 #include "tcgs_internal.cuh"
 
 namespace tcgs {
@@ -31,8 +40,11 @@ namespace {
 
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float CUT_LOG2 = -7.994353436858858f;  // -log2(255): beta' < CUT culls (tensor_path.py:79-81)
+constexpr float LN255 = 5.541263545158426f;
 constexpr float TERM_T = 0.0001f;                // src/tilesplat/raster.py:16
-constexpr int K7_SMEM_BYTES = 80 * 1024;         // also caps residency at 2 CTAs/SM (TMEM: 2 x 256 columns)
+constexpr int K7_SMEM_BYTES = 72 * 1024;         // also caps residency at 3 CTAs/SM (TMEM: 3 x 128 columns)
+constexpr int S = K7_STAGES;
+constexpr int NB = K7_TMEM_BUFS;
 
 struct RenderArgs {
     const Rec *rec;
@@ -47,15 +59,27 @@ struct RenderArgs {
     int32_t *n_contrib;
 };
 
+struct StageMeta {
+    int tile;        // -1: no more tiles
+    int seq;         // CTA-local tile sequence number
+    int n_live;      // live Gaussians in this stage (<= K7_BATCH)
+    int last;        // last stage of the tile's list
+    uint32_t dead_total;  // (last stage) dead Gaussians in the whole list
+    uint32_t n_total;     // list length of the tile
+    int pad[2];
+};
+
 struct __align__(1024) K7Smem {
-    __half U[2][128 * 16];           // A operands: pixel halves, K-major no-swizzle core matrices
-    __half V[2][K7_BATCH * 16];      // B operands: one per stage
-    float vf[2][K7_BATCH][8];        // FFMA mode coefficients
-    float4 col[2][K7_BATCH];         // colours per stage
-    unsigned long long bar[2];       // MMA-complete mbarriers, one per stage
+    __half U[2][128 * 16];              // A operands: pixel halves, K-major no-swizzle core matrices
+    __half V[S][K7_BATCH * 16];         // B operands, one per stage
+    float4 vf[S][K7_BATCH][2];          // FFMA mode: fp32 coefficients
+    float4 col[S][K7_BATCH];            // colours
+    uint32_t dead_before[S][K7_BATCH];  // dead Gaussians before each live one (list order)
+    StageMeta meta[S];
+    unsigned long long full[S], empty[S], mma_done[NB], tmem_empty[NB];
     uint32_t tmem_base;
-    int tile;
-    unsigned long long red[K7_THREADS / 32][4];
+    int retire[8];
+    unsigned long long red[K7_CONSUMER_WARPS][4];
 };
 
 // Element offset (in halves) of (row, k) in a K-major, no-swizzle UMMA operand of 16 K-columns:
@@ -70,7 +94,7 @@ __device__ __forceinline__ uint64_t umma_desc(const void *smem) {
            (1ull << 46);  // version 1 (sm_100), base offset 0, SWIZZLE_NONE
 }
 
-// kind::f16 instruction descriptor: D f32, A/B f16, K-major both, N = 64, M = 128.
+// kind::f16 instruction descriptor: D f32, A/B f16, K-major both, N = K7_BATCH, M = 128.
 constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(K7_BATCH >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t count) {
@@ -87,6 +111,14 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t pari
         "DONE:\n"
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile(
+        "{\n"
+        ".reg .b64 st;\n"
+        "mbarrier.arrive.shared::cta.b64 st, [%0];\n"
+        "}\n" ::"r"(smem_u32(bar))
         : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -120,19 +152,35 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// Gaussian coefficients for one tile (gaussian_vector, src/tilesplat/tensor_path.py:25-40), relative to the
-// tile centre (G2L), scaled by log2 e.  Returns false when no pixel of the tile can pass EarlyCull: then
-// sqrt(q(mu - c)) - sqrt(lambda_max(conic)) * 8 sqrt(2) > sqrt(2 (ln o + ln 255)) holds with margin and every
-// fragment of this Gaussian in the tile is culled in exact arithmetic (the reference would cull it too).
+// Gaussian coefficients for one tile (gaussian_vector, src/tilesplat/tensor_path.py:25-40) relative to the
+// tile centre (G2L), scaled by log2 e.  Returns false ("dead") when EarlyCull fails at every point of the
+// tile's pixel box [-8,7]^2: the minimum of the convex quadratic q(d - u) over the box is exact (interior
+// minimiser or the clamped minimiser on one of the four edges), and the test keeps a 0.01 margin on
+// beta, so every fragment of a dead Gaussian in this tile is a cull in exact arithmetic too.
 __device__ __forceinline__ bool gaussian_coeffs(const Rec &r, double ox, double oy, float v[6]) {
     const float dx = (float)(r.mx - ox), dy = (float)(r.my - oy);
     const float s11 = r.s11, s12 = r.s12, s22 = r.s22;
     const float q = s11 * dx * dx + 2.0f * s12 * dx * dy + s22 * dy * dy;
-    const float hm = 0.5f * (s11 - s22);
-    const float lam = 0.5f * (s11 + s22) + sqrtf(hm * hm + s12 * s12);
-    const float gap = sqrtf(fmaxf(q, 0.0f)) - sqrtf(fmaxf(lam, 0.0f)) * 11.3137085f;
-    const float need = 2.0f * (r.ln_o + 5.5412635451584258f) + 1.0f;  // 2 (ln o + ln 255) + margin
-    if (gap > 0.0f && gap * gap > need) return false;
+    if (s11 > 0.0f && s22 > 0.0f && !(dx >= -8.0f && dx <= 7.0f && dy >= -8.0f && dy <= 7.0f)) {
+        float qmin = 3.0e38f;
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+            const float a = e ? 7.0f : -8.0f;
+            {  // edge ux = a
+                const float ex = dx - a;
+                const float uy = fminf(fmaxf(dy + s12 * ex / s22, -8.0f), 7.0f);
+                const float ey = dy - uy;
+                qmin = fminf(qmin, s11 * ex * ex + 2.0f * s12 * ex * ey + s22 * ey * ey);
+            }
+            {  // edge uy = a
+                const float ey = dy - a;
+                const float ux = fminf(fmaxf(dx + s12 * ey / s11, -8.0f), 7.0f);
+                const float ex = dx - ux;
+                qmin = fminf(qmin, s11 * ex * ex + 2.0f * s12 * ex * ey + s22 * ey * ey);
+            }
+        }
+        if (r.ln_o - 0.5f * qmin < -LN255 - 0.01f) return false;
+    }
     v[0] = (r.ln_o - 0.5f * q) * LOG2E;
     v[1] = (s11 * dx + s12 * dy) * LOG2E;
     v[2] = (s12 * dx + s22 * dy) * LOG2E;
@@ -145,17 +193,13 @@ __device__ __forceinline__ bool gaussian_coeffs(const Rec &r, double ox, double 
 __device__ __forceinline__ __half h16(float x) { return __float2half_rn(x); }
 __device__ __forceinline__ float f32(__half x) { return __half2float(x); }
 
-// Write one B-operand row (16 fp16) for MODE: hi/lo split (0) or the paper's K8 vector (1).
+// One B-operand row (16 fp16) for MODE: hi/lo split (0) or the paper's K8 vector (1).
+// U row: [1, 1, 1, ux, uy, ux^2, ux uy, uy^2, ux, uy, ux^2, ux uy, uy^2, 1, 0, 0]
 template <int MODE>
-__device__ __forceinline__ void write_vrow(__half *V, int row, const float v[6], bool live) {
+__device__ __forceinline__ void write_vrow(__half *V, int row, const float v[6]) {
     __align__(16) __half e[16];
-    if (!live) {
-#pragma unroll
-        for (int k = 0; k < 16; k++) e[k] = __float2half_rn(0.0f);
-        e[0] = h16(-1000.0f);  // beta' = -1000: culled at every pixel
-    } else if (MODE == TCGS_ALPHA_TC_HILO) {
-        // v0 = a + b + c + d (four fp16 pieces), v1..v5 = hi + lo
-        const __half a = h16(v[0]);
+    if (MODE == TCGS_ALPHA_TC_HILO) {
+        const __half a = h16(v[0]);  // v0 = a + b + c + d
         const float r1 = v[0] - f32(a);
         const __half b = h16(r1);
         const float r2 = r1 - f32(b);
@@ -188,203 +232,286 @@ __device__ __forceinline__ void write_vrow(__half *V, int row, const float v[6],
     *reinterpret_cast<uint4 *>(V + kmaj_off(row, 8)) = src[1];
 }
 
+// ------------------------------------------------------------------------------------------ producer
+template <int MODE>
+__device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, uint32_t tmem) {
+    constexpr bool TC = MODE != TCGS_ALPHA_FFMA;
+    const int lane = threadIdx.x & 31;
+    const unsigned FULL = 0xffffffffu, lt = lanemask_lt();
+    int k = 0;                  // stage sequence number
+    int seq = 0;                // tile sequence number
+    bool open = false;          // stage k % S acquired
+    auto acquire = [&]() {
+        if (!open) {
+            mbar_wait(&sm.empty[k % S], ((k / S) & 1) ^ 1);
+            open = true;
+        }
+    };
+    auto emit = [&](int tile, int sq, int n_live, int last, uint32_t dead_total, uint32_t n_total) {
+        acquire();
+        const int st = k % S;
+        if (TC) fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            StageMeta m;
+            m.tile = tile;
+            m.seq = sq;
+            m.n_live = n_live;
+            m.last = last;
+            m.dead_total = dead_total;
+            m.n_total = n_total;
+            sm.meta[st] = m;
+            mbar_arrive(&sm.full[st]);
+            if (TC && tile >= 0) {
+                const int b = k % NB;
+                mbar_wait(&sm.tmem_empty[b], ((k / NB) & 1) ^ 1);
+                tc_fence_after();
+                const uint64_t bdesc = umma_desc(sm.V[st]);
+#pragma unroll
+                for (int h = 0; h < 2; h++)
+                    mma_f16(tmem + b * (2 * K7_BATCH) + h * K7_BATCH, umma_desc(sm.U[h]), bdesc, IDESC);
+                mma_commit(&sm.mma_done[b]);
+            }
+        }
+        __syncwarp();
+        k++;
+        open = false;
+    };
+    auto write_slot = [&](int slot, const float v[6], const Rec &r, uint32_t dead_before) {
+        const int st = k % S;
+        if (TC) {
+            write_vrow<MODE>(sm.V[st], slot, v);
+        } else {
+            sm.vf[st][slot][0] = make_float4(v[0], v[1], v[2], v[3]);
+            sm.vf[st][slot][1] = make_float4(v[4], v[5], 0.f, 0.f);
+        }
+        sm.col[st][slot] = make_float4(r.r, r.g, r.b, 0.f);
+        sm.dead_before[st][slot] = dead_before;
+    };
+
+    for (;;) {
+        int tile = 0;
+        if (lane == 0) tile = (int)atomicAdd(&a.ctr->tile_queue, 1u);
+        tile = __shfl_sync(FULL, tile, 0);
+        if (tile >= a.n_tiles) {
+            emit(-1, seq, 0, 1, 0u, 0u);
+            break;
+        }
+        const int sq = seq++;
+        if (lane == 0) *((volatile int *)&sm.retire[sq & 7]) = 0;
+        __syncwarp();
+        const uint2 rg = a.ranges[tile];
+        const int n = (int)(rg.y - rg.x);
+        const int tx = tile % a.tiles_x, ty = a.band_y0 + tile / a.tiles_x;
+        const double ox = tx * TILE + 8.0, oy = ty * TILE + 8.0;  // tile_center (tensor_path.py:21-22)
+        int fill = 0;
+        uint32_t dead = 0;
+        bool retired = false;
+        // software pipeline: the next chunk's id and record are in flight while this one is processed
+        Rec nr;
+        bool nvalid = lane < n;
+        if (nvalid) nr = a.rec[ids[rg.x + lane]];
+        for (int base = 0; base < n; base += 32) {
+            if (*((volatile int *)&sm.retire[sq & 7]) >= K7_CONSUMER_WARPS) {
+                retired = true;
+                break;
+            }
+            const Rec r = nr;
+            const bool valid = nvalid;
+            nvalid = base + 32 + lane < n;
+            if (nvalid) nr = a.rec[ids[rg.x + base + 32 + lane]];
+            float v[6];
+            const bool live = valid && gaussian_coeffs(r, ox, oy, v);
+            const unsigned lm = __ballot_sync(FULL, live), dm = __ballot_sync(FULL, valid && !live);
+            const int slot = fill + __popc(lm & lt);
+            const uint32_t my_dead = dead + __popc(dm & lt);
+            const int nl = __popc(lm);
+            acquire();
+            if (live && slot < K7_BATCH) write_slot(slot, v, r, my_dead);
+            if (fill + nl >= K7_BATCH) {
+                emit(tile, sq, K7_BATCH, 0, 0u, (uint32_t)n);
+                fill = fill + nl - K7_BATCH;
+                if (fill > 0) {
+                    acquire();
+                    if (live && slot >= K7_BATCH) write_slot(slot - K7_BATCH, v, r, my_dead);
+                }
+            } else {
+                fill += nl;
+            }
+            dead += __popc(dm);
+        }
+        if (!retired) emit(tile, sq, fill, 1, dead, (uint32_t)n);
+    }
+}
+
+// ------------------------------------------------------------------------------------------ kernel
 template <int MODE>
 __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(RenderArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     K7Smem &sm = *reinterpret_cast<K7Smem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr bool TC = MODE != TCGS_ALPHA_FFMA;
+    const unsigned FULL = 0xffffffffu;
 
-    // pixel owned by this thread: warp w covers an 8x4 block (compact footprints per warp)
+    // pixel owned by a consumer thread: warp w covers an 8x4 block (compact footprints per warp)
     const int lx = 8 * (warp & 1) + (lane & 7);
-    const int ly = 4 * (warp >> 1) + (lane >> 3);
+    const int ly = 4 * ((warp >> 1) & 3) + (lane >> 3);
     const float ux = (float)(lx - 8), uy = (float)(ly - 8);
-    const int half = warp >> 2;               // which M=128 MMA (TMEM column block) holds this pixel
+    const int half = (warp >> 2) & 1;         // which M=128 MMA (TMEM column block) holds this pixel
     const int urow = 32 * (warp & 3) + lane;  // TMEM lane == U row within the half
 
-    if (TC) {
-        // U: [1, 1, 1, ux, uy, ux^2, ux uy, uy^2, ux, uy, ux^2, ux uy, uy^2, 1, 0, 0]
+    if (warp < K7_CONSUMER_WARPS && TC) {
         const float u[16] = {1.f, 1.f, 1.f, ux, uy, ux * ux, ux * uy, uy * uy, ux, uy, ux * ux, ux * uy, uy * uy, 1.f, 0.f, 0.f};
 #pragma unroll
         for (int k = 0; k < 16; k++) sm.U[half][kmaj_off(urow, k)] = __float2half_rn(u[k]);
-        if (tid == 0) {
-            mbar_init(&sm.bar[0], 1);
-            mbar_init(&sm.bar[1], 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        if (warp == 0) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
-                         "r"(K7_TMEM_COLS));
-            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-        }
         fence_async_smem();
-        tc_fence_before();
     }
+    if (tid == 0) {
+        for (int s = 0; s < S; s++) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], K7_CONSUMER_WARPS);
+        }
+        for (int b = 0; b < NB; b++) {
+            mbar_init(&sm.mma_done[b], 1);
+            mbar_init(&sm.tmem_empty[b], K7_CONSUMER_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (TC && warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sm.tmem_base)),
+                     "r"(K7_TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (TC) tc_fence_before();
     __syncthreads();
     if (TC) tc_fence_after();
     const uint32_t tmem = TC ? sm.tmem_base : 0u;
-    uint32_t phase = 0;  // bit s: parity of the next completion of bar[s]
-
-    unsigned long long s_blend = 0, s_cull = 0, s_term = 0, s_pairs = 0;
     const uint32_t *ids = a.ids_override ? a.ids_override : (a.ctr->tile_cur ? a.ids1 : a.ids0);
 
-    for (;;) {
-        if (tid == 0) sm.tile = (int)atomicAdd(&a.ctr->tile_queue, 1u);
-        __syncthreads();
-        const int tile = sm.tile;
-        if (tile >= a.n_tiles) break;
-        const uint2 rg = a.ranges[tile];
-        const int n = (int)(rg.y - rg.x);
-        const int tx = tile % a.tiles_x, ty = a.band_y0 + tile / a.tiles_x;
-        const int px = tx * TILE + lx, py = ty * TILE + ly;
-        const bool inside = px < a.width && py < a.height;
-        const double ox = tx * TILE + 8.0, oy = ty * TILE + 8.0;  // tile_center (tensor_path.py:21-22)
-        bool done = !inside;
-        bool term = false;
+    unsigned long long s_blend = 0, s_cull = 0, s_term = 0, s_pairs = 0;
+    if (warp == K7_CONSUMER_WARPS) {
+        producer<MODE>(sm, a, ids, tmem);
+    } else {
+        int cur_seq = -1, cur_tile = -1;
+        int px = 0, py = 0;
+        bool inside = false, done = true, term = false, warp_done = true;
         float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
-        uint32_t cnt = 0, cull = 0;
-        const int nb = (n + K7_BATCH - 1) / K7_BATCH;
-
-        auto build = [&](int kb, int s) {
-            if (tid < K7_BATCH) {
-                const int j = kb * K7_BATCH + tid;
-                float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                bool live = false;
-                float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (j < n) {
-                    const Rec r = a.rec[ids[rg.x + j]];
-                    live = gaussian_coeffs(r, ox, oy, v);
-                    col = make_float4(r.r, r.g, r.b, 0.f);
-                }
-                sm.col[s][tid] = col;
-                if (TC) {
-                    write_vrow<MODE>(sm.V[s], tid, v, live);
-                } else {
-                    if (!live) {
-                        v[0] = -1000.0f;
-                        v[1] = v[2] = v[3] = v[4] = v[5] = 0.0f;
-                    }
-#pragma unroll
-                    for (int i = 0; i < 6; i++) sm.vf[s][tid][i] = v[i];
-                }
+        uint32_t cnt = 0, cull = 0, n_total = 0;
+        auto flush = [&]() {
+            if (inside) {
+                const int64_t p = (int64_t)py * a.width + px;
+                a.rgb[3 * p] = c0;
+                a.rgb[3 * p + 1] = c1;
+                a.rgb[3 * p + 2] = c2;
+                a.T[p] = T;
+                a.n_contrib[p] = (int32_t)cnt;
+                s_pairs += n_total;
             }
+            s_blend += cnt;
+            s_cull += cull;
+            s_term += term ? 1u : 0u;
         };
-        auto issue = [&](int s) {
-            if (TC && tid == 0) {
+        for (int k = 0;; k++) {
+            const int st = k % S, b = k % NB;
+            mbar_wait(&sm.full[st], (k / S) & 1);
+            const StageMeta m = sm.meta[st];
+            if (m.seq != cur_seq || m.tile < 0) {
+                if (cur_seq >= 0) flush();
+                if (m.tile < 0) break;
+                cur_seq = m.seq;
+                cur_tile = m.tile;
+                const int tx = cur_tile % a.tiles_x, ty = a.band_y0 + cur_tile / a.tiles_x;
+                px = tx * TILE + lx;
+                py = ty * TILE + ly;
+                inside = px < a.width && py < a.height;
+                done = !inside;
+                term = false;
+                T = 1.0f;
+                c0 = c1 = c2 = 0.0f;
+                cnt = cull = 0;
+                n_total = m.n_total;
+                warp_done = __all_sync(FULL, done);
+                if (warp_done && lane == 0) atomicAdd(&sm.retire[cur_seq & 7], 1);
+            }
+            if (TC) {
+                mbar_wait(&sm.mma_done[b], (k / NB) & 1);
                 tc_fence_after();
-                const uint64_t bdesc = umma_desc(sm.V[s]);
-#pragma unroll
-                for (int h = 0; h < 2; h++) mma_f16(tmem + s * 128 + h * 64, umma_desc(sm.U[h]), bdesc, IDESC);
-                mma_commit(&sm.bar[s]);
             }
-        };
-        auto wait_mma = [&](int s) {
-            if (TC) {
-                mbar_wait(&sm.bar[s], (phase >> s) & 1u);
-                phase ^= 1u << s;
-            }
-        };
-
-        if (nb > 0) {
-            build(0, 0);
-            if (TC) {
-                fence_async_smem();
-                tc_fence_before();
-            }
-            __syncthreads();
-            issue(0);
-            for (int kb = 0; kb < nb; kb++) {
-                const int s = kb & 1;
-                if (kb + 1 < nb) build(kb + 1, s ^ 1);
+            if (!warp_done) {
+                uint32_t r[32];
                 if (TC) {
-                    fence_async_smem();
-                    tc_fence_before();
-                }
-                __syncthreads();
-                if (kb + 1 < nb) issue(s ^ 1);
-                wait_mma(s);
-                const int jmax = min(K7_BATCH, n - kb * K7_BATCH);
-                float beta[K7_BATCH];
-                if (TC) {
-                    tc_fence_after();
-                    uint32_t r0[32], r1[32];
-                    const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + s * 128 + half * 64;
-                    tmem_ld32(taddr, r0);
-                    tmem_ld32(taddr + 32, r1);
+                    tmem_ld32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (2 * K7_BATCH) + half * K7_BATCH, r);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int j = 0; j < 32; j++) {
-                        asm volatile("" : "+r"(r0[j]));
-                        asm volatile("" : "+r"(r1[j]));
-                    }
+                    for (int j = 0; j < 32; j++) asm volatile("" : "+r"(r[j]));
+                } else {
 #pragma unroll
                     for (int j = 0; j < 32; j++) {
-                        beta[j] = __uint_as_float(r0[j]);
-                        beta[32 + j] = __uint_as_float(r1[j]);
+                        const float4 p0 = sm.vf[st][j][0], p1 = sm.vf[st][j][1];
+                        const float bj = p0.x + p0.y * ux + p0.z * uy + p0.w * ux * ux + p1.x * ux * uy + p1.y * uy * uy;
+                        r[j] = __float_as_uint(bj);
                     }
                 }
+                const int nl = m.n_live;
+                const uint32_t act = done ? 0u : (nl >= 32 ? FULL : ((1u << nl) - 1u));
+                uint32_t pass = 0;
 #pragma unroll
-                for (int j = 0; j < K7_BATCH; j++) {
-                    if (!done && j < jmax) {
-                        float b;
-                        if (TC) {
-                            b = beta[j];
-                        } else {
-                            const float *v = sm.vf[s][j];
-                            b = v[0] + v[1] * ux + v[2] * uy + v[3] * ux * ux + v[4] * ux * uy + v[5] * uy * uy;
-                        }
-                        if (b >= CUT_LOG2) {
-                            const float al = fminf(ex2_approx(b), 1.0f);
+                for (int j = 0; j < 32; j++)
+                    if (__uint_as_float(r[j]) >= CUT_LOG2) pass |= 1u << j;
+                pass &= act;
+                const uint32_t wm = __reduce_or_sync(FULL, pass);
+                int jt = 32;
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    if (wm & (1u << j)) {
+                        if (((pass >> j) & 1u) && !done) {
+                            const float al = fminf(ex2_approx(__uint_as_float(r[j])), 1.0f);
                             const float tn = fmaf(-al, T, T);
                             if (tn < TERM_T) {
                                 done = true;
                                 term = true;
+                                jt = j;
                             } else {
                                 const float w = al * T;
-                                const float4 cc = sm.col[s][j];
+                                const float4 cc = sm.col[st][j];
                                 c0 = fmaf(w, cc.x, c0);
                                 c1 = fmaf(w, cc.y, c1);
                                 c2 = fmaf(w, cc.z, c2);
                                 T = tn;
                                 cnt++;
                             }
-                        } else {
-                            cull++;
                         }
                     }
                 }
-                if (TC) tc_fence_before();
-                const int alive = __syncthreads_or(!done);
-                if (!alive) {
-                    if (kb + 1 < nb) wait_mma(s ^ 1);  // drain the MMA already in flight
-                    break;
+                // EarlyCull counts: live columns failing the cut before termination, plus the dead
+                // Gaussians of the list before the terminating one
+                const uint32_t before = jt >= 32 ? FULL : ((1u << jt) - 1u);
+                cull += __popc(act & ~pass & before);
+                if (jt < 32) cull += sm.dead_before[st][jt];
+                if (__all_sync(FULL, done)) {
+                    warp_done = true;
+                    if (lane == 0) atomicAdd(&sm.retire[cur_seq & 7], 1);
                 }
             }
+            if (m.last && !done) cull += m.dead_total;  // list exhausted: every dead Gaussian was a cull
+            if (TC) tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (TC) mbar_arrive(&sm.tmem_empty[b]);
+                mbar_arrive(&sm.empty[st]);
+            }
         }
-        if (inside) {
-            const int64_t p = (int64_t)py * a.width + px;
-            a.rgb[3 * p] = c0;
-            a.rgb[3 * p + 1] = c1;
-            a.rgb[3 * p + 2] = c2;
-            a.T[p] = T;
-            a.n_contrib[p] = (int32_t)cnt;
-            s_pairs += (unsigned long long)n;
-        }
-        s_blend += cnt;
-        s_cull += cull;
-        s_term += term ? 1u : 0u;
-        __syncthreads();
     }
 
     // K8: fragment statistics, one atomic per CTA and counter
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        s_blend += __shfl_xor_sync(0xffffffffu, s_blend, o);
-        s_cull += __shfl_xor_sync(0xffffffffu, s_cull, o);
-        s_term += __shfl_xor_sync(0xffffffffu, s_term, o);
-        s_pairs += __shfl_xor_sync(0xffffffffu, s_pairs, o);
+        s_blend += __shfl_xor_sync(FULL, s_blend, o);
+        s_cull += __shfl_xor_sync(FULL, s_cull, o);
+        s_term += __shfl_xor_sync(FULL, s_term, o);
+        s_pairs += __shfl_xor_sync(FULL, s_pairs, o);
     }
-    if (lane == 0) {
+    if (lane == 0 && warp < K7_CONSUMER_WARPS) {
         sm.red[warp][0] = s_blend;
         sm.red[warp][1] = s_cull;
         sm.red[warp][2] = s_term;
@@ -394,7 +521,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
     __syncthreads();
     if (tid < 4) {
         unsigned long long t = 0;
-        for (int w = 0; w < K7_THREADS / 32; w++) t += sm.red[w][tid];
+        for (int w = 0; w < K7_CONSUMER_WARPS; w++) t += sm.red[w][tid];
         unsigned long long *dst = tid == 0 ? &a.ctr->f_blend
                                   : tid == 1 ? &a.ctr->f_cull
                                   : tid == 2 ? &a.ctr->pixels_terminated
@@ -424,7 +551,7 @@ cudaError_t launch_mode(const RenderArgs &a, int num_sms, cudaStream_t st) {
 
 cudaError_t launch_render(int alpha_mode, const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
                           void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st) {
-    static_assert(sizeof(K7Smem) <= K7_SMEM_BYTES, "K7 shared memory");
+    static_assert(sizeof(K7Smem) + 1024 <= K7_SMEM_BYTES, "K7 shared memory");
     RenderArgs a;
     a.rec = at<Rec>(ws, L.rec);
     a.ids0 = at<uint32_t>(ws, L.tval[0]);

@@ -21,10 +21,13 @@ constexpr int SCAN_THREADS = 256;
 constexpr int MAX_PASSES = 8;         // depth key: <= 64 bits
 constexpr int TILE_PASS_SLOT = 8;     // pass bookkeeping slots 8.. are the tile-key passes
 
-constexpr int K7_THREADS = 256;       // one pixel per thread, 16x16 tile
-constexpr int K7_BATCH = 64;          // Gaussians per tcgen05 batch (MMA N)
-constexpr int K7_TMEM_COLS = 256;     // 2 buffers x 2 pixel halves x 64 columns
-constexpr int K7_CTAS_PER_SM = 2;
+constexpr int K7_CONSUMER_WARPS = 8;  // one pixel per thread, 16x16 tile
+constexpr int K7_THREADS = 32 * (K7_CONSUMER_WARPS + 1);  // + one producer / MMA-issue warp
+constexpr int K7_BATCH = 32;          // live Gaussians per tcgen05 batch (MMA N)
+constexpr int K7_STAGES = 4;          // shared-memory B-operand stages
+constexpr int K7_TMEM_BUFS = 2;       // TMEM accumulator buffers
+constexpr int K7_TMEM_COLS = K7_TMEM_BUFS * 2 * K7_BATCH;  // buffers x pixel halves x N
+constexpr int K7_CTAS_PER_SM = 3;
 
 // Per-Gaussian record consumed by the blend kernel (48 B, three 16 B loads).
 struct __align__(16) Rec {
@@ -47,7 +50,7 @@ struct DevCounters {
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-    size_t counters, rec, rect, touched, key64[2], idx[2], radius, dbg_conic, dbg_depth;
+    size_t counters, rec, rect, touched, key64[2], idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
     size_t hist, blocksum, tkey[2], tval[2], ranges, total;
     static Layout make(int64_t P, int W, int H, int64_t cap) {
         Layout L;
@@ -66,6 +69,7 @@ struct Layout {
         L.radius = take(sizeof(int32_t) * Pn);
         L.dbg_conic = take(sizeof(double) * 3 * Pn);
         L.dbg_depth = take(sizeof(double) * Pn);
+        L.dbg_mean2d = take(sizeof(double) * 2 * Pn);
         L.hist = take(sizeof(uint32_t) * RADIX * SORT_BLOCKS);
         L.blocksum = take(sizeof(unsigned long long) * SCAN_BLOCKS);
         L.tkey[0] = take(sizeof(uint32_t) * cn);

@@ -154,19 +154,18 @@ def profile_traffic():
 
 
 def launches_per_frame(P, cam, band_rows=None):
-    """Kernels libtcgs.so launches per frame (fixed schedule, see csrc/binning.cu)."""
+    """Kernels libtcgs.so launches per frame (fixed schedule, csrc/abi.cu + csrc/binning.cu)."""
     tiles_x = (cam.width + 15) // 16
     tiles_y = (cam.height + 15) // 16 if band_rows is None else band_rows
     nt = tiles_x * tiles_y
     bits = max(1, math.ceil(math.log2(max(nt, 2))))
     tile_passes = math.ceil(bits / 8)
-    depth_passes = 8
-    k = 1 + 1  # init_counters, preprocess
+    k = 2  # init_counters, preprocess_kernel
     if P > 0:
-        k += 1 + 3 * depth_passes  # depth_key_fix + (upsweep, scan, downsweep) per pass
+        k += 2 + 8  # depth_fix_hist, sort_plan, 8 onesweep passes (identity passes exit at entry)
     k += 3  # count_upsweep, count_scan, duplicate_keys
-    k += 3 * tile_passes + 1  # tile sort + ranges
-    k += 1  # render
+    k += 1 + tile_passes + 1  # sort_plan, onesweep passes, tile_ranges
+    k += 1  # render_kernel
     return k
 
 

@@ -3,27 +3,37 @@
 // Replaces tilesplat.tiling.build_tiles (/root/reference/pkg/src/tilesplat/
 // tiling.py:46-59): every tile's list holds the Gaussians whose closed
 // bounding square covers it, ascending by float64 depth, ties by index
-// (Python's stable sort).  The order is the LSD radix order of the composite
-// key (tile, depth, index), produced in two stages so the expensive depth
-// digits are sorted on the P Gaussians rather than the N splats:
+// (Python's stable sort).  That is the LSD radix order of the composite key
+// (tile, depth, index), produced in two stages so that the wide depth digits
+// are sorted on the P Gaussians rather than on the N splats:
 //
 //   K2  depth-rank sort: stable LSD radix (8-bit digits) of the float64 depth
-//       bits (minus the visible minimum) carrying the Gaussian index; passes
-//       whose digit is constant are detected on the device and skipped;
+//       bits minus the visible minimum, carrying the Gaussian index; passes
+//       above the key range or with a single digit value are skipped on the
+//       device (the digit histograms of all passes come from one read, fused
+//       with the key rebase);
 //   K3  exclusive scan of the tile counts in depth order -> write offsets, N;
-//   K4  duplicate-with-keys: emit (tile, id) for every covered tile, in depth
-//       order, with a block-cooperative load-balanced expansion (coalesced
-//       stores);
-//   K5  stable LSD radix sort of the splats on the tile digits only;
-//   K6  identify tile ranges [start, end).
+//   K4  duplicate-with-keys: emit (tile, id) for every covered tile in depth
+//       order with a CTA-cooperative, load-balanced expansion (coalesced
+//       stores), histogramming the tile digits for K5 on the fly;
+//   K5  stable LSD radix sort of the splats on the tile digits only (16-bit
+//       keys when the band has <= 65536 tiles);
+//   K6  tile ranges [start, end) from the sorted keys.
 //
-// Every kernel runs on a fixed grid and reads its item count from device
-// memory, so a frame needs no host synchronisation (graph-capturable).
+// Every radix pass is one "onesweep" kernel: in-order tile tickets, warp
+// match_any multi-split for the stable local rank, decoupled look-back over
+// the per-tile digit counts, and a shared-memory staged scatter so the
+// global stores are coalesced runs.  All counts live on the device: a frame
+// needs no host synchronisation (graph-capturable).
 #include "tcgs_internal.cuh"
 
 namespace tcgs {
 
 namespace {
+
+constexpr uint32_t LB_AGG = 1u << 30;  // look-back word: flag (2 bits) | count (30 bits)
+constexpr uint32_t LB_PRE = 2u << 30;
+constexpr uint32_t LB_MASK = (1u << 30) - 1u;
 
 __device__ __forceinline__ int64_t dev_count(const unsigned long long *n_dev, int64_t n_host, int64_t cap) {
     if (!n_dev) return n_host;
@@ -31,337 +41,351 @@ __device__ __forceinline__ int64_t dev_count(const unsigned long long *n_dev, in
     return (int64_t)(n < (unsigned long long)cap ? n : (unsigned long long)cap);
 }
 
-__device__ __forceinline__ void chunk_of(int64_t n, int nblocks, int b, int64_t &beg, int64_t &end) {
-    int64_t c = (n + nblocks - 1) / nblocks;
-    c = (c + 31) & ~31ll;
-    beg = (int64_t)b * c;
-    end = beg + c < n ? beg + c : n;
-    if (beg > n) beg = n;
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t *warp_tmp, uint32_t *total) {
+    // exclusive scan over the 256 threads of the CTA (blockDim.x == 256)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tmp[warp] = x;
+    __syncthreads();
+    uint32_t pre = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+        const uint32_t s = warp_tmp[w];
+        pre += w < warp ? s : 0u;
+        tot += s;
+    }
+    if (total) *total = tot;
+    __syncthreads();
+    return pre + x - v;
 }
 
-// K2 prologue: depth bits -> (bits - min over visible); Gaussians touching no tile get 0
-// (they emit nothing, so their position in the depth order is irrelevant).
-__global__ void depth_key_fix(unsigned long long *keys, int64_t P, DevCounters *ctr) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P) return;
+// ---------------------------------------------------------------- K2 prologue
+// depth bits -> bits - min over visible; Gaussians touching no tile get 0 (they emit nothing, so their
+// place in the depth order is irrelevant).  Histograms every digit below the key range in the same read.
+__global__ void __launch_bounds__(256) depth_fix_hist(unsigned long long *keys, int64_t P, DevCounters *ctr,
+                                                      SortState *ss) {
+    __shared__ uint32_t h[MAX_PASSES][RADIX];
+    for (int e = threadIdx.x; e < MAX_PASSES * RADIX; e += blockDim.x) (&h[0][0])[e] = 0;
+    __syncthreads();
     const unsigned long long kmin = ctr->key_min;
-    if (i == 0) ctr->key_range = ctr->n_visible ? ctr->key_max - kmin : 0ull;
-    const unsigned long long k = keys[i];
-    keys[i] = (k == ~0ull) ? 0ull : k - kmin;
-}
-
-template <typename KT>
-__device__ __forceinline__ const KT *sel(const KT *a, const KT *b, int s) {
-    return s ? b : a;
-}
-
-// ---------------------------------------------------------------- radix sort
-// Upsweep: per-block digit histograms of the block's contiguous chunk.
-template <typename KT>
-__global__ void __launch_bounds__(SORT_THREADS) radix_upsweep(const KT *keys0, const KT *keys1, const int *cur,
-                                                              const unsigned long long *n_dev, int64_t n_host,
-                                                              int64_t cap, int shift, const unsigned long long *range,
-                                                              uint32_t *hist) {
-    __shared__ uint32_t wh[SORT_WARPS][RADIX];
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const int64_t n = dev_count(n_dev, n_host, cap);
-    int64_t beg, end;
-    chunk_of(n, gridDim.x, blockIdx.x, beg, end);
-    if (range && ((*range) >> shift) == 0) {  // every digit is 0: nothing to count
-        for (int d = tid; d < RADIX; d += SORT_THREADS) hist[d * gridDim.x + blockIdx.x] = d == 0 ? (uint32_t)(end - beg) : 0u;
-        return;
+    const unsigned long long range = ctr->n_visible ? ctr->key_max - kmin : 0ull;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->key_range = range;
+    const int np = range ? (64 - __clzll((long long)range) + RADIX_BITS - 1) / RADIX_BITS : 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long k = keys[i];
+        k = (k == ~0ull) ? 0ull : k - kmin;
+        keys[i] = k;
+        for (int p = 0; p < np; p++) atomicAdd(&h[p][(unsigned)(k >> (RADIX_BITS * p)) & (RADIX - 1)], 1u);
     }
-    for (int d = tid; d < SORT_WARPS * RADIX; d += SORT_THREADS) (&wh[0][0])[d] = 0;
     __syncthreads();
-    const KT *keys = sel(keys0, keys1, *cur);
-    int64_t i = beg + tid;
-    for (; i + 3 * SORT_THREADS < end; i += 4 * SORT_THREADS) {
-        KT k[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) k[u] = keys[i + u * SORT_THREADS];
-#pragma unroll
-        for (int u = 0; u < 4; u++) atomicAdd(&wh[warp][(unsigned)(k[u] >> shift) & (RADIX - 1)], 1u);
-    }
-    for (; i < end; i += SORT_THREADS) atomicAdd(&wh[warp][(unsigned)(keys[i] >> shift) & (RADIX - 1)], 1u);
-    __syncthreads();
-    for (int d = tid; d < RADIX; d += SORT_THREADS) {
-        uint32_t s = 0;
-#pragma unroll
-        for (int w = 0; w < SORT_WARPS; w++) s += wh[w][d];
-        hist[d * gridDim.x + blockIdx.x] = s;
+    for (int e = threadIdx.x; e < np * RADIX; e += blockDim.x) {
+        const uint32_t c = (&h[0][0])[e];
+        if (c) atomicAdd(&(&ss->ghist[0][0])[e], c);
     }
 }
 
-// Scan: digit-major exclusive scan of the [RADIX][blocks] histogram table (stable order),
-// plus the triviality test (one digit holds every item -> the pass is the identity).
-__global__ void __launch_bounds__(1024) radix_scan(uint32_t *hist, int nblocks, const unsigned long long *n_dev,
-                                                   int64_t n_host, int64_t cap, int *cur, DevCounters *ctr, int slot) {
-    __shared__ uint32_t total[RADIX];
+// Turn the digit histograms into exclusive global bases, mark identity passes, assign ping-pong buffers.
+__global__ void __launch_bounds__(256) sort_plan(SortState *ss, int npass, const unsigned long long *n_dev,
+                                                 int64_t n_host, int64_t cap, const unsigned long long *range,
+                                                 int *final_out) {
+    __shared__ uint32_t wt[8];
     __shared__ int trivial;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int d = threadIdx.x;
     const int64_t n = dev_count(n_dev, n_host, cap);
-    if (tid == 0) trivial = 0;
-    __syncthreads();
-    for (int d = warp; d < RADIX; d += 32) {
-        uint32_t run = 0;
-        for (int b0 = 0; b0 < nblocks; b0 += 32) {
-            const int b = b0 + lane;
-            const uint32_t v = b < nblocks ? hist[d * nblocks + b] : 0u;
-            uint32_t x = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (b < nblocks) hist[d * nblocks + b] = run + x - v;
-            run += __shfl_sync(0xffffffffu, x, 31);
+    int cur = 0;
+    for (int p = 0; p < npass; p++) {
+        const bool active = range ? (((*range) >> (RADIX_BITS * p)) != 0ull) : true;
+        if (d == 0) trivial = (!active || n == 0) ? 1 : 0;
+        __syncthreads();
+        const uint32_t c = active ? ss->ghist[p][d] : 0u;
+        if ((int64_t)c == n) trivial = 1;
+        const uint32_t base = block_excl_scan256(c, wt, nullptr);
+        ss->ghist[p][d] = base;
+        const int triv = trivial;
+        if (d == 0) {
+            ss->pass_in[p] = cur;
+            ss->pass_do[p] = triv ? 0 : 1;
         }
-        if (lane == 0) {
-            total[d] = run;
-            if ((int64_t)run == n) trivial = 1;
-        }
+        if (!triv) cur ^= 1;
+        __syncthreads();
     }
-    __syncthreads();
-    if (n == 0) trivial = 1;
-    if (trivial) {
-        if (tid == 0) {
-            ctr->pass_in[slot] = *cur;
-            ctr->pass_do[slot] = 0;
-        }
-        return;
-    }
-    if (warp == 0) {  // exclusive scan of the RADIX digit totals (8 per lane)
-        uint32_t v[RADIX / 32], s = 0;
-#pragma unroll
-        for (int k = 0; k < RADIX / 32; k++) {
-            v[k] = total[lane * (RADIX / 32) + k];
-            s += v[k];
-        }
-        uint32_t x = s;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        uint32_t base = x - s;
-#pragma unroll
-        for (int k = 0; k < RADIX / 32; k++) {
-            total[lane * (RADIX / 32) + k] = base;
-            base += v[k];
-        }
-    }
-    __syncthreads();
-    for (int e = tid; e < RADIX * nblocks; e += blockDim.x) hist[e] += total[e / nblocks];
-    if (tid == 0) {
-        const int in = *cur;
-        ctr->pass_in[slot] = in;
-        ctr->pass_do[slot] = 1;
-        *cur = in ^ 1;
+    if (d == 0) {
+        ss->final_buf = cur;
+        *final_out = cur;
     }
 }
 
-// Downsweep: stable block-local ranking (warp match_any multi-split) and scatter.
-template <typename KT>
-__global__ void __launch_bounds__(SORT_THREADS) radix_downsweep(KT *keys0, KT *keys1, uint32_t *vals0, uint32_t *vals1,
-                                                                const unsigned long long *n_dev, int64_t n_host,
-                                                                int64_t cap, int shift, const uint32_t *hist,
-                                                                const DevCounters *ctr, int slot) {
-    if (!ctr->pass_do[slot]) return;
-    __shared__ uint32_t running[RADIX];
-    __shared__ uint32_t tot[RADIX];
-    __shared__ uint32_t wh[SORT_WARPS][RADIX];
+// One stable LSD radix pass ("onesweep"): local warp multi-split + decoupled look-back + staged scatter.
+template <typename KT, int IPT>
+__global__ void __launch_bounds__(OS_THREADS) onesweep(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1,
+                                                       const unsigned long long *n_dev, int64_t n_host, int64_t cap,
+                                                       int pass, int shift, SortState *ss, uint32_t *lookback) {
+    if (!ss->pass_do[pass]) return;
+    constexpr int TILE_ITEMS = OS_THREADS * IPT;
+    extern __shared__ __align__(16) unsigned char os_smem[];
+    KT *skey = reinterpret_cast<KT *>(os_smem);
+    uint32_t *sval = reinterpret_cast<uint32_t *>(os_smem + sizeof(KT) * TILE_ITEMS);
+    __shared__ uint32_t wh[OS_WARPS][RADIX];
+    __shared__ uint32_t loc[RADIX], gofs[RADIX], wt[8];
+    __shared__ int s_tile;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int in = ctr->pass_in[slot];
-    const KT *kin = in ? keys1 : keys0;
-    KT *kout = in ? keys0 : keys1;
-    const uint32_t *vin = in ? vals1 : vals0;
-    uint32_t *vout = in ? vals0 : vals1;
     const int64_t n = dev_count(n_dev, n_host, cap);
-    int64_t beg, end;
-    chunk_of(n, gridDim.x, blockIdx.x, beg, end);
-    for (int d = tid; d < RADIX; d += SORT_THREADS) running[d] = hist[d * gridDim.x + blockIdx.x];
+    const int64_t ntiles = (n + TILE_ITEMS - 1) / TILE_ITEMS;
+    if (tid == 0) s_tile = (int)atomicAdd(&ss->ticket[pass], 1u);
+    for (int e = lane; e < RADIX; e += 32) wh[warp][e] = 0;
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile >= ntiles) return;
+    const int in = ss->pass_in[pass];
+    const KT *kin = in ? k1 : k0;
+    KT *kout = in ? k0 : k1;
+    const uint32_t *vin = in ? v1 : v0;
+    uint32_t *vout = in ? v0 : v1;
+    const int64_t base = (int64_t)tile * TILE_ITEMS;
+    const int tile_n = (int)(n - base < TILE_ITEMS ? n - base : TILE_ITEMS);
+    const int64_t seg = base + (int64_t)warp * 32 * IPT;
+
+    KT k[IPT];
+    int dig[IPT];
+    uint32_t rank[IPT];
+#pragma unroll
+    for (int it = 0; it < IPT; it++) {
+        const int64_t idx = seg + it * 32 + lane;
+        const bool valid = idx < n;
+        k[it] = valid ? kin[idx] : (KT)0;
+        dig[it] = valid ? (int)((k[it] >> shift) & (RADIX - 1)) : RADIX;
+    }
     const unsigned lt = lanemask_lt();
-    constexpr int SEG = 32 * SORT_IPT;
-    for (int64_t tb = beg; tb < end; tb += SORT_THREADS * SORT_IPT) {
-        for (int d = lane; d < RADIX; d += 32) wh[warp][d] = 0;
+#pragma unroll
+    for (int it = 0; it < IPT; it++) {
+        const int d = dig[it];
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        uint32_t b = 0;
+        if (d < RADIX) b = wh[warp][d];
         __syncwarp();
-        const int64_t seg = tb + (int64_t)warp * SEG;
-        KT k[SORT_IPT];
-        uint32_t rank[SORT_IPT];
-        int dig[SORT_IPT];
+        if (d < RADIX && lane == (int)(__ffs(peers) - 1)) wh[warp][d] = b + __popc(peers);
+        __syncwarp();
+        rank[it] = b + __popc(peers & lt);
+    }
+    __syncthreads();
+    // per digit: exclusive prefix over warps, tile total; publish the aggregate right away
+    const int d = tid;
+    uint32_t total = 0;
 #pragma unroll
-        for (int it = 0; it < SORT_IPT; it++) {
-            const int64_t idx = seg + it * 32 + lane;
-            const bool valid = idx < end;
-            k[it] = valid ? kin[idx] : (KT)0;
-            dig[it] = valid ? (int)((k[it] >> shift) & (RADIX - 1)) : RADIX;
+    for (int w = 0; w < OS_WARPS; w++) {
+        const uint32_t v = wh[w][d];
+        wh[w][d] = total;
+        total += v;
+    }
+    volatile uint32_t *lb = lookback;
+    lb[(int64_t)tile * RADIX + d] = (tile == 0 ? LB_PRE : LB_AGG) | total;
+    const uint32_t lo = block_excl_scan256(total, wt, nullptr);
+    loc[d] = lo;
+    uint32_t excl = 0;
+    if (tile > 0) {
+        for (int t = tile - 1;;) {
+            const uint32_t v = lb[(int64_t)t * RADIX + d];
+            const uint32_t flag = v & ~LB_MASK;
+            if (flag == 0u) continue;  // predecessor has not published yet
+            excl += v & LB_MASK;
+            if (flag == LB_PRE) break;
+            t--;
         }
+        lb[(int64_t)tile * RADIX + d] = LB_PRE | (excl + total);
+    }
+    gofs[d] = ss->ghist[pass][d] + excl - lo;
+    __syncthreads();
+    // stage in local sorted order, then write coalesced runs
 #pragma unroll
-        for (int it = 0; it < SORT_IPT; it++) {
-            const int d = dig[it];
-            const unsigned peers = __match_any_sync(0xffffffffu, d);
-            const unsigned leader = __ffs(peers) - 1;
-            uint32_t base = 0;
-            if (d < RADIX) base = wh[warp][d];
-            __syncwarp();
-            if (d < RADIX && lane == (int)leader) wh[warp][d] = base + __popc(peers);
-            __syncwarp();
-            rank[it] = base + __popc(peers & lt);
+    for (int it = 0; it < IPT; it++) {
+        const int dd = dig[it];
+        if (dd < RADIX) {
+            const uint32_t lp = loc[dd] + wh[warp][dd] + rank[it];
+            skey[lp] = k[it];
+            sval[lp] = vin[seg + it * 32 + lane];
         }
-        __syncthreads();
-        for (int d = tid; d < RADIX; d += SORT_THREADS) {
-            uint32_t s = 0;
-#pragma unroll
-            for (int w = 0; w < SORT_WARPS; w++) {
-                const uint32_t v = wh[w][d];
-                wh[w][d] = s;
-                s += v;
-            }
-            tot[d] = s;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int it = 0; it < SORT_IPT; it++) {
-            const int d = dig[it];
-            if (d < RADIX) {
-                const int64_t idx = seg + it * 32 + lane;
-                const uint32_t pos = running[d] + wh[warp][d] + rank[it];
-                kout[pos] = k[it];
-                vout[pos] = vin[idx];
-            }
-        }
-        __syncthreads();
-        for (int d = tid; d < RADIX; d += SORT_THREADS) running[d] += tot[d];
-        __syncthreads();
+    }
+    __syncthreads();
+    for (int i = tid; i < tile_n; i += OS_THREADS) {
+        const KT key = skey[i];
+        const uint32_t pos = gofs[(unsigned)(key >> shift) & (RADIX - 1)] + (uint32_t)i;
+        kout[pos] = key;
+        vout[pos] = sval[i];
     }
 }
 
-template <typename KT>
-void radix_sort(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, int *cur, const unsigned long long *n_dev, int64_t n_host,
-                int64_t cap, int bits, int first_slot, const unsigned long long *range, uint32_t *hist,
-                DevCounters *ctr, cudaStream_t st) {
-    const int passes = (bits + RADIX_BITS - 1) / RADIX_BITS;
-    for (int p = 0; p < passes; p++) {
-        const int shift = p * RADIX_BITS;
-        radix_upsweep<KT><<<SORT_BLOCKS, SORT_THREADS, 0, st>>>(k0, k1, cur, n_dev, n_host, cap, shift, range, hist);
-        radix_scan<<<1, 1024, 0, st>>>(hist, SORT_BLOCKS, n_dev, n_host, cap, cur, ctr, first_slot + p);
-        radix_downsweep<KT><<<SORT_BLOCKS, SORT_THREADS, 0, st>>>(k0, k1, v0, v1, n_dev, n_host, cap, shift, hist, ctr,
-                                                                   first_slot + p);
+template <typename KT, int IPT>
+constexpr int onesweep_smem() {
+    return (int)((sizeof(KT) + sizeof(uint32_t)) * OS_THREADS * IPT);
+}
+
+template <typename KT, int IPT>
+cudaError_t launch_onesweep(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const unsigned long long *n_dev,
+                            int64_t n_host, int64_t cap, int pass, SortState *ss, uint32_t *lookback,
+                            cudaStream_t st) {
+    static bool configured = false;
+    constexpr int smem = onesweep_smem<KT, IPT>();
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(onesweep<KT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
     }
+    const int64_t tiles = div_up(n_dev ? cap : n_host, OS_THREADS * IPT);
+    onesweep<KT, IPT><<<(unsigned)(tiles > 0 ? tiles : 1), OS_THREADS, smem, st>>>(k0, k1, v0, v1, n_dev, n_host, cap,
+                                                                                    pass, RADIX_BITS * pass, ss,
+                                                                                    lookback + (int64_t)pass * RADIX * tiles);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- K3 / K4
-// Per-block sums of the tile counts, taken in depth order.
-__global__ void __launch_bounds__(SCAN_THREADS) count_upsweep(const uint32_t *idx0, const uint32_t *idx1,
-                                                              const DevCounters *ctr, const uint32_t *touched,
-                                                              int64_t P, unsigned long long *blocksum) {
+__global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx0, const uint32_t *idx1,
+                                                             const DevCounters *ctr, const uint32_t *touched,
+                                                             int64_t P, unsigned long long *blocksum) {
     const uint32_t *order = ctr->depth_cur ? idx1 : idx0;
-    int64_t beg, end;
-    chunk_of(P, gridDim.x, blockIdx.x, beg, end);
+    const int64_t beg = (int64_t)blockIdx.x * DUP_ITEMS;
     unsigned long long s = 0;
-    for (int64_t i = beg + threadIdx.x; i < end; i += SCAN_THREADS) s += touched[order[i]];
+#pragma unroll
+    for (int u = 0; u < DUP_ITEMS / DUP_THREADS; u++) {
+        const int64_t i = beg + u * DUP_THREADS + threadIdx.x;
+        if (i < P) s += touched[order[i]];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    __shared__ unsigned long long ws[SCAN_THREADS / 32];
+    __shared__ unsigned long long ws[DUP_THREADS / 32];
     if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long t = 0;
-        for (int w = 0; w < SCAN_THREADS / 32; w++) t += ws[w];
+        for (int w = 0; w < DUP_THREADS / 32; w++) t += ws[w];
         blocksum[blockIdx.x] = t;
     }
 }
 
-__global__ void count_scan(unsigned long long *blocksum, int nblocks, DevCounters *ctr, int64_t cap) {
-    if (threadIdx.x != 0) return;
-    unsigned long long run = 0;
-    for (int b = 0; b < nblocks; b++) {
+// Exclusive scan of the per-block counts (one CTA of 1024 threads) -> write offsets and N.
+__global__ void __launch_bounds__(1024) count_scan(unsigned long long *blocksum, int nblocks, DevCounters *ctr,
+                                                   int64_t cap) {
+    __shared__ unsigned long long wt[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (nblocks + 1023) / 1024;
+    const int b0 = tid * per;
+    unsigned long long s = 0;
+    for (int b = b0; b < b0 + per && b < nblocks; b++) s += blocksum[b];
+    unsigned long long x = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wt[warp] = x;
+    __syncthreads();
+    unsigned long long pre = 0, tot = 0;
+    for (int w = 0; w < 32; w++) {
+        pre += w < warp ? wt[w] : 0ull;
+        tot += wt[w];
+    }
+    unsigned long long run = pre + x - s;
+    for (int b = b0; b < b0 + per && b < nblocks; b++) {
         const unsigned long long v = blocksum[b];
         blocksum[b] = run;
         run += v;
     }
-    ctr->n_splats = run;
-    ctr->overflow = run > (unsigned long long)cap ? 1ull : 0ull;
-    ctr->tile_cur = 0;
+    if (tid == 0) {
+        ctr->n_splats = tot;
+        ctr->overflow = tot > (unsigned long long)cap ? 1ull : 0ull;
+    }
 }
 
-// K4: duplicate-with-keys.  Each block walks its chunk 256 Gaussians at a time, scans their
-// counts, then expands the (Gaussian, covered tile) pairs cooperatively: consecutive threads
-// write consecutive splats (binary search of the slot in the shared scan).
-__global__ void __launch_bounds__(SCAN_THREADS) duplicate_keys(const uint32_t *idx0, const uint32_t *idx1,
-                                                               const DevCounters *ctr, const uint32_t *touched,
-                                                               const short4 *rect, int64_t P,
-                                                               const unsigned long long *blockoff, int tiles_x,
-                                                               int band_y0, int64_t cap, uint32_t *tkey,
-                                                               uint32_t *tval) {
-    __shared__ uint32_t incl[SCAN_THREADS];
-    __shared__ uint32_t gid[SCAN_THREADS];
-    __shared__ short4 rc[SCAN_THREADS];
-    __shared__ uint32_t wsum[SCAN_THREADS / 32];
+// K4: duplicate-with-keys.  Each CTA walks DUP_ITEMS depth-ordered Gaussians 256 at a time, scans their
+// tile counts, then expands (Gaussian, covered tile) pairs cooperatively: consecutive threads write
+// consecutive splats (binary search of the slot in the shared inclusive scan).  The tile-key digits are
+// histogrammed for K5 in the same pass.
+template <typename KT>
+__global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *idx0, const uint32_t *idx1,
+                                                              const DevCounters *ctr, const uint32_t *touched,
+                                                              const short4 *rect, int64_t P,
+                                                              const unsigned long long *blockoff, int tiles_x,
+                                                              int band_y0, int64_t cap, KT *tkey, uint32_t *tval,
+                                                              SortState *ss, int npass) {
+    __shared__ uint32_t incl[DUP_THREADS];
+    __shared__ uint32_t gid[DUP_THREADS];
+    __shared__ short4 rc[DUP_THREADS];
+    __shared__ uint32_t wt[8];
+    __shared__ uint32_t h[TILE_MAX_PASSES][RADIX];
     const uint32_t *order = ctr->depth_cur ? idx1 : idx0;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    int64_t beg, end;
-    chunk_of(P, gridDim.x, blockIdx.x, beg, end);
+    const int tid = threadIdx.x;
+    for (int e = tid; e < TILE_MAX_PASSES * RADIX; e += DUP_THREADS) (&h[0][0])[e] = 0;
+    const int64_t beg = (int64_t)blockIdx.x * DUP_ITEMS;
     unsigned long long base = blockoff[blockIdx.x];
-    for (int64_t tb = beg; tb < end; tb += SCAN_THREADS) {
-        const int64_t i = tb + tid;
+    for (int r = 0; r < DUP_ITEMS / DUP_THREADS; r++) {
+        const int64_t i = beg + r * DUP_THREADS + tid;
         uint32_t c = 0, g = 0;
-        short4 r = make_short4(0, 0, -1, -1);
-        if (i < end) {
+        short4 q = make_short4(0, 0, -1, -1);
+        if (i < P) {
             g = order[i];
             c = touched[g];
-            if (c) r = rect[g];
+            if (c) q = rect[g];
         }
-        uint32_t x = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) wsum[warp] = x;
-        __syncthreads();
-        uint32_t wpre = 0, total = 0;
-#pragma unroll
-        for (int w = 0; w < SCAN_THREADS / 32; w++) {
-            const uint32_t s = wsum[w];
-            if (w < warp) wpre += s;
-            total += s;
-        }
-        incl[tid] = wpre + x;
+        uint32_t total;
+        const uint32_t ex = block_excl_scan256(c, wt, &total);
+        incl[tid] = ex + c;
         gid[tid] = g;
-        rc[tid] = r;
+        rc[tid] = q;
         __syncthreads();
-        for (uint32_t s = tid; s < total; s += SCAN_THREADS) {
-            int lo = 0, hi = SCAN_THREADS - 1;  // first item with incl > s
-            while (lo < hi) {
+        for (uint32_t s = tid; s < total; s += DUP_THREADS) {
+            int lo = 0, hi = DUP_THREADS - 1;  // first item whose inclusive count exceeds s
+#pragma unroll 8
+            for (int step = 0; step < 8; step++) {
                 const int mid = (lo + hi) >> 1;
                 if (incl[mid] > s) hi = mid;
                 else lo = mid + 1;
             }
-            const uint32_t k = s - (lo ? incl[lo - 1] : 0u);
-            const short4 q = rc[lo];
-            const int w = q.z - q.x + 1;
-            const int ty = q.y + (int)(k / w), tx = q.x + (int)(k % w);
+            const uint32_t kk = s - (lo ? incl[lo - 1] : 0u);
+            const short4 qq = rc[lo];
+            const int w = qq.z - qq.x + 1;
+            const int ty = qq.y + (int)(kk / w), tx = qq.x + (int)(kk % w);
+            const uint32_t key = (uint32_t)((ty - band_y0) * tiles_x + tx);
             const unsigned long long pos = base + s;
             if (pos < (unsigned long long)cap) {
-                tkey[pos] = (uint32_t)((ty - band_y0) * tiles_x + tx);
+                tkey[pos] = (KT)key;
                 tval[pos] = gid[lo];
+                for (int p = 0; p < npass; p++) atomicAdd(&h[p][(key >> (RADIX_BITS * p)) & (RADIX - 1)], 1u);
             }
         }
         base += total;
         __syncthreads();
     }
+    for (int e = tid; e < npass * RADIX; e += DUP_THREADS) {
+        const uint32_t c = (&h[0][0])[e];
+        if (c) atomicAdd(&(&ss->ghist[0][0])[e], c);
+    }
 }
 
-// K6: tile ranges from the sorted keys.
-__global__ void tile_ranges(const uint32_t *k0, const uint32_t *k1, const DevCounters *ctr, int64_t cap, uint2 *ranges) {
-    const uint32_t *keys = ctr->tile_cur ? k1 : k0;
+// K6: tile ranges from the sorted keys (4 consecutive keys per thread).
+template <typename KT>
+__global__ void tile_ranges(const KT *k0, const KT *k1, const DevCounters *ctr, int64_t cap, uint2 *ranges) {
+    const KT *keys = ctr->tile_cur ? k1 : k0;
     const unsigned long long nn = ctr->n_splats;
     const int64_t n = (int64_t)(nn < (unsigned long long)cap ? nn : (unsigned long long)cap);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t t = keys[i];
-        if (i == 0 || keys[i - 1] != t) ranges[t].x = (uint32_t)i;
-        if (i == n - 1 || keys[i + 1] != t) ranges[t].y = (uint32_t)(i + 1);
+    for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i0 < n;
+         i0 += (int64_t)gridDim.x * blockDim.x * 4) {
+        uint32_t prev = i0 > 0 ? (uint32_t)keys[i0 - 1] : 0xffffffffu;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int64_t i = i0 + u;
+            if (i >= n) break;
+            const uint32_t t = keys[i];
+            if (t != prev) {
+                ranges[t].x = (uint32_t)i;
+                if (prev != 0xffffffffu) ranges[prev].y = (uint32_t)i;
+            }
+            prev = t;
+        }
+        if (i0 + 4 >= n && prev != 0xffffffffu) ranges[prev].y = (uint32_t)n;
     }
 }
 
@@ -390,6 +414,38 @@ __global__ void pack_ranges(const int64_t *offsets, int band_tile0, int n_tiles,
     ranges[t] = make_uint2((uint32_t)offsets[band_tile0 + t], (uint32_t)offsets[band_tile0 + t + 1]);
 }
 
+template <typename KT>
+cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st) {
+    DevCounters *ctr = at<DevCounters>(ws, L.counters);
+    SortState *ss_tile = at<SortState>(ws, L.sort_state[1]);
+    const int bits = tile_key_bits(band);
+    const int npass = (bits + RADIX_BITS - 1) / RADIX_BITS;
+    KT *tk0 = at<KT>(ws, L.tkey[0]);
+    KT *tk1 = at<KT>(ws, L.tkey[1]);
+    uint32_t *tv0 = at<uint32_t>(ws, L.tval[0]);
+    uint32_t *tv1 = at<uint32_t>(ws, L.tval[1]);
+    unsigned long long *blocksum = at<unsigned long long>(ws, L.blocksum);
+    const int nblk = (int)div_up(P > 0 ? P : 1, DUP_ITEMS);
+    // K3
+    count_upsweep<<<nblk, DUP_THREADS, 0, st>>>(at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr,
+                                                 at<uint32_t>(ws, L.touched), P, blocksum);
+    count_scan<<<1, 1024, 0, st>>>(blocksum, nblk, ctr, cap);
+    // K4
+    duplicate_keys<KT><<<nblk, DUP_THREADS, 0, st>>>(at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr,
+                                                      at<uint32_t>(ws, L.touched), at<short4>(ws, L.rect), P,
+                                                      blocksum, band.tiles_x, band.y0, cap, tk0, tv0, ss_tile, npass);
+    // K5
+    sort_plan<<<1, 256, 0, st>>>(ss_tile, npass, &ctr->n_splats, 0, cap, nullptr, &ctr->tile_cur);
+    for (int p = 0; p < npass; p++) {
+        cudaError_t e = launch_onesweep<KT, TILEKEY_IPT>(tk0, tk1, tv0, tv1, &ctr->n_splats, 0, cap, p, ss_tile,
+                                                          at<uint32_t>(ws, L.lb_tile), st);
+        if (e != cudaSuccess) return e;
+    }
+    // K6
+    tile_ranges<KT><<<4 * 148, 256, 0, st>>>(tk0, tk1, ctr, cap, at<uint2>(ws, L.ranges));
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 int tile_key_bits(const Band &band) {
@@ -399,40 +455,34 @@ int tile_key_bits(const Band &band) {
     return bits;
 }
 
+int bin_launch_count(int64_t P, const Band &band) {
+    const int npass = (tile_key_bits(band) + RADIX_BITS - 1) / RADIX_BITS;
+    return (P > 0 ? 2 + MAX_PASSES : 0) + 3 + 1 + npass + 1;
+}
+
 cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st) {
     DevCounters *ctr = at<DevCounters>(ws, L.counters);
-    uint32_t *hist = at<uint32_t>(ws, L.hist);
+    SortState *ss_depth = at<SortState>(ws, L.sort_state[0]);
+    cudaError_t e = cudaMemsetAsync(static_cast<char *>(ws) + L.zero_begin, 0, L.zero_bytes, st);
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync(at<uint2>(ws, L.ranges), 0, sizeof(uint2) * (size_t)(band.n_tiles() ? band.n_tiles() : 1), st);
+    if (e != cudaSuccess) return e;
     unsigned long long *k0 = at<unsigned long long>(ws, L.key64[0]);
     unsigned long long *k1 = at<unsigned long long>(ws, L.key64[1]);
     uint32_t *i0 = at<uint32_t>(ws, L.idx[0]);
     uint32_t *i1 = at<uint32_t>(ws, L.idx[1]);
-    uint32_t *tk0 = at<uint32_t>(ws, L.tkey[0]);
-    uint32_t *tk1 = at<uint32_t>(ws, L.tkey[1]);
-    uint32_t *tv0 = at<uint32_t>(ws, L.tval[0]);
-    uint32_t *tv1 = at<uint32_t>(ws, L.tval[1]);
-    unsigned long long *blocksum = at<unsigned long long>(ws, L.blocksum);
-    uint2 *ranges = at<uint2>(ws, L.ranges);
-    cudaError_t e = cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)(band.n_tiles() ? band.n_tiles() : 1), st);
-    if (e != cudaSuccess) return e;
     if (P > 0) {
-        depth_key_fix<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(k0, P, ctr);
-        // K2: key_range = max - min bounds every fixed key, so passes above its top bit are skipped
-        radix_sort<unsigned long long>(k0, k1, i0, i1, &ctr->depth_cur, nullptr, P, P, 64, 0, &ctr->key_range, hist,
-                                       ctr, st);
+        // K2
+        depth_fix_hist<<<2 * 148, 256, 0, st>>>(k0, P, ctr, ss_depth);
+        sort_plan<<<1, 256, 0, st>>>(ss_depth, MAX_PASSES, nullptr, P, P, &ctr->key_range, &ctr->depth_cur);
+        for (int p = 0; p < MAX_PASSES; p++) {
+            e = launch_onesweep<unsigned long long, DEPTH_IPT>(k0, k1, i0, i1, nullptr, P, P, p, ss_depth,
+                                                               at<uint32_t>(ws, L.lb_depth), st);
+            if (e != cudaSuccess) return e;
+        }
     }
-    // K3
-    count_upsweep<<<SCAN_BLOCKS, SCAN_THREADS, 0, st>>>(i0, i1, ctr, at<uint32_t>(ws, L.touched), P, blocksum);
-    count_scan<<<1, 32, 0, st>>>(blocksum, SCAN_BLOCKS, ctr, cap);
-    // K4
-    duplicate_keys<<<SCAN_BLOCKS, SCAN_THREADS, 0, st>>>(i0, i1, ctr, at<uint32_t>(ws, L.touched),
-                                                          at<short4>(ws, L.rect), P, blocksum, band.tiles_x, band.y0,
-                                                          cap, tk0, tv0);
-    // K5
-    radix_sort<uint32_t>(tk0, tk1, tv0, tv1, &ctr->tile_cur, &ctr->n_splats, 0, cap, tile_key_bits(band),
-                         TILE_PASS_SLOT, nullptr, hist, ctr, st);
-    // K6
-    tile_ranges<<<4 * 148, 256, 0, st>>>(tk0, tk1, ctr, cap, ranges);
-    return cudaGetLastError();
+    if (band.n_tiles() <= 65536) return bin_tiles<uint16_t>(P, band, ws, L, cap, st);
+    return bin_tiles<uint32_t>(P, band, ws, L, cap, st);
 }
 
 cudaError_t launch_pack_lists(int64_t P, const double *mean2d, const double *conic, const double *opacity,

@@ -12,14 +12,14 @@ namespace tcgs {
 constexpr int TILE = 16;              // src/tilesplat/tiling.py:11
 constexpr int RADIX_BITS = 8;
 constexpr int RADIX = 1 << RADIX_BITS;
-constexpr int SORT_BLOCKS = 296;      // 2 x 148 SMs: fixed grid, chunks sized from the device-side count
-constexpr int SORT_THREADS = 256;
-constexpr int SORT_WARPS = SORT_THREADS / 32;
-constexpr int SORT_IPT = 16;          // items per thread per tile in the downsweep
-constexpr int SCAN_BLOCKS = 296;
-constexpr int SCAN_THREADS = 256;
+constexpr int OS_THREADS = 256;       // onesweep radix pass: 8 warps per CTA
+constexpr int OS_WARPS = OS_THREADS / 32;
+constexpr int DEPTH_IPT = 8;          // items per thread: depth sort (u64 keys), 2048-item tiles
+constexpr int TILEKEY_IPT = 16;       // items per thread: tile-key sort, 4096-item tiles
 constexpr int MAX_PASSES = 8;         // depth key: <= 64 bits
-constexpr int TILE_PASS_SLOT = 8;     // pass bookkeeping slots 8.. are the tile-key passes
+constexpr int TILE_MAX_PASSES = 4;    // tile key: <= 32 bits
+constexpr int DUP_ITEMS = 1024;       // Gaussians per duplicate-with-keys CTA
+constexpr int DUP_THREADS = 256;
 
 constexpr int K7_CONSUMER_WARPS = 8;  // one pixel per thread, 16x16 tile
 constexpr int K7_THREADS = 32 * (K7_CONSUMER_WARPS + 1);  // + one producer / MMA-issue warp
@@ -43,15 +43,26 @@ struct DevCounters {
     unsigned long long key_min, key_max, key_range;
     unsigned int tile_queue;
     int depth_cur, tile_cur;
-    int pass_in[16];
-    int pass_do[16];
+};
+
+// Per-sort bookkeeping of the onesweep LSD radix sort (all decided on the device).
+struct SortState {
+    unsigned int ghist[MAX_PASSES][RADIX];  // digit counts, then exclusive global bases
+    int pass_do[MAX_PASSES];                // 0: the pass is the identity (one digit value or above the key range)
+    int pass_in[MAX_PASSES];                // ping-pong buffer the pass reads
+    unsigned int ticket[MAX_PASSES];        // in-order tile tickets (decoupled look-back)
+    int final_buf;
+    int pad[3];
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
 struct Layout {
-    size_t counters, rec, rect, touched, key64[2], idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
-    size_t hist, blocksum, tkey[2], tval[2], ranges, total;
+    size_t counters, sort_state[2], rec, rect, touched, key64[2], idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
+    size_t blocksum, lb_depth, lb_tile, tkey[2], tval[2], ranges, total;
+    size_t zero_begin, zero_bytes;  // sort state + look-back flags, cleared at the start of every binning
     static Layout make(int64_t P, int W, int H, int64_t cap) {
         Layout L;
         size_t o = 0;
@@ -59,6 +70,12 @@ struct Layout {
         size_t nt = (size_t)((W + TILE - 1) / TILE) * (size_t)((H + TILE - 1) / TILE);
         auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
         L.counters = take(sizeof(DevCounters));
+        L.zero_begin = o;
+        L.sort_state[0] = take(sizeof(SortState));
+        L.sort_state[1] = take(sizeof(SortState));
+        L.lb_depth = take(sizeof(uint32_t) * RADIX * MAX_PASSES * (size_t)div_up((int64_t)Pn, OS_THREADS * DEPTH_IPT));
+        L.lb_tile = take(sizeof(uint32_t) * RADIX * TILE_MAX_PASSES * (size_t)div_up((int64_t)cn, OS_THREADS * TILEKEY_IPT));
+        L.zero_bytes = o - L.zero_begin;
         L.rec = take(sizeof(Rec) * Pn);
         L.rect = take(sizeof(short4) * Pn);
         L.touched = take(sizeof(uint32_t) * Pn);
@@ -70,8 +87,7 @@ struct Layout {
         L.dbg_conic = take(sizeof(double) * 3 * Pn);
         L.dbg_depth = take(sizeof(double) * Pn);
         L.dbg_mean2d = take(sizeof(double) * 2 * Pn);
-        L.hist = take(sizeof(uint32_t) * RADIX * SORT_BLOCKS);
-        L.blocksum = take(sizeof(unsigned long long) * SCAN_BLOCKS);
+        L.blocksum = take(sizeof(unsigned long long) * (size_t)div_up((int64_t)Pn, DUP_ITEMS));
         L.tkey[0] = take(sizeof(uint32_t) * cn);
         L.tkey[1] = take(sizeof(uint32_t) * cn);
         L.tval[0] = take(sizeof(uint32_t) * cn);

@@ -44,6 +44,7 @@ def explain_count_mismatches(gpu_counts, ref_counts, offsets, ids, mean2d, inv_c
         ox, oy = (x // 16) * 16 + 8.0, (y // 16) * 16 + 8.0
         u = np.array([1.0, x - ox, y - oy, (x - ox) ** 2, (x - ox) * (y - oy), (y - oy) ** 2])
         T = 1.0
+        rel_T = 0.0  # first-order relative error of T accumulated through the blended fragments
         near = False
         for g in ids[offsets[t]:offsets[t + 1]]:
             v = gaussian_vector(mean2d[g, 0], mean2d[g, 1], *inv_cov[g], opacity[g], ox, oy)
@@ -56,11 +57,13 @@ def explain_count_mismatches(gpu_counts, ref_counts, offsets, ids, mean2d, inv_c
                 continue
             a = min(math.exp(beta), 1.0)
             tn = T - a * T
-            if abs(tn - 1e-4) <= 1e-4 * (4.0 * band + 1e-3):
+            err = tn * rel_T + T * a * (math.exp(band) - 1.0) + 1e-7
+            if abs(tn - 1e-4) <= err:
                 near = True
                 break
             if tn < 1e-4:
                 break
+            rel_T += a * band / max(1.0 - a, 1e-6) + 2e-7
             T = tn
         if not near:
             unexplained.append((int(x), int(y), int(gpu_counts[y, x]), int(ref_counts[y, x])))

@@ -161,20 +161,23 @@ __device__ __forceinline__ bool gaussian_coeffs(const Rec &r, double ox, double 
     const float dx = (float)(r.mx - ox), dy = (float)(r.my - oy);
     const float s11 = r.s11, s12 = r.s12, s22 = r.s22;
     const float q = s11 * dx * dx + 2.0f * s12 * dx * dy + s22 * dy * dy;
-    if (s11 > 0.0f && s22 > 0.0f && !(dx >= -8.0f && dx <= 7.0f && dy >= -8.0f && dy <= 7.0f)) {
+    const bool outside = !(dx >= -8.0f && dx <= 7.0f && dy >= -8.0f && dy <= 7.0f);
+    if (outside && s11 > 0.0f && s22 > 0.0f) {
+        // (the minimiser only needs to be accurate to first order: q is flat there, and the test keeps a margin)
+        const float r11 = __fdividef(s12, s11), r22 = __fdividef(s12, s22);
         float qmin = 3.0e38f;
 #pragma unroll
         for (int e = 0; e < 2; e++) {
             const float a = e ? 7.0f : -8.0f;
             {  // edge ux = a
                 const float ex = dx - a;
-                const float uy = fminf(fmaxf(dy + s12 * ex / s22, -8.0f), 7.0f);
+                const float uy = fminf(fmaxf(dy + r22 * ex, -8.0f), 7.0f);
                 const float ey = dy - uy;
                 qmin = fminf(qmin, s11 * ex * ex + 2.0f * s12 * ex * ey + s22 * ey * ey);
             }
             {  // edge uy = a
                 const float ey = dy - a;
-                const float ux = fminf(fmaxf(dx + s12 * ey / s11, -8.0f), 7.0f);
+                const float ux = fminf(fmaxf(dx + r11 * ey, -8.0f), 7.0f);
                 const float ex = dx - ux;
                 qmin = fminf(qmin, s11 * ex * ex + 2.0f * s12 * ex * ey + s22 * ey * ey);
             }
@@ -307,19 +310,20 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
         int fill = 0;
         uint32_t dead = 0;
         bool retired = false;
-        // software pipeline: the next chunk's id and record are in flight while this one is processed
+        // software pipeline: list ids two chunks ahead, records one chunk ahead of the chunk being processed
+        const uint32_t *lst = ids + rg.x;
+        uint32_t id_next = (32 + lane < n) ? lst[32 + lane] : 0u;
         Rec nr;
-        bool nvalid = lane < n;
-        if (nvalid) nr = a.rec[ids[rg.x + lane]];
+        if (lane < n) nr = a.rec[lst[lane]];
         for (int base = 0; base < n; base += 32) {
             if (*((volatile int *)&sm.retire[sq & 7]) >= K7_CONSUMER_WARPS) {
                 retired = true;
                 break;
             }
             const Rec r = nr;
-            const bool valid = nvalid;
-            nvalid = base + 32 + lane < n;
-            if (nvalid) nr = a.rec[ids[rg.x + base + 32 + lane]];
+            const bool valid = base + lane < n;
+            if (base + 32 + lane < n) nr = a.rec[id_next];
+            id_next = (base + 64 + lane < n) ? lst[base + 64 + lane] : 0u;
             float v[6];
             const bool live = valid && gaussian_coeffs(r, ox, oy, v);
             const unsigned lm = __ballot_sync(FULL, live), dm = __ballot_sync(FULL, valid && !live);
@@ -463,26 +467,24 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 int jt = 32;
 #pragma unroll
                 for (int j = 0; j < 32; j++) {
-                    if (wm & (1u << j)) {
-                        if (((pass >> j) & 1u) && !done) {
-                            const float al = fminf(ex2_approx(__uint_as_float(r[j])), 1.0f);
-                            const float tn = fmaf(-al, T, T);
-                            if (tn < TERM_T) {
-                                done = true;
-                                term = true;
-                                jt = j;
-                            } else {
-                                const float w = al * T;
-                                const float4 cc = sm.col[st][j];
-                                c0 = fmaf(w, cc.x, c0);
-                                c1 = fmaf(w, cc.y, c1);
-                                c2 = fmaf(w, cc.z, c2);
-                                T = tn;
-                                cnt++;
-                            }
-                        }
+                    if (wm & (1u << j)) {  // warp-uniform: some pixel of the warp passes EarlyCull here
+                        const bool p = ((pass >> j) & 1u) && !done;
+                        const float al = fminf(ex2_approx(__uint_as_float(r[j])), 1.0f);
+                        const float tn = fmaf(-al, T, T);
+                        const bool stop = p && tn < TERM_T;  // termination precedes compositing
+                        const bool blend = p && !(tn < TERM_T);
+                        const float w = blend ? al * T : 0.0f;
+                        const float4 cc = sm.col[st][j];
+                        c0 = fmaf(w, cc.x, c0);
+                        c1 = fmaf(w, cc.y, c1);
+                        c2 = fmaf(w, cc.z, c2);
+                        T = blend ? tn : T;
+                        cnt += blend ? 1u : 0u;
+                        jt = stop ? j : jt;
+                        done = done || stop;
                     }
                 }
+                term = term || jt < 32;
                 // EarlyCull counts: live columns failing the cut before termination, plus the dead
                 // Gaussians of the list before the terminating one
                 const uint32_t before = jt >= 32 ? FULL : ((1u << jt) - 1u);

@@ -76,9 +76,11 @@ struct __align__(1024) K7Smem {
     float4 col[S][K7_BATCH];            // colours
     uint32_t dead_before[S][K7_BATCH];  // dead Gaussians before each live one (list order)
     StageMeta meta[S];
-    unsigned long long full[S], empty[S], mma_done[NB], tmem_empty[NB];
+    unsigned long long full[S], empty[S], mma_done[NB], tmem_empty[NB], tok[K7_PRODUCERS];
     uint32_t tmem_base;
     int retire[8];
+    int c_fill, c_k, c_open;  // compaction state: touched only by the producer holding the token
+    uint32_t c_dead;
     unsigned long long red[K7_CONSUMER_WARPS][4];
 };
 
@@ -150,6 +152,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
           "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
         : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Gaussian coefficients for one tile (gaussian_vector, src/tilesplat/tensor_path.py:25-40) relative to the
@@ -196,13 +206,22 @@ __device__ __forceinline__ bool gaussian_coeffs(const Rec &r, double ox, double 
 __device__ __forceinline__ __half h16(float x) { return __float2half_rn(x); }
 __device__ __forceinline__ float f32(__half x) { return __half2float(x); }
 
-// One B-operand row (16 fp16) for MODE: hi/lo split (0) or the paper's K8 vector (1).
+// One B-operand row (16 fp16, as two uint4) for MODE: hi/lo split (0) or the paper's K8 vector (1).
 // U row: [1, 1, 1, ux, uy, ux^2, ux uy, uy^2, ux, uy, ux^2, ux uy, uy^2, 1, 0, 0]
 template <int MODE>
-__device__ __forceinline__ void write_vrow(__half *V, int row, const float v[6]) {
+__device__ __forceinline__ void make_vrow(const float v[6], uint4 &lo8, uint4 &hi8) {
     __align__(16) __half e[16];
-    if (MODE == TCGS_ALPHA_TC_HILO) {
-        const __half a = h16(v[0]);  // v0 = a + b + c + d
+    if (MODE == TCGS_ALPHA_TC_K8) {  // [v0/3, v0/3, v0/3, v1..v5] in fp16, the rest zero
+        const __half third = h16(v[0] / 3.0f);
+        e[0] = third;
+        e[1] = third;
+        e[2] = third;
+#pragma unroll
+        for (int i = 1; i <= 5; i++) e[2 + i] = h16(v[i]);
+#pragma unroll
+        for (int k = 8; k < 16; k++) e[k] = h16(0.0f);
+    } else {  // hi/lo: v0 = a + b + c + d (four fp16 pieces), v1..v5 = hi + lo
+        const __half a = h16(v[0]);
         const float r1 = v[0] - f32(a);
         const __half b = h16(r1);
         const float r2 = r1 - f32(b);
@@ -220,131 +239,198 @@ __device__ __forceinline__ void write_vrow(__half *V, int row, const float v[6])
         e[13] = d;
         e[14] = h16(0.0f);
         e[15] = h16(0.0f);
-    } else {  // TCGS_ALPHA_TC_K8: [v0/3, v0/3, v0/3, v1..v5] in fp16, the rest zero
-        const __half third = h16(v[0] / 3.0f);
-        e[0] = third;
-        e[1] = third;
-        e[2] = third;
-#pragma unroll
-        for (int i = 1; i <= 5; i++) e[2 + i] = h16(v[i]);
-#pragma unroll
-        for (int k = 8; k < 16; k++) e[k] = h16(0.0f);
     }
-    const uint4 *src = reinterpret_cast<const uint4 *>(e);
-    *reinterpret_cast<uint4 *>(V + kmaj_off(row, 0)) = src[0];
-    *reinterpret_cast<uint4 *>(V + kmaj_off(row, 8)) = src[1];
+    lo8 = reinterpret_cast<const uint4 *>(e)[0];
+    hi8 = reinterpret_cast<const uint4 *>(e)[1];
 }
 
-// ------------------------------------------------------------------------------------------ producer
+// ------------------------------------------------------------------------------------------ producers
+// The CTA's tile stream is static (tiles blockIdx.x, +gridDim.x, ...); each tile contributes
+// max(1, ceil(n/32)) chunks of 32 list entries, and one "end" chunk closes the stream.  Producer warp p
+// owns chunks p, p + NP, ...: it gathers and evaluates its chunk in parallel with the other producer,
+// then waits for the compaction token, places its live rows into the current stage, emits full stages
+// (issuing their MMAs) and passes the token on.
+struct Cursor {
+    int tile, seq, c, chunks, n;
+    uint32_t beg;
+};
+
+__device__ __forceinline__ void cursor_tile(Cursor &k, const RenderArgs &a) {
+    k.c = 0;
+    if (k.tile < a.n_tiles) {
+        const uint2 rg = a.ranges[k.tile];
+        k.beg = rg.x;
+        k.n = (int)(rg.y - rg.x);
+        k.chunks = k.n > 0 ? (k.n + 31) / 32 : 1;
+    } else {
+        k.beg = 0;
+        k.n = 0;
+        k.chunks = 1;
+    }
+}
+
+__device__ __forceinline__ void cursor_next(Cursor &k, const RenderArgs &a) {
+    if (++k.c >= k.chunks) {
+        k.tile += gridDim.x;
+        k.seq++;
+        cursor_tile(k, a);
+    }
+}
+
 template <int MODE>
-__device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, uint32_t tmem) {
+__device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, uint32_t tmem, int p) {
     constexpr bool TC = MODE != TCGS_ALPHA_FFMA;
+    constexpr int NP = K7_PRODUCERS;
     const int lane = threadIdx.x & 31;
     const unsigned FULL = 0xffffffffu, lt = lanemask_lt();
-    int k = 0;                  // stage sequence number
-    int seq = 0;                // tile sequence number
-    bool open = false;          // stage k % S acquired
-    auto acquire = [&]() {
-        if (!open) {
-            mbar_wait(&sm.empty[k % S], ((k / S) & 1) ^ 1);
-            open = true;
-        }
-    };
-    auto emit = [&](int tile, int sq, int n_live, int last, uint32_t dead_total, uint32_t n_total) {
-        acquire();
-        const int st = k % S;
-        if (TC) fence_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-            StageMeta m;
-            m.tile = tile;
-            m.seq = sq;
-            m.n_live = n_live;
-            m.last = last;
-            m.dead_total = dead_total;
-            m.n_total = n_total;
-            sm.meta[st] = m;
-            mbar_arrive(&sm.full[st]);
-            if (TC && tile >= 0) {
-                const int b = k % NB;
-                mbar_wait(&sm.tmem_empty[b], ((k / NB) & 1) ^ 1);
-                tc_fence_after();
-                const uint64_t bdesc = umma_desc(sm.V[st]);
-#pragma unroll
-                for (int h = 0; h < 2; h++)
-                    mma_f16(tmem + b * (2 * K7_BATCH) + h * K7_BATCH, umma_desc(sm.U[h]), bdesc, IDESC);
-                mma_commit(&sm.mma_done[b]);
-            }
-        }
-        __syncwarp();
-        k++;
-        open = false;
-    };
-    auto write_slot = [&](int slot, const float v[6], const Rec &r, uint32_t dead_before) {
-        const int st = k % S;
-        if (TC) {
-            write_vrow<MODE>(sm.V[st], slot, v);
-        } else {
-            sm.vf[st][slot][0] = make_float4(v[0], v[1], v[2], v[3]);
-            sm.vf[st][slot][1] = make_float4(v[4], v[5], 0.f, 0.f);
-        }
-        sm.col[st][slot] = make_float4(r.r, r.g, r.b, 0.f);
-        sm.dead_before[st][slot] = dead_before;
-    };
+    const int real_tiles = (int)blockIdx.x < a.n_tiles ? (a.n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
-    for (;;) {
-        int tile = 0;
-        if (lane == 0) tile = (int)atomicAdd(&a.ctr->tile_queue, 1u);
-        tile = __shfl_sync(FULL, tile, 0);
-        if (tile >= a.n_tiles) {
-            emit(-1, seq, 0, 1, 0u, 0u);
-            break;
+    Cursor cur;
+    cur.tile = blockIdx.x;
+    cur.seq = 0;
+    cursor_tile(cur, a);
+    for (int i = 0; i < p; i++) cursor_next(cur, a);
+    Cursor nxt = cur;
+    for (int i = 0; i < NP; i++) cursor_next(nxt, a);
+    auto list_id = [&](const Cursor &k) -> uint32_t {
+        const int i = k.c * 32 + lane;
+        return i < k.n ? ids[k.beg + i] : 0u;
+    };
+    // gather pipeline: the records of the chunk being evaluated, and the ids of the next owned chunk
+    Rec rc;
+    {
+        const uint32_t id0 = list_id(cur);
+        if (cur.c * 32 + lane < cur.n) rc = a.rec[id0];
+    }
+    uint32_t id_nxt = list_id(nxt);
+
+    for (int m = 0;; m++) {
+        const bool end = cur.tile >= a.n_tiles;
+        if (end && !(cur.seq == real_tiles && cur.c == 0)) return;  // past the stream: the terminator is elsewhere
+        // prefetch the next owned chunk's records; its successor's ids
+        Cursor nx2 = nxt;
+        for (int i = 0; i < NP; i++) cursor_next(nx2, a);
+        Rec rn;
+        if (nxt.c * 32 + lane < nxt.n) rn = a.rec[id_nxt];
+        const uint32_t id_nx2 = list_id(nx2);
+
+        // evaluate this chunk (registers only)
+        const bool valid = cur.c * 32 + lane < cur.n;
+        float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        bool live = false;
+        if (valid) {
+            const int tx = cur.tile % a.tiles_x, ty = a.band_y0 + cur.tile / a.tiles_x;
+            live = gaussian_coeffs(rc, tx * TILE + 8.0, ty * TILE + 8.0, v);  // tile_center (tensor_path.py:21-22)
         }
-        const int sq = seq++;
-        if (lane == 0) *((volatile int *)&sm.retire[sq & 7]) = 0;
-        __syncwarp();
-        const uint2 rg = a.ranges[tile];
-        const int n = (int)(rg.y - rg.x);
-        const int tx = tile % a.tiles_x, ty = a.band_y0 + tile / a.tiles_x;
-        const double ox = tx * TILE + 8.0, oy = ty * TILE + 8.0;  // tile_center (tensor_path.py:21-22)
-        int fill = 0;
-        uint32_t dead = 0;
-        bool retired = false;
-        // software pipeline: list ids two chunks ahead, records one chunk ahead of the chunk being processed
-        const uint32_t *lst = ids + rg.x;
-        uint32_t id_next = (32 + lane < n) ? lst[32 + lane] : 0u;
-        Rec nr;
-        if (lane < n) nr = a.rec[lst[lane]];
-        for (int base = 0; base < n; base += 32) {
-            if (*((volatile int *)&sm.retire[sq & 7]) >= K7_CONSUMER_WARPS) {
-                retired = true;
-                break;
+        uint4 vlo = make_uint4(0, 0, 0, 0), vhi = make_uint4(0, 0, 0, 0);
+        if (TC && live) make_vrow<MODE>(v, vlo, vhi);
+        const float4 col = make_float4(rc.r, rc.g, rc.b, 0.f);
+
+        // wait for the compaction token
+        if (!(p == 0 && m == 0)) mbar_wait(&sm.tok[p], p == 0 ? ((m - 1) & 1) : (m & 1));
+        int k = sm.c_k;
+        bool open = sm.c_open != 0;
+        auto acquire = [&]() {
+            if (!open) {
+                mbar_wait(&sm.empty[k % S], ((k / S) & 1) ^ 1);
+                open = true;
             }
-            const Rec r = nr;
-            const bool valid = base + lane < n;
-            if (base + 32 + lane < n) nr = a.rec[id_next];
-            id_next = (base + 64 + lane < n) ? lst[base + 64 + lane] : 0u;
-            float v[6];
-            const bool live = valid && gaussian_coeffs(r, ox, oy, v);
+        };
+        auto emit = [&](int tile, int sq, int n_live, int last, uint32_t dead_total, uint32_t n_total) {
+            acquire();
+            const int st = k % S;
+            if (TC) fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                StageMeta mt;
+                mt.tile = tile;
+                mt.seq = sq;
+                mt.n_live = n_live;
+                mt.last = last;
+                mt.dead_total = dead_total;
+                mt.n_total = n_total;
+                sm.meta[st] = mt;
+                mbar_arrive(&sm.full[st]);
+                if (TC && tile >= 0) {
+                    const int b = k % NB;
+                    mbar_wait(&sm.tmem_empty[b], ((k / NB) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint64_t bdesc = umma_desc(sm.V[st]);
+#pragma unroll
+                    for (int h = 0; h < 2; h++)
+                        mma_f16(tmem + b * (2 * K7_BATCH) + h * K7_BATCH, umma_desc(sm.U[h]), bdesc, IDESC);
+                    mma_commit(&sm.mma_done[b]);
+                }
+            }
+            __syncwarp();
+            k++;
+            open = false;
+        };
+        if (end) {
+            emit(-1, cur.seq, 0, 1, 0u, 0u);
+            return;
+        }
+        const int sq = cur.seq;
+        if (cur.c == 0) {  // first chunk of a tile: reset its retirement counter and running counts
+            if (lane == 0) *((volatile int *)&sm.retire[sq & 7]) = 0;
+            sm.c_fill = 0;
+            sm.c_dead = 0;
+        }
+        __syncwarp();
+        const bool retired = cur.c > 0 && *((volatile int *)&sm.retire[sq & 7]) >= K7_CONSUMER_WARPS;
+        if (!retired) {
+            int fill = sm.c_fill;
+            uint32_t dead = sm.c_dead;
             const unsigned lm = __ballot_sync(FULL, live), dm = __ballot_sync(FULL, valid && !live);
             const int slot = fill + __popc(lm & lt);
             const uint32_t my_dead = dead + __popc(dm & lt);
             const int nl = __popc(lm);
-            acquire();
-            if (live && slot < K7_BATCH) write_slot(slot, v, r, my_dead);
+            auto put = [&](int row) {
+                const int st = k % S;
+                if (TC) {
+                    *reinterpret_cast<uint4 *>(sm.V[st] + kmaj_off(row, 0)) = vlo;
+                    *reinterpret_cast<uint4 *>(sm.V[st] + kmaj_off(row, 8)) = vhi;
+                } else {
+                    sm.vf[st][row][0] = make_float4(v[0], v[1], v[2], v[3]);
+                    sm.vf[st][row][1] = make_float4(v[4], v[5], 0.f, 0.f);
+                }
+                sm.col[st][row] = col;
+                sm.dead_before[st][row] = my_dead;
+            };
+            if (nl > 0) acquire();
+            if (live && slot < K7_BATCH) put(slot);
             if (fill + nl >= K7_BATCH) {
-                emit(tile, sq, K7_BATCH, 0, 0u, (uint32_t)n);
+                emit(cur.tile, sq, K7_BATCH, 0, 0u, (uint32_t)cur.n);
                 fill = fill + nl - K7_BATCH;
                 if (fill > 0) {
                     acquire();
-                    if (live && slot >= K7_BATCH) write_slot(slot - K7_BATCH, v, r, my_dead);
+                    if (live && slot >= K7_BATCH) put(slot - K7_BATCH);
                 }
             } else {
                 fill += nl;
             }
             dead += __popc(dm);
+            if (cur.c == cur.chunks - 1) {
+                emit(cur.tile, sq, fill, 1, dead, (uint32_t)cur.n);
+                fill = 0;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                sm.c_fill = fill;
+                sm.c_dead = dead;
+            }
         }
-        if (!retired) emit(tile, sq, fill, 1, dead, (uint32_t)n);
+        __syncwarp();
+        if (lane == 0) {
+            sm.c_k = k;
+            sm.c_open = open ? 1 : 0;
+            mbar_arrive(&sm.tok[(p + 1) % NP]);  // release: the compaction state travels with the token
+        }
+        __syncwarp();
+        cur = nxt;
+        nxt = nx2;
+        rc = rn;
+        id_nxt = id_nx2;
     }
 }
 
@@ -379,6 +465,11 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
             mbar_init(&sm.mma_done[b], 1);
             mbar_init(&sm.tmem_empty[b], K7_CONSUMER_WARPS);
         }
+        for (int q = 0; q < K7_PRODUCERS; q++) mbar_init(&sm.tok[q], 1);
+        sm.c_fill = 0;
+        sm.c_k = 0;
+        sm.c_open = 0;
+        sm.c_dead = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (TC && warp == 0) {
@@ -393,8 +484,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
     const uint32_t *ids = a.ids_override ? a.ids_override : (a.ctr->tile_cur ? a.ids1 : a.ids0);
 
     unsigned long long s_blend = 0, s_cull = 0, s_term = 0, s_pairs = 0;
-    if (warp == K7_CONSUMER_WARPS) {
-        producer<MODE>(sm, a, ids, tmem);
+    if (warp >= K7_CONSUMER_WARPS) {
+        producer<MODE>(sm, a, ids, tmem, warp - K7_CONSUMER_WARPS);
     } else {
         int cur_seq = -1, cur_tile = -1;
         int px = 0, py = 0;
@@ -442,49 +533,56 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 tc_fence_after();
             }
             if (!warp_done) {
-                uint32_t r[32];
-                if (TC) {
-                    tmem_ld32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (2 * K7_BATCH) + half * K7_BATCH, r);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int j = 0; j < 32; j++) asm volatile("" : "+r"(r[j]));
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; j++) {
-                        const float4 p0 = sm.vf[st][j][0], p1 = sm.vf[st][j][1];
-                        const float bj = p0.x + p0.y * ux + p0.z * uy + p0.w * ux * ux + p1.x * ux * uy + p1.y * uy * uy;
-                        r[j] = __float_as_uint(bj);
-                    }
-                }
                 const int nl = m.n_live;
                 const uint32_t act = done ? 0u : (nl >= 32 ? FULL : ((1u << nl) - 1u));
-                uint32_t pass = 0;
-#pragma unroll
-                for (int j = 0; j < 32; j++)
-                    if (__uint_as_float(r[j]) >= CUT_LOG2) pass |= 1u << j;
-                pass &= act;
-                const uint32_t wm = __reduce_or_sync(FULL, pass);
+                const uint32_t tb = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (2 * K7_BATCH) + half * K7_BATCH;
+                uint32_t pass_all = 0;
                 int jt = 32;
 #pragma unroll
-                for (int j = 0; j < 32; j++) {
-                    if (wm & (1u << j)) {  // warp-uniform: some pixel of the warp passes EarlyCull here
-                        const bool p = ((pass >> j) & 1u) && !done;
-                        const float al = fminf(ex2_approx(__uint_as_float(r[j])), 1.0f);
-                        const float tn = fmaf(-al, T, T);
-                        const bool stop = p && tn < TERM_T;  // termination precedes compositing
-                        const bool blend = p && !(tn < TERM_T);
-                        const float w = blend ? al * T : 0.0f;
-                        const float4 cc = sm.col[st][j];
-                        c0 = fmaf(w, cc.x, c0);
-                        c1 = fmaf(w, cc.y, c1);
-                        c2 = fmaf(w, cc.z, c2);
-                        T = blend ? tn : T;
-                        cnt += blend ? 1u : 0u;
-                        jt = stop ? j : jt;
-                        done = done || stop;
+                for (int hc = 0; hc < 2; hc++) {  // two 16-column halves keep 16 betas live in registers
+                    uint32_t r[16];
+                    if (TC) {
+                        tmem_ld16(tb + 16 * hc, r);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int j = 0; j < 16; j++) asm volatile("" : "+r"(r[j]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; j++) {
+                            const float4 p0 = sm.vf[st][16 * hc + j][0], p1 = sm.vf[st][16 * hc + j][1];
+                            r[j] = __float_as_uint(p0.x + p0.y * ux + p0.z * uy + p0.w * ux * ux + p1.x * ux * uy +
+                                                   p1.y * uy * uy);
+                        }
+                    }
+                    uint32_t pass = 0;
+#pragma unroll
+                    for (int j = 0; j < 16; j++)
+                        if (__uint_as_float(r[j]) >= CUT_LOG2) pass |= 1u << j;
+                    pass &= (act >> (16 * hc)) & 0xffffu;
+                    pass_all |= pass << (16 * hc);
+                    const uint32_t wm = __reduce_or_sync(FULL, pass);
+#pragma unroll
+                    for (int j = 0; j < 16; j++) {
+                        if (wm & (1u << j)) {  // warp-uniform: some pixel of the warp passes EarlyCull here
+                            const bool p = ((pass >> j) & 1u) && !done;
+                            const float al = fminf(ex2_approx(__uint_as_float(r[j])), 1.0f);
+                            const float tn = fmaf(-al, T, T);
+                            const bool stop = p && tn < TERM_T;  // termination precedes compositing
+                            const bool blend = p && !(tn < TERM_T);
+                            const float w = blend ? al * T : 0.0f;
+                            const float4 cc = sm.col[st][16 * hc + j];
+                            c0 = fmaf(w, cc.x, c0);
+                            c1 = fmaf(w, cc.y, c1);
+                            c2 = fmaf(w, cc.z, c2);
+                            T = blend ? tn : T;
+                            cnt += blend ? 1u : 0u;
+                            jt = stop ? 16 * hc + j : jt;
+                            done = done || stop;
+                        }
                     }
                 }
                 term = term || jt < 32;
+                const uint32_t pass = pass_all;
                 // EarlyCull counts: live columns failing the cut before termination, plus the dead
                 // Gaussians of the list before the terminating one
                 const uint32_t before = jt >= 32 ? FULL : ((1u << jt) - 1u);

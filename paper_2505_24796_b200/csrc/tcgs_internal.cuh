@@ -22,7 +22,8 @@ constexpr int DUP_ITEMS = 1024;       // Gaussians per duplicate-with-keys CTA
 constexpr int DUP_THREADS = 256;
 
 constexpr int K7_CONSUMER_WARPS = 8;  // one pixel per thread, 16x16 tile
-constexpr int K7_THREADS = 32 * (K7_CONSUMER_WARPS + 1);  // + one producer / MMA-issue warp
+constexpr int K7_PRODUCERS = 2;       // producer warps (alternate 32-entry chunks, token-ordered compaction)
+constexpr int K7_THREADS = 32 * (K7_CONSUMER_WARPS + K7_PRODUCERS);
 constexpr int K7_BATCH = 32;          // live Gaussians per tcgen05 batch (MMA N)
 constexpr int K7_STAGES = 4;          // shared-memory B-operand stages
 constexpr int K7_TMEM_BUFS = 2;       // TMEM accumulator buffers

@@ -107,12 +107,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t pari
         "{\n"
         ".reg .pred P1;\n"
         "LAB_WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@P1 bra DONE;\n"
         "bra LAB_WAIT;\n"
         "DONE:\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)  // suspend-time hint: sleep until the phase flips instead of spinning
         : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
@@ -534,7 +534,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
             }
             if (!warp_done) {
                 const int nl = m.n_live;
-                const uint32_t act = done ? 0u : (nl >= 32 ? FULL : ((1u << nl) - 1u));
+                const uint32_t act0 = done ? 0u : (nl >= 32 ? FULL : ((1u << nl) - 1u));
+                uint32_t act = act0;
                 const uint32_t tb = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (2 * K7_BATCH) + half * K7_BATCH;
                 uint32_t pass_all = 0;
                 int jt = 32;
@@ -561,32 +562,37 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                     pass &= (act >> (16 * hc)) & 0xffffu;
                     pass_all |= pass << (16 * hc);
                     const uint32_t wm = __reduce_or_sync(FULL, pass);
+                    uint32_t lm = pass;  // still-active passing columns: cleared past a termination
 #pragma unroll
                     for (int j = 0; j < 16; j++) {
                         if (wm & (1u << j)) {  // warp-uniform: some pixel of the warp passes EarlyCull here
-                            const bool p = ((pass >> j) & 1u) && !done;
                             const float al = fminf(ex2_approx(__uint_as_float(r[j])), 1.0f);
                             const float tn = fmaf(-al, T, T);
-                            const bool stop = p && tn < TERM_T;  // termination precedes compositing
-                            const bool blend = p && !(tn < TERM_T);
-                            const float w = blend ? al * T : 0.0f;
                             const float4 cc = sm.col[st][16 * hc + j];
-                            c0 = fmaf(w, cc.x, c0);
-                            c1 = fmaf(w, cc.y, c1);
-                            c2 = fmaf(w, cc.z, c2);
-                            T = blend ? tn : T;
-                            cnt += blend ? 1u : 0u;
-                            jt = stop ? 16 * hc + j : jt;
-                            done = done || stop;
+                            const bool p = (lm >> j) & 1u;
+                            if (p && tn < TERM_T) {  // termination precedes compositing
+                                jt = 16 * hc + j;
+                                lm &= (1u << j) - 1u;
+                            }
+                            if (p && !(tn < TERM_T)) {
+                                const float w = al * T;
+                                c0 = fmaf(w, cc.x, c0);
+                                c1 = fmaf(w, cc.y, c1);
+                                c2 = fmaf(w, cc.z, c2);
+                                T = tn;
+                                cnt++;
+                            }
                         }
                     }
+                    if (jt < 32) act = 0u;  // terminated in this half: nothing later is live
                 }
                 term = term || jt < 32;
+                done = done || jt < 32;
                 const uint32_t pass = pass_all;
                 // EarlyCull counts: live columns failing the cut before termination, plus the dead
                 // Gaussians of the list before the terminating one
                 const uint32_t before = jt >= 32 ? FULL : ((1u << jt) - 1u);
-                cull += __popc(act & ~pass & before);
+                cull += __popc(act0 & ~pass & before);
                 if (jt < 32) cull += sm.dead_before[st][jt];
                 if (__all_sync(FULL, done)) {
                     warp_done = true;

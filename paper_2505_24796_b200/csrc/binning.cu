@@ -124,14 +124,15 @@ __global__ void __launch_bounds__(256) sort_plan(SortState *ss, int npass, const
 template <typename KT, int IPT>
 __global__ void __launch_bounds__(OS_THREADS) onesweep(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1,
                                                        const unsigned long long *n_dev, int64_t n_host, int64_t cap,
-                                                       int pass, int shift, SortState *ss, uint32_t *lookback) {
+                                                       int pass, int shift, SortState *ss, uint32_t *lookback,
+                                                       int64_t tiles_cap) {
     if (!ss->pass_do[pass]) return;
     constexpr int TILE_ITEMS = OS_THREADS * IPT;
     extern __shared__ __align__(16) unsigned char os_smem[];
     KT *skey = reinterpret_cast<KT *>(os_smem);
     uint32_t *sval = reinterpret_cast<uint32_t *>(os_smem + sizeof(KT) * TILE_ITEMS);
     __shared__ uint32_t wh[OS_WARPS][RADIX];
-    __shared__ uint32_t loc[RADIX], gofs[RADIX], wt[8];
+    __shared__ uint32_t loc[RADIX], gofs[RADIX], tot[RADIX], wex[RADIX], wt[8];
     __shared__ int s_tile;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t n = dev_count(n_dev, n_host, cap);
@@ -182,22 +183,50 @@ __global__ void __launch_bounds__(OS_THREADS) onesweep(KT *k0, KT *k1, uint32_t 
         wh[w][d] = total;
         total += v;
     }
+    // look-back table is digit-major ([digit][tile]) so a warp reads 32 predecessors of a digit in one load
     volatile uint32_t *lb = lookback;
-    lb[(int64_t)tile * RADIX + d] = (tile == 0 ? LB_PRE : LB_AGG) | total;
-    const uint32_t lo = block_excl_scan256(total, wt, nullptr);
+    const int64_t T = tiles_cap;
+    lb[(int64_t)d * T + tile] = (tile == 0 ? LB_PRE : LB_AGG) | total;
+    tot[d] = total;
+    const uint32_t lo = block_excl_scan256(total, wt, nullptr);  // (contains __syncthreads)
     loc[d] = lo;
-    uint32_t excl = 0;
     if (tile > 0) {
-        for (int t = tile - 1;;) {
-            const uint32_t v = lb[(int64_t)t * RADIX + d];
-            const uint32_t flag = v & ~LB_MASK;
-            if (flag == 0u) continue;  // predecessor has not published yet
-            excl += v & LB_MASK;
-            if (flag == LB_PRE) break;
-            t--;
+        // warp w resolves digits 32w..32w+31: first windows of all 32 digits are loaded together
+        uint32_t win[32];
+        const int tp = tile - 1 - lane;
+#pragma unroll
+        for (int dd = 0; dd < 32; dd++) win[dd] = tp >= 0 ? lb[(int64_t)(warp * 32 + dd) * T + tp] : (uint32_t)(2u << 30);
+#pragma unroll
+        for (int dd = 0; dd < 32; dd++) {
+            const int dg = warp * 32 + dd;
+            uint32_t v = win[dd], excl = 0;
+            int t0 = tile - 1;
+            for (;;) {
+                const uint32_t flag = v & ~LB_MASK;
+                const unsigned pre = __ballot_sync(0xffffffffu, flag == LB_PRE);
+                const unsigned lim = pre ? (((pre & (0u - pre)) << 1) - 1u) : 0xffffffffu;
+                if (__ballot_sync(0xffffffffu, flag == 0u) & lim) {  // a needed predecessor is not published yet
+                    v = (t0 - lane >= 0) ? lb[(int64_t)dg * T + (t0 - lane)] : (uint32_t)(2u << 30);
+                    continue;
+                }
+                uint32_t x = ((1u << lane) & lim) ? (v & LB_MASK) : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                excl += x;
+                if (pre) break;
+                t0 -= 32;
+                v = (t0 - lane >= 0) ? lb[(int64_t)dg * T + (t0 - lane)] : (uint32_t)(2u << 30);
+            }
+            if (lane == 0) {
+                lb[(int64_t)dg * T + tile] = LB_PRE | (excl + tot[dg]);
+                wex[dg] = excl;
+            }
         }
-        lb[(int64_t)tile * RADIX + d] = LB_PRE | (excl + total);
+    } else {
+        wex[d] = 0u;
     }
+    __syncthreads();
+    const uint32_t excl = wex[d];
     gofs[d] = ss->ghist[pass][d] + excl - lo;
     __syncthreads();
     // stage in local sorted order, then write coalesced runs
@@ -238,7 +267,8 @@ cudaError_t launch_onesweep(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const un
     const int64_t tiles = div_up(n_dev ? cap : n_host, OS_THREADS * IPT);
     onesweep<KT, IPT><<<(unsigned)(tiles > 0 ? tiles : 1), OS_THREADS, smem, st>>>(k0, k1, v0, v1, n_dev, n_host, cap,
                                                                                     pass, RADIX_BITS * pass, ss,
-                                                                                    lookback + (int64_t)pass * RADIX * tiles);
+                                                                                    lookback + (int64_t)pass * RADIX * tiles,
+                                                                                    tiles);
     return cudaGetLastError();
 }
 

@@ -162,9 +162,9 @@ def launches_per_frame(P, cam, band_rows=None):
     tile_passes = math.ceil(bits / 8)
     k = 2  # init_counters, preprocess_kernel
     if P > 0:
-        k += 2 + 8  # depth_fix_hist, sort_plan, 8 onesweep passes (identity passes exit at entry)
+        k += 2 + 3 * 8  # depth_fix_hist, sort_plan, 8 x (upsweep, rowscan, downsweep); identity passes exit at entry
     k += 3  # count_upsweep, count_scan, duplicate_keys
-    k += 1 + tile_passes + 1  # sort_plan, onesweep passes, tile_ranges
+    k += 1 + 3 * tile_passes + 1  # sort_plan, radix passes, tile_ranges
     k += 1  # render_kernel
     return k
 

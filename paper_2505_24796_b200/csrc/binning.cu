@@ -20,20 +20,18 @@
 //       keys when the band has <= 65536 tiles);
 //   K6  tile ranges [start, end) from the sorted keys.
 //
-// Every radix pass is one "onesweep" kernel: in-order tile tickets, warp
-// match_any multi-split for the stable local rank, decoupled look-back over
-// the per-tile digit counts, and a shared-memory staged scatter so the
-// global stores are coalesced runs.  All counts live on the device: a frame
-// needs no host synchronisation (graph-capturable).
+// Every radix pass is reduce-then-scan: per-tile digit histograms, a
+// per-digit row scan over the tiles, and a downsweep with a warp match_any
+// multi-split for the stable local rank and a shared-memory staged scatter
+// so the global stores are coalesced runs.  Digit histograms of all passes
+// come from the producers (K2 prologue, K4), and passes whose digit is
+// constant exit at entry.  All counts live on the device: a frame needs no
+// host synchronisation (graph-capturable).
 #include "tcgs_internal.cuh"
 
 namespace tcgs {
 
 namespace {
-
-constexpr uint32_t LB_AGG = 1u << 30;  // look-back word: flag (2 bits) | count (30 bits)
-constexpr uint32_t LB_PRE = 2u << 30;
-constexpr uint32_t LB_MASK = (1u << 30) - 1u;
 
 __device__ __forceinline__ int64_t dev_count(const unsigned long long *n_dev, int64_t n_host, int64_t cap) {
     if (!n_dev) return n_host;
@@ -120,38 +118,108 @@ __global__ void __launch_bounds__(256) sort_plan(SortState *ss, int npass, const
     }
 }
 
-// One stable LSD radix pass ("onesweep"): local warp multi-split + decoupled look-back + staged scatter.
+// One stable LSD radix pass = three kernels with no inter-CTA chain:
+//   radix_upsweep   per-tile digit histograms -> table[digit][tile]
+//   radix_rowscan   one CTA per digit: exclusive scan of its row over the tiles
+//   radix_downsweep stable local rank (warp match_any multi-split), global position =
+//                   digit base + row prefix + local rank, scatter staged through shared memory
+//                   so the stores are coalesced runs.
 template <typename KT, int IPT>
-__global__ void __launch_bounds__(OS_THREADS) onesweep(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1,
-                                                       const unsigned long long *n_dev, int64_t n_host, int64_t cap,
-                                                       int pass, int shift, SortState *ss, uint32_t *lookback,
-                                                       int64_t tiles_cap) {
+__global__ void __launch_bounds__(OS_THREADS) radix_upsweep(const KT *k0, const KT *k1, const unsigned long long *n_dev,
+                                                            int64_t n_host, int64_t cap, int pass, int shift,
+                                                            const SortState *ss, uint32_t *table, int64_t T) {
+    if (!ss->pass_do[pass]) return;
+    constexpr int TILE_ITEMS = OS_THREADS * IPT;
+    __shared__ uint32_t wh[OS_WARPS][RADIX];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t n = dev_count(n_dev, n_host, cap);
+    const int64_t tile = blockIdx.x;
+    if (tile * TILE_ITEMS >= n) return;
+    for (int e = lane; e < RADIX; e += 32) wh[warp][e] = 0;
+    __syncwarp();
+    const KT *kin = ss->pass_in[pass] ? k1 : k0;
+    const int64_t seg = tile * TILE_ITEMS + (int64_t)warp * 32 * IPT;
+    KT k[IPT];
+#pragma unroll
+    for (int it = 0; it < IPT; it++) {
+        const int64_t idx = seg + it * 32 + lane;
+        k[it] = idx < n ? kin[idx] : (KT)0;
+    }
+#pragma unroll
+    for (int it = 0; it < IPT; it++) {
+        const int64_t idx = seg + it * 32 + lane;
+        const int d = idx < n ? (int)((k[it] >> shift) & (RADIX - 1)) : RADIX;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);  // warp-aggregated shared atomics
+        if (d < RADIX && lane == (int)(__ffs(peers) - 1)) wh[warp][d] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    const int d = tid;
+    uint32_t t = 0;
+#pragma unroll
+    for (int w = 0; w < OS_WARPS; w++) t += wh[w][d];
+    table[(int64_t)d * T + tile] = t;
+}
+
+template <int IPT>
+__global__ void __launch_bounds__(256) radix_rowscan(const unsigned long long *n_dev, int64_t n_host, int64_t cap,
+                                                     int pass, const SortState *ss, uint32_t *table, int64_t T) {
+    if (!ss->pass_do[pass]) return;
+    constexpr int TILE_ITEMS = OS_THREADS * IPT;
+    __shared__ uint32_t wt[8];
+    const int64_t n = dev_count(n_dev, n_host, cap);
+    const int64_t ntiles = (n + TILE_ITEMS - 1) / TILE_ITEMS;
+    uint32_t *row = table + (int64_t)blockIdx.x * T;
+    uint32_t carry = 0;
+    for (int64_t c0 = 0; c0 < ntiles; c0 += 256 * 8) {
+        uint32_t v[8], s = 0;
+        const int64_t b = c0 + threadIdx.x * 8;
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            v[u] = b + u < ntiles ? row[b + u] : 0u;
+            s += v[u];
+        }
+        uint32_t tot;
+        uint32_t ex = carry + block_excl_scan256(s, wt, &tot);
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            if (b + u < ntiles) row[b + u] = ex;
+            ex += v[u];
+        }
+        carry += tot;
+    }
+}
+
+template <typename KT, int IPT>
+__global__ void __launch_bounds__(OS_THREADS) radix_downsweep(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1,
+                                                              const unsigned long long *n_dev, int64_t n_host,
+                                                              int64_t cap, int pass, int shift, const SortState *ss,
+                                                              const uint32_t *table, int64_t T) {
     if (!ss->pass_do[pass]) return;
     constexpr int TILE_ITEMS = OS_THREADS * IPT;
     extern __shared__ __align__(16) unsigned char os_smem[];
     KT *skey = reinterpret_cast<KT *>(os_smem);
     uint32_t *sval = reinterpret_cast<uint32_t *>(os_smem + sizeof(KT) * TILE_ITEMS);
     __shared__ uint32_t wh[OS_WARPS][RADIX];
-    __shared__ uint32_t loc[RADIX], gofs[RADIX], tot[RADIX], wex[RADIX], wt[8];
-    __shared__ int s_tile;
+    __shared__ uint32_t loc[RADIX], gofs[RADIX], wt[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t n = dev_count(n_dev, n_host, cap);
-    const int64_t ntiles = (n + TILE_ITEMS - 1) / TILE_ITEMS;
-    if (tid == 0) s_tile = (int)atomicAdd(&ss->ticket[pass], 1u);
+    const int64_t tile = blockIdx.x;
+    if (tile * TILE_ITEMS >= n) return;
     for (int e = lane; e < RADIX; e += 32) wh[warp][e] = 0;
-    __syncthreads();
-    const int tile = s_tile;
-    if (tile >= ntiles) return;
     const int in = ss->pass_in[pass];
     const KT *kin = in ? k1 : k0;
     KT *kout = in ? k0 : k1;
     const uint32_t *vin = in ? v1 : v0;
     uint32_t *vout = in ? v0 : v1;
-    const int64_t base = (int64_t)tile * TILE_ITEMS;
+    const int64_t base = tile * TILE_ITEMS;
     const int tile_n = (int)(n - base < TILE_ITEMS ? n - base : TILE_ITEMS);
     const int64_t seg = base + (int64_t)warp * 32 * IPT;
+    // the row prefix and digit base are ready before the keys arrive
+    const uint32_t gbase = ss->ghist[pass][tid] + table[(int64_t)tid * T + tile];
 
     KT k[IPT];
+    uint32_t val[IPT];
     int dig[IPT];
     uint32_t rank[IPT];
 #pragma unroll
@@ -159,8 +227,10 @@ __global__ void __launch_bounds__(OS_THREADS) onesweep(KT *k0, KT *k1, uint32_t 
         const int64_t idx = seg + it * 32 + lane;
         const bool valid = idx < n;
         k[it] = valid ? kin[idx] : (KT)0;
+        val[it] = valid ? vin[idx] : 0u;
         dig[it] = valid ? (int)((k[it] >> shift) & (RADIX - 1)) : RADIX;
     }
+    __syncwarp();
     const unsigned lt = lanemask_lt();
 #pragma unroll
     for (int it = 0; it < IPT; it++) {
@@ -174,7 +244,6 @@ __global__ void __launch_bounds__(OS_THREADS) onesweep(KT *k0, KT *k1, uint32_t 
         rank[it] = b + __popc(peers & lt);
     }
     __syncthreads();
-    // per digit: exclusive prefix over warps, tile total; publish the aggregate right away
     const int d = tid;
     uint32_t total = 0;
 #pragma unroll
@@ -183,60 +252,17 @@ __global__ void __launch_bounds__(OS_THREADS) onesweep(KT *k0, KT *k1, uint32_t 
         wh[w][d] = total;
         total += v;
     }
-    // look-back table is digit-major ([digit][tile]) so a warp reads 32 predecessors of a digit in one load
-    volatile uint32_t *lb = lookback;
-    const int64_t T = tiles_cap;
-    lb[(int64_t)d * T + tile] = (tile == 0 ? LB_PRE : LB_AGG) | total;
-    tot[d] = total;
     const uint32_t lo = block_excl_scan256(total, wt, nullptr);  // (contains __syncthreads)
     loc[d] = lo;
-    if (tile > 0) {
-        // warp w resolves digits 32w..32w+31: first windows of all 32 digits are loaded together
-        uint32_t win[32];
-        const int tp = tile - 1 - lane;
-#pragma unroll
-        for (int dd = 0; dd < 32; dd++) win[dd] = tp >= 0 ? lb[(int64_t)(warp * 32 + dd) * T + tp] : (uint32_t)(2u << 30);
-#pragma unroll
-        for (int dd = 0; dd < 32; dd++) {
-            const int dg = warp * 32 + dd;
-            uint32_t v = win[dd], excl = 0;
-            int t0 = tile - 1;
-            for (;;) {
-                const uint32_t flag = v & ~LB_MASK;
-                const unsigned pre = __ballot_sync(0xffffffffu, flag == LB_PRE);
-                const unsigned lim = pre ? (((pre & (0u - pre)) << 1) - 1u) : 0xffffffffu;
-                if (__ballot_sync(0xffffffffu, flag == 0u) & lim) {  // a needed predecessor is not published yet
-                    v = (t0 - lane >= 0) ? lb[(int64_t)dg * T + (t0 - lane)] : (uint32_t)(2u << 30);
-                    continue;
-                }
-                uint32_t x = ((1u << lane) & lim) ? (v & LB_MASK) : 0u;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-                excl += x;
-                if (pre) break;
-                t0 -= 32;
-                v = (t0 - lane >= 0) ? lb[(int64_t)dg * T + (t0 - lane)] : (uint32_t)(2u << 30);
-            }
-            if (lane == 0) {
-                lb[(int64_t)dg * T + tile] = LB_PRE | (excl + tot[dg]);
-                wex[dg] = excl;
-            }
-        }
-    } else {
-        wex[d] = 0u;
-    }
+    gofs[d] = gbase - lo;
     __syncthreads();
-    const uint32_t excl = wex[d];
-    gofs[d] = ss->ghist[pass][d] + excl - lo;
-    __syncthreads();
-    // stage in local sorted order, then write coalesced runs
 #pragma unroll
     for (int it = 0; it < IPT; it++) {
         const int dd = dig[it];
         if (dd < RADIX) {
             const uint32_t lp = loc[dd] + wh[warp][dd] + rank[it];
             skey[lp] = k[it];
-            sval[lp] = vin[seg + it * 32 + lane];
+            sval[lp] = val[it];
         }
     }
     __syncthreads();
@@ -249,26 +275,29 @@ __global__ void __launch_bounds__(OS_THREADS) onesweep(KT *k0, KT *k1, uint32_t 
 }
 
 template <typename KT, int IPT>
-constexpr int onesweep_smem() {
+constexpr int downsweep_smem() {
     return (int)((sizeof(KT) + sizeof(uint32_t)) * OS_THREADS * IPT);
 }
 
 template <typename KT, int IPT>
-cudaError_t launch_onesweep(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const unsigned long long *n_dev,
-                            int64_t n_host, int64_t cap, int pass, SortState *ss, uint32_t *lookback,
-                            cudaStream_t st) {
+cudaError_t launch_radix_pass(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const unsigned long long *n_dev,
+                              int64_t n_host, int64_t cap, int pass, SortState *ss, uint32_t *table_all,
+                              cudaStream_t st) {
     static bool configured = false;
-    constexpr int smem = onesweep_smem<KT, IPT>();
+    constexpr int smem = downsweep_smem<KT, IPT>();
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(onesweep<KT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(radix_downsweep<KT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
     const int64_t tiles = div_up(n_dev ? cap : n_host, OS_THREADS * IPT);
-    onesweep<KT, IPT><<<(unsigned)(tiles > 0 ? tiles : 1), OS_THREADS, smem, st>>>(k0, k1, v0, v1, n_dev, n_host, cap,
-                                                                                    pass, RADIX_BITS * pass, ss,
-                                                                                    lookback + (int64_t)pass * RADIX * tiles,
-                                                                                    tiles);
+    const unsigned grid = (unsigned)(tiles > 0 ? tiles : 1);
+    uint32_t *table = table_all + (int64_t)pass * RADIX * tiles;
+    const int shift = RADIX_BITS * pass;
+    radix_upsweep<KT, IPT><<<grid, OS_THREADS, 0, st>>>(k0, k1, n_dev, n_host, cap, pass, shift, ss, table, tiles);
+    radix_rowscan<IPT><<<RADIX, 256, 0, st>>>(n_dev, n_host, cap, pass, ss, table, tiles);
+    radix_downsweep<KT, IPT><<<grid, OS_THREADS, smem, st>>>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table,
+                                                             tiles);
     return cudaGetLastError();
 }
 
@@ -467,7 +496,7 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     // K5
     sort_plan<<<1, 256, 0, st>>>(ss_tile, npass, &ctr->n_splats, 0, cap, nullptr, &ctr->tile_cur);
     for (int p = 0; p < npass; p++) {
-        cudaError_t e = launch_onesweep<KT, TILEKEY_IPT>(tk0, tk1, tv0, tv1, &ctr->n_splats, 0, cap, p, ss_tile,
+        cudaError_t e = launch_radix_pass<KT, TILEKEY_IPT>(tk0, tk1, tv0, tv1, &ctr->n_splats, 0, cap, p, ss_tile,
                                                           at<uint32_t>(ws, L.lb_tile), st);
         if (e != cudaSuccess) return e;
     }
@@ -487,7 +516,7 @@ int tile_key_bits(const Band &band) {
 
 int bin_launch_count(int64_t P, const Band &band) {
     const int npass = (tile_key_bits(band) + RADIX_BITS - 1) / RADIX_BITS;
-    return (P > 0 ? 2 + MAX_PASSES : 0) + 3 + 1 + npass + 1;
+    return (P > 0 ? 2 + 3 * MAX_PASSES : 0) + 3 + 1 + 3 * npass + 1;
 }
 
 cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st) {
@@ -506,7 +535,7 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
         depth_fix_hist<<<2 * 148, 256, 0, st>>>(k0, P, ctr, ss_depth);
         sort_plan<<<1, 256, 0, st>>>(ss_depth, MAX_PASSES, nullptr, P, P, &ctr->key_range, &ctr->depth_cur);
         for (int p = 0; p < MAX_PASSES; p++) {
-            e = launch_onesweep<unsigned long long, DEPTH_IPT>(k0, k1, i0, i1, nullptr, P, P, p, ss_depth,
+            e = launch_radix_pass<unsigned long long, DEPTH_IPT>(k0, k1, i0, i1, nullptr, P, P, p, ss_depth,
                                                                at<uint32_t>(ws, L.lb_depth), st);
             if (e != cudaSuccess) return e;
         }

@@ -51,7 +51,6 @@ struct SortState {
     unsigned int ghist[MAX_PASSES][RADIX];  // digit counts, then exclusive global bases
     int pass_do[MAX_PASSES];                // 0: the pass is the identity (one digit value or above the key range)
     int pass_in[MAX_PASSES];                // ping-pong buffer the pass reads
-    unsigned int ticket[MAX_PASSES];        // in-order tile tickets (decoupled look-back)
     int final_buf;
     int pad[3];
 };
@@ -63,7 +62,7 @@ inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
 struct Layout {
     size_t counters, sort_state[2], rec, rect, touched, key64[2], idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
     size_t blocksum, lb_depth, lb_tile, tkey[2], tval[2], ranges, total;
-    size_t zero_begin, zero_bytes;  // sort state + look-back flags, cleared at the start of every binning
+    size_t zero_begin, zero_bytes;  // sort state, cleared at the start of every binning
     static Layout make(int64_t P, int W, int H, int64_t cap) {
         Layout L;
         size_t o = 0;
@@ -74,9 +73,10 @@ struct Layout {
         L.zero_begin = o;
         L.sort_state[0] = take(sizeof(SortState));
         L.sort_state[1] = take(sizeof(SortState));
+        L.zero_bytes = o - L.zero_begin;
+        // per-pass [digit][tile] count tables of the radix passes
         L.lb_depth = take(sizeof(uint32_t) * RADIX * MAX_PASSES * (size_t)div_up((int64_t)Pn, OS_THREADS * DEPTH_IPT));
         L.lb_tile = take(sizeof(uint32_t) * RADIX * TILE_MAX_PASSES * (size_t)div_up((int64_t)cn, OS_THREADS * TILEKEY_IPT));
-        L.zero_bytes = o - L.zero_begin;
         L.rec = take(sizeof(Rec) * Pn);
         L.rect = take(sizeof(short4) * Pn);
         L.touched = take(sizeof(uint32_t) * Pn);

@@ -21,11 +21,12 @@
 //   K6  tile ranges [start, end) from the sorted keys.
 //
 // Every radix pass is reduce-then-scan: per-tile digit histograms, a
-// per-digit row scan over the tiles, and a downsweep with a warp match_any
-// multi-split for the stable local rank and a shared-memory staged scatter
-// so the global stores are coalesced runs.  Digit histograms of all passes
-// come from the producers (K2 prologue, K4), and passes whose digit is
-// constant exit at entry.  All counts live on the device: a frame needs no
+// per-digit row scan over the tiles (which also yields the digit totals),
+// and a downsweep with a ballot-based warp multi-split for the stable local
+// rank and a shared-memory staged scatter so the global stores are coalesced
+// runs.  For the depth key, the digit histograms of all passes come from one
+// read fused with the key rebase, so passes above the key range or with a
+// single digit value exit at entry.  All counts live on the device: a frame needs no
 // host synchronisation (graph-capturable).
 #include "tcgs_internal.cuh"
 
@@ -62,6 +63,20 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t *war
     return pre + x - v;
 }
 
+// Lanes of the warp holding the same 8-bit digit (invalid items: digit >= RADIX match only each other).
+// Nine ballots instead of MATCH.ANY, whose throughput is far lower.
+__device__ __forceinline__ unsigned warp_peers(int d) {
+    unsigned peers = __ballot_sync(0xffffffffu, d < RADIX);
+    if (d >= RADIX) peers = ~peers;
+#pragma unroll
+    for (int b = 0; b < RADIX_BITS; b++) {
+        const bool bit = (d >> b) & 1;
+        const unsigned m = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? m : ~m;
+    }
+    return peers;
+}
+
 // ---------------------------------------------------------------- K2 prologue
 // depth bits -> bits - min over visible; Gaussians touching no tile get 0 (they emit nothing, so their
 // place in the depth order is irrelevant).  Histograms every digit below the key range in the same read.
@@ -87,11 +102,10 @@ __global__ void __launch_bounds__(256) depth_fix_hist(unsigned long long *keys, 
     }
 }
 
-// Turn the digit histograms into exclusive global bases, mark identity passes, assign ping-pong buffers.
+// Mark identity passes (from the digit histograms when count_hist) and assign ping-pong buffers.
 __global__ void __launch_bounds__(256) sort_plan(SortState *ss, int npass, const unsigned long long *n_dev,
                                                  int64_t n_host, int64_t cap, const unsigned long long *range,
-                                                 int *final_out) {
-    __shared__ uint32_t wt[8];
+                                                 int count_hist, int *final_out) {
     __shared__ int trivial;
     const int d = threadIdx.x;
     const int64_t n = dev_count(n_dev, n_host, cap);
@@ -100,10 +114,9 @@ __global__ void __launch_bounds__(256) sort_plan(SortState *ss, int npass, const
         const bool active = range ? (((*range) >> (RADIX_BITS * p)) != 0ull) : true;
         if (d == 0) trivial = (!active || n == 0) ? 1 : 0;
         __syncthreads();
-        const uint32_t c = active ? ss->ghist[p][d] : 0u;
-        if ((int64_t)c == n) trivial = 1;
-        const uint32_t base = block_excl_scan256(c, wt, nullptr);
-        ss->ghist[p][d] = base;
+        const uint32_t c = (active && count_hist) ? ss->ghist[p][d] : 0u;
+        if (count_hist && (int64_t)c == n) trivial = 1;
+        __syncthreads();
         const int triv = trivial;
         if (d == 0) {
             ss->pass_in[p] = cur;
@@ -120,9 +133,10 @@ __global__ void __launch_bounds__(256) sort_plan(SortState *ss, int npass, const
 
 // One stable LSD radix pass = three kernels with no inter-CTA chain:
 //   radix_upsweep   per-tile digit histograms -> table[digit][tile]
-//   radix_rowscan   one CTA per digit: exclusive scan of its row over the tiles
-//   radix_downsweep stable local rank (warp match_any multi-split), global position =
-//                   digit base + row prefix + local rank, scatter staged through shared memory
+//   radix_rowscan   one CTA per digit: exclusive scan of its row over the tiles, digit total
+//   radix_downsweep stable local rank (ballot multi-split), global position =
+//                   digit base (scan of the totals) + row prefix + local rank, scatter staged
+//                   through shared memory
 //                   so the stores are coalesced runs.
 template <typename KT, int IPT>
 __global__ void __launch_bounds__(OS_THREADS) radix_upsweep(const KT *k0, const KT *k1, const unsigned long long *n_dev,
@@ -149,7 +163,7 @@ __global__ void __launch_bounds__(OS_THREADS) radix_upsweep(const KT *k0, const 
     for (int it = 0; it < IPT; it++) {
         const int64_t idx = seg + it * 32 + lane;
         const int d = idx < n ? (int)((k[it] >> shift) & (RADIX - 1)) : RADIX;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);  // warp-aggregated shared atomics
+        const unsigned peers = warp_peers(d);  // warp-aggregated shared atomics
         if (d < RADIX && lane == (int)(__ffs(peers) - 1)) wh[warp][d] += __popc(peers);
         __syncwarp();
     }
@@ -163,7 +177,7 @@ __global__ void __launch_bounds__(OS_THREADS) radix_upsweep(const KT *k0, const 
 
 template <int IPT>
 __global__ void __launch_bounds__(256) radix_rowscan(const unsigned long long *n_dev, int64_t n_host, int64_t cap,
-                                                     int pass, const SortState *ss, uint32_t *table, int64_t T) {
+                                                     int pass, SortState *ss, uint32_t *table, int64_t T) {
     if (!ss->pass_do[pass]) return;
     constexpr int TILE_ITEMS = OS_THREADS * IPT;
     __shared__ uint32_t wt[8];
@@ -188,6 +202,7 @@ __global__ void __launch_bounds__(256) radix_rowscan(const unsigned long long *n
         }
         carry += tot;
     }
+    if (threadIdx.x == 0) ss->ghist[pass][blockIdx.x] = carry;  // digit total
 }
 
 template <typename KT, int IPT>
@@ -215,8 +230,8 @@ __global__ void __launch_bounds__(OS_THREADS) radix_downsweep(KT *k0, KT *k1, ui
     const int64_t base = tile * TILE_ITEMS;
     const int tile_n = (int)(n - base < TILE_ITEMS ? n - base : TILE_ITEMS);
     const int64_t seg = base + (int64_t)warp * 32 * IPT;
-    // the row prefix and digit base are ready before the keys arrive
-    const uint32_t gbase = ss->ghist[pass][tid] + table[(int64_t)tid * T + tile];
+    const uint32_t dtot = ss->ghist[pass][tid];
+    const uint32_t rowpre = table[(int64_t)tid * T + tile];
 
     KT k[IPT];
     uint32_t val[IPT];
@@ -235,7 +250,7 @@ __global__ void __launch_bounds__(OS_THREADS) radix_downsweep(KT *k0, KT *k1, ui
 #pragma unroll
     for (int it = 0; it < IPT; it++) {
         const int d = dig[it];
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned peers = warp_peers(d);
         uint32_t b = 0;
         if (d < RADIX) b = wh[warp][d];
         __syncwarp();
@@ -253,8 +268,9 @@ __global__ void __launch_bounds__(OS_THREADS) radix_downsweep(KT *k0, KT *k1, ui
         total += v;
     }
     const uint32_t lo = block_excl_scan256(total, wt, nullptr);  // (contains __syncthreads)
+    const uint32_t dbase = block_excl_scan256(dtot, wt, nullptr);
     loc[d] = lo;
-    gofs[d] = gbase - lo;
+    gofs[d] = dbase + rowpre - lo;
     __syncthreads();
 #pragma unroll
     for (int it = 0; it < IPT; it++) {
@@ -361,23 +377,19 @@ __global__ void __launch_bounds__(1024) count_scan(unsigned long long *blocksum,
 
 // K4: duplicate-with-keys.  Each CTA walks DUP_ITEMS depth-ordered Gaussians 256 at a time, scans their
 // tile counts, then expands (Gaussian, covered tile) pairs cooperatively: consecutive threads write
-// consecutive splats (binary search of the slot in the shared inclusive scan).  The tile-key digits are
-// histogrammed for K5 in the same pass.
+// consecutive splats (binary search of the slot in the shared inclusive scan).
 template <typename KT>
 __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *idx0, const uint32_t *idx1,
                                                               const DevCounters *ctr, const uint32_t *touched,
                                                               const short4 *rect, int64_t P,
                                                               const unsigned long long *blockoff, int tiles_x,
-                                                              int band_y0, int64_t cap, KT *tkey, uint32_t *tval,
-                                                              SortState *ss, int npass) {
+                                                              int band_y0, int64_t cap, KT *tkey, uint32_t *tval) {
     __shared__ uint32_t incl[DUP_THREADS];
     __shared__ uint32_t gid[DUP_THREADS];
     __shared__ short4 rc[DUP_THREADS];
     __shared__ uint32_t wt[8];
-    __shared__ uint32_t h[TILE_MAX_PASSES][RADIX];
     const uint32_t *order = ctr->depth_cur ? idx1 : idx0;
     const int tid = threadIdx.x;
-    for (int e = tid; e < TILE_MAX_PASSES * RADIX; e += DUP_THREADS) (&h[0][0])[e] = 0;
     const int64_t beg = (int64_t)blockIdx.x * DUP_ITEMS;
     unsigned long long base = blockoff[blockIdx.x];
     for (int r = 0; r < DUP_ITEMS / DUP_THREADS; r++) {
@@ -412,39 +424,47 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
             if (pos < (unsigned long long)cap) {
                 tkey[pos] = (KT)key;
                 tval[pos] = gid[lo];
-                for (int p = 0; p < npass; p++) atomicAdd(&h[p][(key >> (RADIX_BITS * p)) & (RADIX - 1)], 1u);
             }
         }
         base += total;
         __syncthreads();
     }
-    for (int e = tid; e < npass * RADIX; e += DUP_THREADS) {
-        const uint32_t c = (&h[0][0])[e];
-        if (c) atomicAdd(&(&ss->ghist[0][0])[e], c);
-    }
 }
 
-// K6: tile ranges from the sorted keys (4 consecutive keys per thread).
+// K6: tile ranges from the sorted keys: each thread compares 8 consecutive keys (one 16-byte load for
+// 16-bit keys) with their successors.
 template <typename KT>
-__global__ void tile_ranges(const KT *k0, const KT *k1, const DevCounters *ctr, int64_t cap, uint2 *ranges) {
+__global__ void __launch_bounds__(256) tile_ranges(const KT *k0, const KT *k1, const DevCounters *ctr, int64_t cap,
+                                                   uint2 *ranges) {
     const KT *keys = ctr->tile_cur ? k1 : k0;
     const unsigned long long nn = ctr->n_splats;
     const int64_t n = (int64_t)(nn < (unsigned long long)cap ? nn : (unsigned long long)cap);
-    for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i0 < n;
-         i0 += (int64_t)gridDim.x * blockDim.x * 4) {
-        uint32_t prev = i0 > 0 ? (uint32_t)keys[i0 - 1] : 0xffffffffu;
+    constexpr int V = 8;
+    for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V; i0 < n;
+         i0 += (int64_t)gridDim.x * blockDim.x * V) {
+        uint32_t k[V + 1];
+        if (sizeof(KT) == 2 && i0 + V <= n) {
+            const uint4 q = *reinterpret_cast<const uint4 *>(keys + i0);
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int64_t i = i0 + u;
-            if (i >= n) break;
-            const uint32_t t = keys[i];
-            if (t != prev) {
-                ranges[t].x = (uint32_t)i;
-                if (prev != 0xffffffffu) ranges[prev].y = (uint32_t)i;
+            for (int u = 0; u < 4; u++) {
+                k[2 * u] = w[u] & 0xffffu;
+                k[2 * u + 1] = w[u] >> 16;
             }
-            prev = t;
+        } else {
+#pragma unroll
+            for (int u = 0; u < V; u++) k[u] = i0 + u < n ? (uint32_t)keys[i0 + u] : 0xffffffffu;
         }
-        if (i0 + 4 >= n && prev != 0xffffffffu) ranges[prev].y = (uint32_t)n;
+        k[V] = i0 + V < n ? (uint32_t)keys[i0 + V] : 0xffffffffu;
+        if (i0 == 0) ranges[k[0]].x = 0u;
+#pragma unroll
+        for (int u = 0; u < V; u++) {
+            const int64_t i = i0 + u;
+            if (i < n && k[u] != k[u + 1]) {  // last entry of tile k[u]
+                ranges[k[u]].y = (uint32_t)(i + 1);
+                if (i + 1 < n) ranges[k[u + 1]].x = (uint32_t)(i + 1);
+            }
+        }
     }
 }
 
@@ -492,16 +512,16 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     // K4
     duplicate_keys<KT><<<nblk, DUP_THREADS, 0, st>>>(at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr,
                                                       at<uint32_t>(ws, L.touched), at<short4>(ws, L.rect), P,
-                                                      blocksum, band.tiles_x, band.y0, cap, tk0, tv0, ss_tile, npass);
+                                                      blocksum, band.tiles_x, band.y0, cap, tk0, tv0);
     // K5
-    sort_plan<<<1, 256, 0, st>>>(ss_tile, npass, &ctr->n_splats, 0, cap, nullptr, &ctr->tile_cur);
+    sort_plan<<<1, 256, 0, st>>>(ss_tile, npass, &ctr->n_splats, 0, cap, nullptr, 0, &ctr->tile_cur);
     for (int p = 0; p < npass; p++) {
         cudaError_t e = launch_radix_pass<KT, TILEKEY_IPT>(tk0, tk1, tv0, tv1, &ctr->n_splats, 0, cap, p, ss_tile,
                                                           at<uint32_t>(ws, L.lb_tile), st);
         if (e != cudaSuccess) return e;
     }
     // K6
-    tile_ranges<KT><<<4 * 148, 256, 0, st>>>(tk0, tk1, ctr, cap, at<uint2>(ws, L.ranges));
+    tile_ranges<KT><<<(unsigned)div_up(div_up(cap, 8), 256), 256, 0, st>>>(tk0, tk1, ctr, cap, at<uint2>(ws, L.ranges));
     return cudaGetLastError();
 }
 
@@ -533,7 +553,7 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
     if (P > 0) {
         // K2
         depth_fix_hist<<<2 * 148, 256, 0, st>>>(k0, P, ctr, ss_depth);
-        sort_plan<<<1, 256, 0, st>>>(ss_depth, MAX_PASSES, nullptr, P, P, &ctr->key_range, &ctr->depth_cur);
+        sort_plan<<<1, 256, 0, st>>>(ss_depth, MAX_PASSES, nullptr, P, P, &ctr->key_range, 1, &ctr->depth_cur);
         for (int p = 0; p < MAX_PASSES; p++) {
             e = launch_radix_pass<unsigned long long, DEPTH_IPT>(k0, k1, i0, i1, nullptr, P, P, p, ss_depth,
                                                                at<uint32_t>(ws, L.lb_depth), st);

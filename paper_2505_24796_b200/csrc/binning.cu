@@ -162,10 +162,7 @@ __global__ void __launch_bounds__(OS_THREADS) radix_upsweep(const KT *k0, const 
 #pragma unroll
     for (int it = 0; it < IPT; it++) {
         const int64_t idx = seg + it * 32 + lane;
-        const int d = idx < n ? (int)((k[it] >> shift) & (RADIX - 1)) : RADIX;
-        const unsigned peers = warp_peers(d);  // warp-aggregated shared atomics
-        if (d < RADIX && lane == (int)(__ffs(peers) - 1)) wh[warp][d] += __popc(peers);
-        __syncwarp();
+        if (idx < n) atomicAdd(&wh[warp][(unsigned)(k[it] >> shift) & (RADIX - 1)], 1u);
     }
     __syncthreads();
     const int d = tid;
@@ -206,7 +203,7 @@ __global__ void __launch_bounds__(256) radix_rowscan(const unsigned long long *n
 }
 
 template <typename KT, int IPT>
-__global__ void __launch_bounds__(OS_THREADS) radix_downsweep(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1,
+__global__ void __launch_bounds__(OS_THREADS, 3) radix_downsweep(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1,
                                                               const unsigned long long *n_dev, int64_t n_host,
                                                               int64_t cap, int pass, int shift, const SortState *ss,
                                                               const uint32_t *table, int64_t T) {
@@ -235,28 +232,27 @@ __global__ void __launch_bounds__(OS_THREADS) radix_downsweep(KT *k0, KT *k1, ui
 
     KT k[IPT];
     uint32_t val[IPT];
-    int dig[IPT];
-    uint32_t rank[IPT];
+    uint32_t dr[IPT];  // digit (bits 16..24, RADIX = invalid) | rank within the warp's digit (bits 0..15)
 #pragma unroll
     for (int it = 0; it < IPT; it++) {
         const int64_t idx = seg + it * 32 + lane;
         const bool valid = idx < n;
         k[it] = valid ? kin[idx] : (KT)0;
         val[it] = valid ? vin[idx] : 0u;
-        dig[it] = valid ? (int)((k[it] >> shift) & (RADIX - 1)) : RADIX;
     }
     __syncwarp();
     const unsigned lt = lanemask_lt();
 #pragma unroll
     for (int it = 0; it < IPT; it++) {
-        const int d = dig[it];
+        const bool valid = seg + it * 32 + lane < n;
+        const int d = valid ? (int)((k[it] >> shift) & (RADIX - 1)) : RADIX;
         const unsigned peers = warp_peers(d);
         uint32_t b = 0;
         if (d < RADIX) b = wh[warp][d];
         __syncwarp();
         if (d < RADIX && lane == (int)(__ffs(peers) - 1)) wh[warp][d] = b + __popc(peers);
         __syncwarp();
-        rank[it] = b + __popc(peers & lt);
+        dr[it] = ((uint32_t)d << 16) | (b + __popc(peers & lt));
     }
     __syncthreads();
     const int d = tid;
@@ -274,9 +270,9 @@ __global__ void __launch_bounds__(OS_THREADS) radix_downsweep(KT *k0, KT *k1, ui
     __syncthreads();
 #pragma unroll
     for (int it = 0; it < IPT; it++) {
-        const int dd = dig[it];
+        const uint32_t dd = dr[it] >> 16;
         if (dd < RADIX) {
-            const uint32_t lp = loc[dd] + wh[warp][dd] + rank[it];
+            const uint32_t lp = loc[dd] + wh[warp][dd] + (dr[it] & 0xffffu);
             skey[lp] = k[it];
             sval[lp] = val[it];
         }
@@ -303,6 +299,9 @@ cudaError_t launch_radix_pass(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const 
     constexpr int smem = downsweep_smem<KT, IPT>();
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(radix_downsweep<KT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(radix_downsweep<KT, IPT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
         configured = true;
     }

@@ -7,7 +7,9 @@ K7 tensor-core alpha + blend) for the config-2 workload: 1M synthetic
 Gaussians with SH degree 3 at 1920x1080, inputs resident in HBM (the 236 MB
 scene exceeds the 126 MB L2, so no flush is needed between frames).  N > 1
 shards camera views across ranks (one process per GPU, no collective on the
-data path; weak scaling: every rank renders K frames).
+data path; weak scaling: every rank renders K frames).  ``--config c3``
+renders 4K frames split into tile-row bands across the ranks with one NCCL
+gather to rank 0 per frame (strong scaling).
 
 The JSON line carries the device-timed throughput (`value`), the end-to-end
 throughput through the public API with host buffers (`e2e`), the roofline of
@@ -145,28 +147,18 @@ def measured_peaks():
 
 
 def profile_traffic():
-    """K7 DRAM bytes per launch from the committed ncu --set full capture summary, if present."""
-    p = os.path.join(ROOT, "profiles", "k7_ncu_summary.json")
-    if os.path.exists(p):
+    """K7 DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the newest committed
+    ncu --set full summary under profiles/ (scripts/ncu_summary.py), if present."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_k7_ncu.json")), key=os.path.getmtime)
+    for p in reversed(files):
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            rows = [e for e in json.load(f) if "render_kernel" in e.get("kernel", "")]
+        if rows:
+            mb = [e["dram_read_MB"] + e["dram_write_MB"] for e in rows]
+            return {"bytes_per_launch": 1e6 * sum(mb) / len(mb), "source": os.path.relpath(p, ROOT)}
     return None
-
-
-def launches_per_frame(P, cam, band_rows=None):
-    """Kernels libtcgs.so launches per frame (fixed schedule, csrc/abi.cu + csrc/binning.cu)."""
-    tiles_x = (cam.width + 15) // 16
-    tiles_y = (cam.height + 15) // 16 if band_rows is None else band_rows
-    nt = tiles_x * tiles_y
-    bits = max(1, math.ceil(math.log2(max(nt, 2))))
-    tile_passes = math.ceil(bits / 8)
-    k = 2  # init_counters, preprocess_kernel
-    if P > 0:
-        k += 2 + 3 * 8  # depth_fix_hist, sort_plan, 8 x (upsweep, rowscan, downsweep); identity passes exit at entry
-    k += 3  # count_upsweep, count_scan, duplicate_keys
-    k += 1 + 3 * tile_passes + 1  # sort_plan, radix passes, tile_ranges
-    k += 1  # render_kernel
-    return k
 
 
 # ------------------------------------------------------------------------------------------ CPU side
@@ -244,27 +236,43 @@ def run_tcgs(args):
     import torch.distributed as dist
 
     import paper_2505_24796_b200 as tcgs
-    from paper_2505_24796_b200 import synthetic
+    from paper_2505_24796_b200 import _abi, shard, synthetic
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    bands_mode = args.config == "c3"
 
     scene, cams = synthetic.config_scene(args.config, args.scale)
     base = cams[0]
-    n_views = world * (args.steps + args.warmup)
-    views = view_cameras(base, n_views)
-    my_views = views[rank::world]
+    per_rank = args.steps + args.warmup
+    if bands_mode:
+        my_views = view_cameras(base, per_rank)  # every rank renders its band of the same frames
+    else:
+        pool = cams if len(cams) > 1 else view_cameras(base, world * per_rank)
+        b0, b1 = shard.view_blocks(len(pool), world)[rank]
+        mine = pool[b0:b1] or pool[:1]
+        my_views = [mine[k % len(mine)] for k in range(per_rank)]
 
     cloud = tcgs.GaussianCloud.from_arrays(scene, dev)
-    r = tcgs.Renderer(dev, args.backend)
-    first = r.render_frame(cloud, base)  # sizes the workspace; stats of the base view
-    st0 = first.stats
+    if bands_mode:
+        if world == 1 and not dist.is_initialized():
+            dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % (29500 + os.getpid() % 1000),
+                                    rank=0, world_size=1)
+        br = shard.BandRenderer(dev, args.backend)
+        r = br.r
+        first = br.render(cloud, base, with_stats=True)  # sizes the workspace
+        st0 = first.stats
+    else:
+        r = tcgs.Renderer(dev, args.backend)
+        st0 = r.render_frame(cloud, base).stats  # sizes the workspace; stats of the base view
     stream = torch.cuda.current_stream(dev)
 
     def frame(cam, ev=None):
+        if bands_mode:
+            return br.render(cloud, cam, with_stats=False, timers=ev)
         return r.launch(cloud, cam, timers=ev)
 
     for k in range(args.warmup):
@@ -272,43 +280,50 @@ def run_tcgs(args):
     torch.cuda.synchronize(dev)
 
     # ---- timed region: K frames, inputs resident in HBM
-    k7_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    nev = 5 if bands_mode else 4
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    launches0 = r.lib.tcgs_launch_count()
     with ClockSampler(local) as clk:
         start.record(stream)
         for k in range(args.steps):
-            frame(my_views[args.warmup + k], k7_ev[k])
+            frame(my_views[args.warmup + k], evs[k])
         stop.record(stream)
         torch.cuda.synchronize(dev)
+    launches = r.lib.tcgs_launch_count() - launches0
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(stop)
-    blend_ms = [e[2].elapsed_time(e[3]) for e in k7_ev]
-    pre_ms = [e[0].elapsed_time(e[1]) for e in k7_ev]
-    bin_ms = [e[1].elapsed_time(e[2]) for e in k7_ev]
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    pre_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    bin_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    blend_ms = [e[2].elapsed_time(e[3]) for e in evs]
+    gather_ms = [e[3].elapsed_time(e[4]) for e in evs] if bands_mode else None
+    t = torch.tensor([ms, sum(blend_ms) / len(blend_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max, blend_max = float(t[0].item()), float(t[1].item())
 
-    # per-frame stats of the last timed view (device counters)
-    rc, st_last = r.read_stats(cloud.P)
+    # per-frame stats of this rank's last timed view (device counters; the band's in bands mode)
+    if bands_mode:
+        st_last = br.render(cloud, my_views[-1], with_stats=True).local.stats
+    else:
+        rc, st_last = r.read_stats(cloud.P)
 
     # ---- end to end through the public API: host scene -> device, render, image -> host
     e2e = None
     if not args.no_e2e:
-        host = {k: torch.as_tensor(np.ascontiguousarray(scene[k])).pin_memory()
-                for k in ("means", "scales", "rotations", "opacities", "features" if scene["sh_degree"] > 0 else "colors")}
         feats_key = "features" if scene["sh_degree"] > 0 else "colors"
+        host = {k: torch.as_tensor(np.ascontiguousarray(scene[k])).pin_memory()
+                for k in ("means", "scales", "rotations", "opacities", feats_key)}
         dev_bufs = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
         out_host = torch.empty((base.height, base.width, 3), dtype=torch.float32).pin_memory()
         stats_bytes = 9 * 8
         h2d = sum(v.numel() * v.element_size() for v in host.values())
-        d2h = out_host.numel() * 4 + stats_bytes
+        d2h = (out_host.numel() * 4 if (rank == 0 or not bands_mode) else 0) + stats_bytes
         e2e_steps = max(3, min(args.steps, 20))
 
         def e2e_frame(cam):
@@ -317,9 +332,15 @@ def run_tcgs(args):
             c = tcgs.GaussianCloud(dev_bufs["means"], dev_bufs["scales"], dev_bufs["rotations"],
                                    dev_bufs["opacities"], dev_bufs[feats_key],
                                    scene["sh_degree"] if scene["sh_degree"] > 0 else -1)
-            rgb, T, cnt = r.launch(c, cam)
-            out_host.copy_(rgb, non_blocking=True)
-            r.read_stats(c.P)  # D2H of the frame's FragmentStats (synchronises the stream)
+            if bands_mode:
+                bf = br.render(c, cam, with_stats=True)  # stats: one all-reduce of 6 counters
+                if rank == 0:
+                    out_host.copy_(bf.rgb, non_blocking=True)
+                torch.cuda.synchronize(dev)
+            else:
+                rgb, T, cnt = r.launch(c, cam)
+                out_host.copy_(rgb, non_blocking=True)
+                r.read_stats(c.P)  # D2H of the frame's FragmentStats (synchronises the stream)
 
         for k in range(2):
             e2e_frame(my_views[k])
@@ -334,18 +355,21 @@ def run_tcgs(args):
         te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * e2e_steps / float(te.item()), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "steps": e2e_steps}
+        frames_e2e = e2e_steps if bands_mode else world * e2e_steps
+        e2e = {"value": frames_e2e / float(te.item()), "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+               "path": "pinned host scene -> H2D -> tcgs render -> D2H RGB + FragmentStats, every step"}
 
     if rank != 0:
-        if world > 1:
+        if dist.is_initialized():
             dist.destroy_process_group()
         return
 
-    frames = world * args.steps
+    frames = args.steps if bands_mode else world * args.steps
     value = frames / (ms_max / 1e3)
     blend_avg = sum(blend_ms) / len(blend_ms)
     peaks, peak_kind = measured_peaks()
+    traffic = profile_traffic()
     # K7 algorithmic work: F_alpha = f_blend + f_cull + pixels_terminated fragments, 16 flops each
     # (length-8 dot = 2*8 flops, src/tilesplat/tensor_path.py:40,53); ex2 = f_blend + terminated.
     F_alpha = st_last.f_blend + st_last.f_cull + st_last.pixels_terminated
@@ -360,9 +384,13 @@ def run_tcgs(args):
         os.environ["OMP_NUM_THREADS"] = str(threads)
         s, det = cpu_reference_frame(scene, base, rows=2)
         cpu = {"value": 1.0 / s, "unit": "frames/s", "cores": threads, "kind": "port",
-               "sample": f"oracle C port of tilesplat.render 'reference' (float64), view 0: full project + "
-                         f"build_tiles, blend on {det['band_rows']}/{det['tile_rows']} tile rows extrapolated",
+               "sample": f"oracle C port of tilesplat.render 'reference' (float64, OpenMP over tiles), view 0: full "
+                         f"project + build_tiles, blend on {det['band_rows']}/{det['tile_rows']} tile rows "
+                         f"extrapolated to the frame",
                "detail": det}
+    stage = {"preprocess": sum(pre_ms) / len(pre_ms), "binning": sum(bin_ms) / len(bin_ms), "blend": blend_avg}
+    if gather_ms:
+        stage["gather"] = sum(gather_ms) / len(gather_ms)
     line = {
         "metric": METRIC,
         "value": value,
@@ -372,35 +400,37 @@ def run_tcgs(args):
         "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if bands_mode else "weak",
         "vs_baseline": None,
         "dtype": "f64 preprocess / fp16-hi-lo tcgen05 alpha, fp32 blend",
-        "data": "synthetic (generator G, seed 2; SURVEY.md Appendix B)",
+        "data": "synthetic (SURVEY.md Appendix B generators; random scene, no dataset)",
         "config": {"workload": f"{args.config}: " + synthetic.CONFIGS[args.config],
                    "P": cloud.P, "sh_degree": scene["sh_degree"], "width": base.width, "height": base.height,
-                   "parallelism": f"views x{world}" if world > 1 else "single view",
+                   "parallelism": (f"tile bands x{world}" if bands_mode else
+                                   (f"views x{world}" if world > 1 else "single view")),
                    "l2": "no flush: per-frame inputs (%.0f MB) exceed the 126 MB L2" % (
                        sum(np.asarray(scene[k]).nbytes for k in ("means", "scales", "rotations", "opacities",
                                                                   "features" if scene["sh_degree"] > 0 else "colors"))
                        / 1e6),
                    "backend": args.backend},
         "alpha_blend_ms": blend_avg,
-        "stage_ms": {"preprocess": sum(pre_ms) / len(pre_ms), "binning": sum(bin_ms) / len(bin_ms),
-                     "blend": blend_avg},
+        "alpha_blend_ms_max_over_ranks": blend_max,
+        "stage_ms": stage,
         "frame_stats": {**st_last.to_dict(), "n_visible": st_last.n_visible},
         "roofline": {"kernel": "K7 render_kernel (alpha + blend)", "bound": "tensor", "achieved": tc_tflops,
                      "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": tc_tflops / peaks["bf16_tflops"],
-                     "traffic": profile_traffic(), "peak_kind": peak_kind,
+                     "traffic": (traffic or {}).get("bytes_per_launch"),
+                     "traffic_source": (traffic or {}).get("source"), "peak_kind": peak_kind,
                      "work": "16 flops x F_alpha (F_alpha = f_blend + f_cull + pixels_terminated)",
                      "mufu": {"achieved_ex2_per_s": ex2_rate, "peak_ex2_per_s": ex2_peak,
                               "frac": ex2_rate / ex2_peak, "peak_kind": "nominal 16/clk/SM"}},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": launches_per_frame(cloud.P, base) * args.steps,
+        "gpu_launches": int(launches),
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

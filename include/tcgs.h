@@ -138,8 +138,18 @@ int tcgs_copy_projection(const void *ws, int64_t P, const tcgs_camera *cam, int6
                          uint8_t *visible, double *mean2d, double *conic, double *depth, int32_t *radius,
                          float *rgb, void *stream);
 
+/* Tile-band partition input (multi-GPU, no reference equivalent: the reference renders one frame on one
+ * CPU thread, src/tilesplat/raster.py:177-193).  After tcgs_preprocess, writes the number of splats of
+ * every tile row of the whole frame into row_counts [tiles_y] i64 (device).  K1 is band-agnostic, so the
+ * same preprocess serves any band passed to tcgs_bin / tcgs_blend afterwards. */
+int tcgs_tile_row_counts(const void *ws, int64_t P, const tcgs_camera *cam, int64_t max_splats, int64_t *row_counts,
+                         void *stream);
+
 /* 0 if the current device is sm_100 (B200); TCGS_ERR_DEVICE otherwise. */
 int tcgs_device_check(void);
+
+/* Number of kernels libtcgs.so has launched so far in this process (all streams, all devices). */
+unsigned long long tcgs_launch_count(void);
 
 const char *tcgs_error_string(int code);
 const char *tcgs_last_error(void);

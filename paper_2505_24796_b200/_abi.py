@@ -66,10 +66,12 @@ SIGNATURES = {
                                         _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "tcgs_copy_lists": (ctypes.c_int, [_P, _I64, ctypes.POINTER(Camera), ctypes.POINTER(Opts), _I64, _P, _P, _P]),
     "tcgs_copy_projection": (ctypes.c_int, [_P, _I64, ctypes.POINTER(Camera), _I64, _P, _P, _P, _P, _P, _P, _P]),
+    "tcgs_tile_row_counts": (ctypes.c_int, [_P, _I64, ctypes.POINTER(Camera), _I64, _P, _P]),
     "tcgs_device_check": (ctypes.c_int, []),
     "tcgs_error_string": (ctypes.c_char_p, [ctypes.c_int]),
     "tcgs_last_error": (ctypes.c_char_p, []),
     "tcgs_version": (ctypes.c_int, []),
+    "tcgs_launch_count": (ctypes.c_ulonglong, []),
 }
 
 _lib = None

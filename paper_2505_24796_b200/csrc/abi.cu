@@ -2,9 +2,14 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "tcgs_internal.cuh"
 
 using namespace tcgs;
+
+static std::atomic<unsigned long long> g_launches{0};
+void tcgs::note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
 
@@ -55,6 +60,8 @@ extern "C" {
 
 int tcgs_version(void) { return 1; }
 
+unsigned long long tcgs_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
 const char *tcgs_last_error(void) { return g_last_error; }
 
 const char *tcgs_error_string(int code) {
@@ -97,6 +104,7 @@ int tcgs_preprocess(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_
         return fail(TCGS_ERR_INVALID_ARG, "null scene array");
     cudaStream_t st = (cudaStream_t)stream;
     const Layout L = Layout::make(scene->P, cam->width, cam->height, max_splats);
+    note_launch();
     init_counters<<<1, 1, 0, st>>>(at<DevCounters>(ws, L.counters));
     cudaError_t e = launch_preprocess(*scene, *cam, make_band(*cam, opts), opts ? opts->debug : 0, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "preprocess");
@@ -169,6 +177,7 @@ int tcgs_blend_lists(int64_t P, const double *mean2d, const double *conic, const
     cudaStream_t st = (cudaStream_t)stream;
     const Layout L = Layout::make(P, cam->width, cam->height, 1);
     const Band band = make_band(*cam, opts);
+    note_launch();
     init_counters<<<1, 1, 0, st>>>(at<DevCounters>(ws, L.counters));
     cudaError_t e = launch_pack_lists(P, mean2d, conic, opacity, colors, offsets, band, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "pack_lists");
@@ -195,6 +204,16 @@ int tcgs_copy_lists(const void *ws, int64_t P, const tcgs_camera *cam, const tcg
         e = cudaMemcpyAsync(ranges_out, at<uint2>(ws, L.ranges), sizeof(uint2) * (size_t)band.n_tiles(),
                             cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e, "copy_lists");
+    return TCGS_OK;
+}
+
+int tcgs_tile_row_counts(const void *ws, int64_t P, const tcgs_camera *cam, int64_t max_splats, int64_t *row_counts,
+                         void *stream) {
+    if (!ws || !cam || !row_counts) return fail(TCGS_ERR_INVALID_ARG, "null argument");
+    if (cam->width <= 0 || cam->height <= 0) return fail(TCGS_ERR_INVALID_ARG, "image dimensions must be positive");
+    const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
+    cudaError_t e = launch_row_counts(P, make_band(*cam, nullptr), ws, L, row_counts, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "tile_row_counts");
     return TCGS_OK;
 }
 
@@ -229,6 +248,7 @@ extern "C" int tcgs_copy_projection(const void *ws, int64_t P, const tcgs_camera
         return fail(TCGS_ERR_INVALID_ARG, "null argument");
     if (P <= 0) return TCGS_OK;
     const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
+    note_launch();
     copy_projection_kernel<<<(unsigned)((P + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         P, at<int32_t>(ws, L.radius), at<Rec>(ws, L.rec), at<double>(ws, L.dbg_conic), at<double>(ws, L.dbg_depth),
         at<double>(ws, L.dbg_mean2d), visible, mean2d, conic, depth, radius, rgb);

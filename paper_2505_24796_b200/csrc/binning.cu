@@ -80,7 +80,8 @@ __device__ __forceinline__ unsigned warp_peers(int d) {
 // ---------------------------------------------------------------- K2 prologue
 // depth bits -> bits - min over visible; Gaussians touching no tile get 0 (they emit nothing, so their
 // place in the depth order is irrelevant).  Histograms every digit below the key range in the same read.
-__global__ void __launch_bounds__(256) depth_fix_hist(unsigned long long *keys, int64_t P, DevCounters *ctr,
+__global__ void __launch_bounds__(256) depth_fix_hist(const unsigned long long *src, unsigned long long *keys,
+                                                      uint32_t *idx, int64_t P, DevCounters *ctr,
                                                       SortState *ss) {
     __shared__ uint32_t h[MAX_PASSES][RADIX];
     for (int e = threadIdx.x; e < MAX_PASSES * RADIX; e += blockDim.x) (&h[0][0])[e] = 0;
@@ -90,9 +91,10 @@ __global__ void __launch_bounds__(256) depth_fix_hist(unsigned long long *keys, 
     if (blockIdx.x == 0 && threadIdx.x == 0) ctr->key_range = range;
     const int np = range ? (64 - __clzll((long long)range) + RADIX_BITS - 1) / RADIX_BITS : 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-        unsigned long long k = keys[i];
+        unsigned long long k = src[i];  // K1's output stays intact: tcgs_bin can run again (other bands)
         k = (k == ~0ull) ? 0ull : k - kmin;
         keys[i] = k;
+        idx[i] = (uint32_t)i;
         for (int p = 0; p < np; p++) atomicAdd(&h[p][(unsigned)(k >> (RADIX_BITS * p)) & (RADIX - 1)], 1u);
     }
     __syncthreads();
@@ -309,16 +311,31 @@ cudaError_t launch_radix_pass(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const 
     const unsigned grid = (unsigned)(tiles > 0 ? tiles : 1);
     uint32_t *table = table_all + (int64_t)pass * RADIX * tiles;
     const int shift = RADIX_BITS * pass;
+    note_launch();
     radix_upsweep<KT, IPT><<<grid, OS_THREADS, 0, st>>>(k0, k1, n_dev, n_host, cap, pass, shift, ss, table, tiles);
+    note_launch();
     radix_rowscan<IPT><<<RADIX, 256, 0, st>>>(n_dev, n_host, cap, pass, ss, table, tiles);
+    note_launch();
     radix_downsweep<KT, IPT><<<grid, OS_THREADS, smem, st>>>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table,
                                                              tiles);
     return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- K3 / K4
+// K1's tile rectangles are clipped to the frame; binning clips them to the tile-row band [y0, y1).
+__device__ __forceinline__ short4 band_rect(short4 q, int y0, int y1) {
+    q.y = q.y > y0 ? q.y : (short)y0;
+    q.w = q.w < y1 - 1 ? q.w : (short)(y1 - 1);
+    return q;
+}
+__device__ __forceinline__ uint32_t band_count(short4 q, int y0, int y1) {
+    q = band_rect(q, y0, y1);
+    return q.y <= q.w ? (uint32_t)((q.z - q.x + 1) * (q.w - q.y + 1)) : 0u;
+}
+
 __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx0, const uint32_t *idx1,
                                                              const DevCounters *ctr, const uint32_t *touched,
+                                                             const short4 *rect, int band_y0, int band_y1,
                                                              int64_t P, unsigned long long *blocksum) {
     const uint32_t *order = ctr->depth_cur ? idx1 : idx0;
     const int64_t beg = (int64_t)blockIdx.x * DUP_ITEMS;
@@ -326,7 +343,10 @@ __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx
 #pragma unroll
     for (int u = 0; u < DUP_ITEMS / DUP_THREADS; u++) {
         const int64_t i = beg + u * DUP_THREADS + threadIdx.x;
-        if (i < P) s += touched[order[i]];
+        if (i < P) {
+            const uint32_t g = order[i];
+            if (touched[g]) s += band_count(rect[g], band_y0, band_y1);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -382,7 +402,8 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                                                               const DevCounters *ctr, const uint32_t *touched,
                                                               const short4 *rect, int64_t P,
                                                               const unsigned long long *blockoff, int tiles_x,
-                                                              int band_y0, int64_t cap, KT *tkey, uint32_t *tval) {
+                                                              int band_y0, int band_y1, int64_t cap, KT *tkey,
+                                                              uint32_t *tval) {
     __shared__ uint32_t incl[DUP_THREADS];
     __shared__ uint32_t gid[DUP_THREADS];
     __shared__ short4 rc[DUP_THREADS];
@@ -397,8 +418,11 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
         short4 q = make_short4(0, 0, -1, -1);
         if (i < P) {
             g = order[i];
-            c = touched[g];
-            if (c) q = rect[g];
+            if (touched[g]) {
+                q = band_rect(rect[g], band_y0, band_y1);
+                c = q.x <= q.z && q.y <= q.w ? (uint32_t)((q.z - q.x + 1) * (q.w - q.y + 1)) : 0u;
+                if (!c) q = make_short4(0, 0, -1, -1);
+            }
         }
         uint32_t total;
         const uint32_t ex = block_excl_scan256(c, wt, &total);
@@ -492,6 +516,28 @@ __global__ void pack_ranges(const int64_t *offsets, int band_tile0, int n_tiles,
     ranges[t] = make_uint2((uint32_t)offsets[band_tile0 + t], (uint32_t)offsets[band_tile0 + t + 1]);
 }
 
+// Splats per tile row of the whole frame (sum over Gaussians of the covered tiles in that row), from K1's
+// frame-clipped rectangles: the replicated input of the tile-band partition (multi-GPU).
+__global__ void __launch_bounds__(256) row_counts_kernel(int64_t P, const uint32_t *touched, const short4 *rect,
+                                                         int tiles_y, unsigned long long *out) {
+    constexpr int SMEM_ROWS = 4096;
+    __shared__ unsigned long long h[SMEM_ROWS];
+    const bool priv = tiles_y <= SMEM_ROWS;
+    if (priv)
+        for (int r = threadIdx.x; r < tiles_y; r += blockDim.x) h[r] = 0ull;
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+        if (!touched[i]) continue;
+        const short4 q = rect[i];
+        const unsigned long long w = (unsigned long long)(q.z - q.x + 1);
+        for (int y = q.y; y <= q.w; y++) atomicAdd(priv ? &h[y] : &out[y], w);
+    }
+    if (!priv) return;
+    __syncthreads();
+    for (int r = threadIdx.x; r < tiles_y; r += blockDim.x)
+        if (h[r]) atomicAdd(&out[r], h[r]);
+}
+
 template <typename KT>
 cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st) {
     DevCounters *ctr = at<DevCounters>(ws, L.counters);
@@ -505,14 +551,19 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     unsigned long long *blocksum = at<unsigned long long>(ws, L.blocksum);
     const int nblk = (int)div_up(P > 0 ? P : 1, DUP_ITEMS);
     // K3
+    note_launch();
     count_upsweep<<<nblk, DUP_THREADS, 0, st>>>(at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr,
-                                                 at<uint32_t>(ws, L.touched), P, blocksum);
+                                                 at<uint32_t>(ws, L.touched), at<short4>(ws, L.rect), band.y0,
+                                                 band.y1, P, blocksum);
+    note_launch();
     count_scan<<<1, 1024, 0, st>>>(blocksum, nblk, ctr, cap);
     // K4
+    note_launch();
     duplicate_keys<KT><<<nblk, DUP_THREADS, 0, st>>>(at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr,
                                                       at<uint32_t>(ws, L.touched), at<short4>(ws, L.rect), P,
-                                                      blocksum, band.tiles_x, band.y0, cap, tk0, tv0);
+                                                      blocksum, band.tiles_x, band.y0, band.y1, cap, tk0, tv0);
     // K5
+    note_launch();
     sort_plan<<<1, 256, 0, st>>>(ss_tile, npass, &ctr->n_splats, 0, cap, nullptr, 0, &ctr->tile_cur);
     for (int p = 0; p < npass; p++) {
         cudaError_t e = launch_radix_pass<KT, TILEKEY_IPT>(tk0, tk1, tv0, tv1, &ctr->n_splats, 0, cap, p, ss_tile,
@@ -520,11 +571,24 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
         if (e != cudaSuccess) return e;
     }
     // K6
+    note_launch();
     tile_ranges<KT><<<(unsigned)div_up(div_up(cap, 8), 256), 256, 0, st>>>(tk0, tk1, ctr, cap, at<uint2>(ws, L.ranges));
     return cudaGetLastError();
 }
 
 }  // namespace
+
+cudaError_t launch_row_counts(int64_t P, const Band &band, const void *ws, const Layout &L, int64_t *out,
+                              cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(int64_t) * (size_t)band.tiles_y, st);
+    if (e != cudaSuccess || P <= 0) return e;
+    const int64_t blocks = div_up(P, 256 * 8);
+    note_launch();
+    row_counts_kernel<<<(unsigned)(blocks < 4 * 148 ? blocks : 4 * 148), 256, 0, st>>>(
+        P, at<uint32_t>(ws, L.touched), at<short4>(ws, L.rect), band.tiles_y,
+        reinterpret_cast<unsigned long long *>(out));
+    return cudaGetLastError();
+}
 
 int tile_key_bits(const Band &band) {
     const int nt = band.n_tiles();
@@ -542,6 +606,8 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
     DevCounters *ctr = at<DevCounters>(ws, L.counters);
     SortState *ss_depth = at<SortState>(ws, L.sort_state[0]);
     cudaError_t e = cudaMemsetAsync(static_cast<char *>(ws) + L.zero_begin, 0, L.zero_bytes, st);
+    // per-binning counters (K1's dropped / n_visible / key_min / key_max stay)
+    if (e == cudaSuccess) e = cudaMemsetAsync(&ctr->n_splats, 0, 2 * sizeof(unsigned long long), st);
     if (e == cudaSuccess)
         e = cudaMemsetAsync(at<uint2>(ws, L.ranges), 0, sizeof(uint2) * (size_t)(band.n_tiles() ? band.n_tiles() : 1), st);
     if (e != cudaSuccess) return e;
@@ -551,7 +617,9 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
     uint32_t *i1 = at<uint32_t>(ws, L.idx[1]);
     if (P > 0) {
         // K2
-        depth_fix_hist<<<2 * 148, 256, 0, st>>>(k0, P, ctr, ss_depth);
+        note_launch();
+        depth_fix_hist<<<2 * 148, 256, 0, st>>>(at<unsigned long long>(ws, L.key_src), k0, i0, P, ctr, ss_depth);
+        note_launch();
         sort_plan<<<1, 256, 0, st>>>(ss_depth, MAX_PASSES, nullptr, P, P, &ctr->key_range, 1, &ctr->depth_cur);
         for (int p = 0; p < MAX_PASSES; p++) {
             e = launch_radix_pass<unsigned long long, DEPTH_IPT>(k0, k1, i0, i1, nullptr, P, P, p, ss_depth,
@@ -567,9 +635,11 @@ cudaError_t launch_pack_lists(int64_t P, const double *mean2d, const double *con
                               const float *colors, const int64_t *offsets, const Band &band, void *ws,
                               const Layout &L, cudaStream_t st) {
     if (P > 0)
+        note_launch();
         pack_records<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(P, mean2d, conic, opacity, colors, at<Rec>(ws, L.rec));
     const int nt = band.n_tiles();
     if (nt > 0)
+        note_launch();
         pack_ranges<<<(nt + 255) / 256, 256, 0, st>>>(offsets, band.y0 * band.tiles_x, nt, at<uint2>(ws, L.ranges));
     return cudaGetLastError();
 }

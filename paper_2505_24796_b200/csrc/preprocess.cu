@@ -258,13 +258,14 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
                     a.dbg_mean2d[2 * i] = mx;
                     a.dbg_mean2d[2 * i + 1] = my;
                 }
-                // covered_tiles (src/tilesplat/tiling.py:34-43), clipped to the grid and the band
+                // covered_tiles (src/tilesplat/tiling.py:34-43), clipped to the grid.  The rectangle is
+                // band-agnostic (binning clips it to a tile-row band), so one K1 serves every band choice.
                 double fx0 = floor((mx - rad) / TILE), fx1 = floor((mx + rad) / TILE);
                 double fy0 = floor((my - rad) / TILE), fy1 = floor((my + rad) / TILE);
                 fx0 = fmax(fx0, 0.0);
-                fy0 = fmax(fy0, (double)a.band_y0);
+                fy0 = fmax(fy0, 0.0);
                 fx1 = fmin(fx1, (double)(a.tiles_x - 1));
-                fy1 = fmin(fy1, (double)(a.band_y1 - 1));
+                fy1 = fmin(fy1, (double)(a.tiles_y - 1));
                 if (fx0 <= fx1 && fy0 <= fy1) {
                     const int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
                     touched = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
@@ -299,7 +300,6 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
         }
         a.touched[i] = touched;
         a.keys[i] = key;
-        a.idx[i] = (uint32_t)i;
     }
     // warp-aggregated counters
     const unsigned full = 0xffffffffu;
@@ -341,8 +341,7 @@ cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, c
     a.rec = at<Rec>(ws, L.rec);
     a.rect = at<short4>(ws, L.rect);
     a.touched = at<uint32_t>(ws, L.touched);
-    a.keys = at<unsigned long long>(ws, L.key64[0]);
-    a.idx = at<uint32_t>(ws, L.idx[0]);
+    a.keys = at<unsigned long long>(ws, L.key_src);
     a.radius = at<int32_t>(ws, L.radius);
     a.dbg_conic = at<double>(ws, L.dbg_conic);
     a.dbg_depth = at<double>(ws, L.dbg_depth);
@@ -351,10 +350,12 @@ cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, c
     if (scene.P <= 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((scene.P + 255) / 256);
     if (scene.dtype == TCGS_F64) {
+        note_launch();
         preprocess_kernel<double><<<blocks, 256, 0, st>>>(
             a, (const double *)scene.means, (const double *)scene.scales, (const double *)scene.rotations,
             (const double *)scene.opacities, (const double *)scene.features);
     } else {
+        note_launch();
         preprocess_kernel<float><<<blocks, 256, 0, st>>>(
             a, (const float *)scene.means, (const float *)scene.scales, (const float *)scene.rotations,
             (const float *)scene.opacities, (const float *)scene.features);

@@ -649,6 +649,7 @@ cudaError_t launch_mode(const RenderArgs &a, int num_sms, cudaStream_t st) {
         configured = true;
     }
     const int grid = num_sms * K7_CTAS_PER_SM;
+    note_launch();
     render_kernel<MODE><<<grid, K7_THREADS, K7_SMEM_BYTES, st>>>(a);
     return cudaGetLastError();
 }

@@ -60,7 +60,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 struct Layout {
-    size_t counters, sort_state[2], rec, rect, touched, key64[2], idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
+    size_t counters, sort_state[2], rec, rect, touched, key_src, key64[2], idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
     size_t blocksum, lb_depth, lb_tile, tkey[2], tval[2], ranges, total;
     size_t zero_begin, zero_bytes;  // sort state, cleared at the start of every binning
     static Layout make(int64_t P, int W, int H, int64_t cap) {
@@ -80,6 +80,7 @@ struct Layout {
         L.rec = take(sizeof(Rec) * Pn);
         L.rect = take(sizeof(short4) * Pn);
         L.touched = take(sizeof(uint32_t) * Pn);
+        L.key_src = take(sizeof(uint64_t) * Pn);
         L.key64[0] = take(sizeof(uint64_t) * Pn);
         L.key64[1] = take(sizeof(uint64_t) * Pn);
         L.idx[0] = take(sizeof(uint32_t) * Pn);
@@ -131,7 +132,11 @@ cudaError_t launch_render(int alpha_mode, const tcgs_camera &cam, const Band &ba
 cudaError_t launch_pack_lists(int64_t P, const double *mean2d, const double *conic, const double *opacity,
                               const float *colors, const int64_t *offsets, const Band &band, void *ws,
                               const Layout &L, cudaStream_t st);
+cudaError_t launch_row_counts(int64_t P, const Band &band, const void *ws, const Layout &L, int64_t *out,
+                              cudaStream_t st);
 int tile_key_bits(const Band &band);
+// Host-side count of kernels this library has launched (tcgs_launch_count): the bench's gpu_launches.
+void note_launch();
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {

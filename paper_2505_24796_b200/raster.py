@@ -279,25 +279,37 @@ class Renderer:
 
     def launch(self, cloud: GaussianCloud, cam, band=None, debug=False, outputs=None, timers=None):
         """Enqueue K1..K7 on the current stream (no host synchronisation)."""
-        c = camera_struct(cam)
-        cap = self.capacity(cloud.P)
-        ws = self.workspace(cloud.P, c.width, c.height, cap)
-        rgb, T, cnt = outputs if outputs is not None else self.outputs(c.width, c.height)
-        o = self._opts(band, debug)
-        st = torch.cuda.current_stream(self.device).cuda_stream
-        s = cloud._c()
-        lib = self.lib
         ev = timers
         if ev:
             ev[0].record()
-        _abi.check(lib.tcgs_preprocess(s, c, o, ws.data_ptr(), ws.numel(), cap, st), "tcgs_preprocess")
+        self.preprocess(cloud, cam, band, debug)
         if ev:
             ev[1].record()
-        _abi.check(lib.tcgs_bin(cloud.P, c, o, ws.data_ptr(), ws.numel(), cap, st), "tcgs_bin")
+        return self.bin_blend(cloud, cam, band, outputs, ev)
+
+    def preprocess(self, cloud: GaussianCloud, cam, band=None, debug=False) -> None:
+        """K1 (band-agnostic: its tile rectangles serve any band binned afterwards)."""
+        c = camera_struct(cam)
+        cap = self.capacity(cloud.P)
+        ws = self.workspace(cloud.P, c.width, c.height, cap)
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        _abi.check(self.lib.tcgs_preprocess(cloud._c(), c, self._opts(band, debug), ws.data_ptr(), ws.numel(), cap,
+                                            st), "tcgs_preprocess")
+
+    def bin_blend(self, cloud: GaussianCloud, cam, band=None, outputs=None, timers=None):
+        """K2-K6 and K7 for ``band`` (tile rows [y0, y1); None = the whole frame) after ``preprocess``."""
+        c = camera_struct(cam)
+        cap = self.capacity(cloud.P)
+        ws = self.ws
+        rgb, T, cnt = outputs if outputs is not None else self.outputs(c.width, c.height)
+        o = self._opts(band)
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        ev = timers
+        _abi.check(self.lib.tcgs_bin(cloud.P, c, o, ws.data_ptr(), ws.numel(), cap, st), "tcgs_bin")
         if ev:
             ev[2].record()
-        _abi.check(lib.tcgs_blend(cloud.P, c, o, ws.data_ptr(), ws.numel(), cap, rgb.data_ptr(), T.data_ptr(),
-                                  cnt.data_ptr(), st), "tcgs_blend")
+        _abi.check(self.lib.tcgs_blend(cloud.P, c, o, ws.data_ptr(), ws.numel(), cap, rgb.data_ptr(), T.data_ptr(),
+                                       cnt.data_ptr(), st), "tcgs_blend")
         if ev:
             ev[3].record()
         return rgb, T, cnt
@@ -310,6 +322,20 @@ class Renderer:
                            n_splats=st_.n_splats, dropped=st_.dropped, pixels_terminated=st_.pixels_terminated,
                            n_visible=st_.n_visible)
         return rc, fs
+
+    def finish(self, cloud: GaussianCloud, cam, band=None, with_stats=True) -> Frame:
+        """K2-K7 for ``band`` after ``preprocess`` + the frame's stats (re-running K1 if the splat
+        capacity had to grow)."""
+        for _attempt in range(3):
+            rgb, T, cnt = self.bin_blend(cloud, cam, band)
+            rc, fs = self.read_stats(cloud.P, band)
+            if rc == _abi.TCGS_ERR_CAPACITY:
+                self.max_splats = int(fs.n_splats * 1.25) + 1024
+                self.preprocess(cloud, cam, band)
+                continue
+            _abi.check(rc, "tcgs_read_stats")
+            return Frame(rgb, T, cnt, fs)
+        raise RuntimeError("splat capacity could not be satisfied")
 
     def render_frame(self, cloud: GaussianCloud, cam, band=None, debug=False, timed=True) -> Frame:
         with torch.cuda.device(self.device):

@@ -253,6 +253,72 @@ def test_tile_band_matches_full_frame(renderers, band):
     assert torch.equal(fb.n_contrib[y0:y1], full_cnt[y0:y1])
 
 
+def test_one_preprocess_serves_every_band(renderers):
+    """K1 is band-agnostic: one preprocess, then K2-K7 per band of a partition, assembles the full frame."""
+    from paper_2505_24796_b200 import shard
+
+    g = load_golden("f32gen")
+    cam = GoldenCam(g)
+    r = renderers["tcgs"]
+    cloud = cloud_of(g)
+    full = r.render_frame(cloud, cam)
+    ref_rgb, ref_T, ref_cnt, ref_st = full.rgb.clone(), full.T.clone(), full.n_contrib.clone(), full.stats
+    r.preprocess(cloud, cam)
+    tiles_y = (cam.height + 15) // 16
+    rows = torch.empty(tiles_y, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    from paper_2505_24796_b200 import _abi
+    from paper_2505_24796_b200.raster import camera_struct
+
+    _abi.check(r.lib.tcgs_tile_row_counts(r.ws.data_ptr(), cloud.P, camera_struct(cam), r.max_splats,
+                                          rows.data_ptr(), st), "row counts")
+    counts = rows.cpu().numpy()
+    offsets, _ = oracle.build_tiles(oracle.project(g["means"], g["scales"], g["rotations"], cam), cam)
+    tiles_x = (cam.width + 15) // 16
+    per_row = np.diff(offsets)[: tiles_x * tiles_y].reshape(tiles_y, tiles_x).sum(axis=1)
+    assert np.array_equal(counts, per_row) and counts.sum() == ref_st.n_splats
+    bands = shard.band_partition(counts, 3)
+    tot = 0
+    for band in bands:
+        f = r.finish(cloud, cam, band)
+        y0, y1 = shard.band_pixel_rows(band, cam.height)
+        assert torch.equal(f.rgb[y0:y1], ref_rgb[y0:y1])
+        assert torch.equal(f.T[y0:y1], ref_T[y0:y1])
+        assert torch.equal(f.n_contrib[y0:y1], ref_cnt[y0:y1])
+        tot += f.stats.f_blend
+    assert tot == ref_st.f_blend
+
+
+def test_band_renderer_single_rank_matches_full_frame(renderers):
+    import torch.distributed as dist
+
+    from paper_2505_24796_b200 import shard
+
+    if not dist.is_initialized():
+        dist.init_process_group("gloo", init_method="tcp://127.0.0.1:29517", rank=0, world_size=1)
+    g = load_golden("c1")
+    cam = GoldenCam(g)
+    cloud = cloud_of(g)
+    full = renderers["tcgs"].render_frame(cloud, cam)
+    br = shard.BandRenderer("cuda")
+    bf = br.render(cloud, cam)
+    assert bf.bands == [(0, (cam.height + 15) // 16)]
+    assert torch.equal(bf.rgb, full.rgb) and torch.equal(bf.n_contrib, full.n_contrib)
+    assert bf.stats.f_blend == full.stats.f_blend and bf.stats.n_splats == full.stats.n_splats
+
+
+def test_launch_counter_counts_frame_kernels(renderers):
+    g = load_golden("c1")
+    cam = GoldenCam(g)
+    r = renderers["tcgs"]
+    cloud = cloud_of(g)
+    r.render_frame(cloud, cam)
+    n0 = r.lib.tcgs_launch_count()
+    r.launch(cloud, cam)
+    torch.cuda.synchronize()
+    assert r.lib.tcgs_launch_count() - n0 >= 6  # K1, K2..K6 passes, K7
+
+
 # ---- full-size parity (BASELINE config shapes) against the oracle ---------------------------------
 
 @pytest.mark.slow

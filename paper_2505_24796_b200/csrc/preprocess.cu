@@ -89,8 +89,23 @@ __device__ __forceinline__ double dot3_gemv(double a0, double a1, double a2, dou
 }
 
 template <typename T>
-__device__ __forceinline__ double ld(const T *p, int64_t i) {
-    return static_cast<double>(__ldg(p + i));
+__device__ __forceinline__ double ld(const T *p, int64_t i) {  // p: shared memory (staged inputs)
+    return static_cast<double>(p[i]);
+}
+
+// ---- input staging: every array segment of the CTA's Gaussians is copied into shared memory with one
+// TMA bulk copy (cp.async.bulk, 16-B aligned segments) or, for a ragged tail, a coalesced cooperative loop;
+// the per-thread AoS reads (e.g. 48 SH floats at a 192-B stride) then hit shared memory instead of L1.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ bool bulk_ok(const T *src, int64_t elems) {
+    return ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((elems * (int64_t)sizeof(T)) % 16 == 0) && elems > 0;
 }
 
 __constant__ double SH_C1 = 0.4886025119029199;
@@ -145,17 +160,66 @@ struct PreArgs {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__restrict__ means,
-                                                         const T *__restrict__ scales, const T *__restrict__ rots,
-                                                         const T *__restrict__ opac, const T *__restrict__ feats) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__restrict__ g_means,
+                                                         const T *__restrict__ g_scales, const T *__restrict__ g_rots,
+                                                         const T *__restrict__ g_opac, const T *__restrict__ g_feats) {
+    extern __shared__ __align__(16) unsigned char pre_smem[];
+    __shared__ __align__(8) unsigned long long bar;
+    const int NT = blockDim.x;
+    const int64_t base = (int64_t)blockIdx.x * NT;
+    const int n = (int)(a.P - base < NT ? a.P - base : NT);
+    const int F = a.sh_degree < 0 ? 3 : 3 * (a.sh_degree + 1) * (a.sh_degree + 1);  // features per Gaussian
+    // staged SoA segments, each 16-B aligned: means 3, scales 3, rotations 4, opacity 1, features F per Gaussian
+    const int per[5] = {3, 3, 4, 1, F};
+    const T *src[5] = {g_means, g_scales, g_rots, g_opac, g_feats};
+    T *seg[5];
+    {
+        size_t off = 0;
+        for (int q = 0; q < 5; q++) {
+            seg[q] = reinterpret_cast<T *>(pre_smem + off);
+            off += (((size_t)per[q] * NT * sizeof(T)) + 15) / 16 * 16;
+        }
+    }
+    bool any_bulk = false;
+    for (int q = 0; q < 5; q++) any_bulk |= bulk_ok(src[q] + base * per[q], (int64_t)n * per[q]);
+    if (threadIdx.x == 0 && any_bulk) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && any_bulk) {
+        uint32_t tx = 0;
+        for (int q = 0; q < 5; q++)
+            if (bulk_ok(src[q] + base * per[q], (int64_t)n * per[q])) tx += (uint32_t)(n * per[q] * sizeof(T));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(tx) : "memory");
+        for (int q = 0; q < 5; q++)
+            if (bulk_ok(src[q] + base * per[q], (int64_t)n * per[q]))
+                bulk_g2s(seg[q], src[q] + base * per[q], (uint32_t)(n * per[q] * sizeof(T)), &bar);
+    }
+    for (int q = 0; q < 5; q++)  // ragged / unaligned segments: coalesced cooperative copy
+        if (!bulk_ok(src[q] + base * per[q], (int64_t)n * per[q]))
+            for (int e = threadIdx.x; e < n * per[q]; e += NT) seg[q][e] = src[q][base * per[q] + e];
+    if (any_bulk) {
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+            "@!P1 bra WAIT_%=;\n"
+            "}\n" ::"r"(smem_u32(&bar))
+            : "memory");
+    }
+    __syncthreads();
+    const int l = threadIdx.x;
+    const T *means = seg[0], *scales = seg[1], *rots = seg[2], *opac = seg[3], *feats = seg[4];
+    const int64_t i = base + l;
     const bool in_range = i < a.P;
     unsigned long long key = ~0ull;  // "touches nothing": rewritten by depth_key_fix
     uint32_t touched = 0;
     bool dropped = false;
     if (in_range) {
         const double *V = a.cam.view;
-        const double m0 = ld(means, 3 * i), m1 = ld(means, 3 * i + 1), m2 = ld(means, 3 * i + 2);
+        const double m0 = ld(means, 3 * l), m1 = ld(means, 3 * l + 1), m2 = ld(means, 3 * l + 2);
         double t[3];
 #pragma unroll
         for (int k = 0; k < 3; k++) t[k] = dot3_gemv(V[4 * k + 0], V[4 * k + 1], V[4 * k + 2], m0, m1, m2) + V[4 * k + 3];
@@ -169,13 +233,13 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
             const double my = fy * t[1] / tz + a.cam.cy;
             const double jac[2][3] = {{fx / tz, 0.0, -fx * t[0] / (tz * tz)}, {0.0, fy / tz, -fy * t[1] / (tz * tz)}};
             // covariance_of (src/tilesplat/scene.py:83-101)
-            const double w = ld(rots, 4 * i), x = ld(rots, 4 * i + 1), y = ld(rots, 4 * i + 2), z = ld(rots, 4 * i + 3);
+            const double w = ld(rots, 4 * l), x = ld(rots, 4 * l + 1), y = ld(rots, 4 * l + 2), z = ld(rots, 4 * l + 3);
             const double r[3][3] = {
                 {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
                 {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
                 {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)},
             };
-            const double s0 = ld(scales, 3 * i), s1 = ld(scales, 3 * i + 1), s2 = ld(scales, 3 * i + 2);
+            const double s0 = ld(scales, 3 * l), s1 = ld(scales, 3 * l + 1), s2 = ld(scales, 3 * l + 2);
             const double sq[3] = {s0 * s0, s1 * s1, s2 * s2};
             double mm[3][3], c[3][3], cov[3][3];
 #pragma unroll
@@ -277,19 +341,19 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
                     rc.s11 = (float)s11;
                     rc.s12 = (float)s12;
                     rc.s22 = (float)s22;
-                    const double o = ld(opac, i);
+                    const double o = ld(opac, l);
                     rc.ln_o = (float)log(o);
                     rc.opacity = (float)o;
                     float col[3];
                     if (a.sh_degree < 0) {
-                        col[0] = (float)ld(feats, 3 * i);
-                        col[1] = (float)ld(feats, 3 * i + 1);
-                        col[2] = (float)ld(feats, 3 * i + 2);
+                        col[0] = (float)ld(feats, 3 * l);
+                        col[1] = (float)ld(feats, 3 * l + 1);
+                        col[2] = (float)ld(feats, 3 * l + 2);
                     } else {
                         const int K = (a.sh_degree + 1) * (a.sh_degree + 1);
                         const double dx = m0 - a.campos[0], dy = m1 - a.campos[1], dz = m2 - a.campos[2];
                         const double nn = sqrt(dx * dx + dy * dy + dz * dz);
-                        sh_color(feats + (size_t)i * K * 3, a.sh_degree, dx / nn, dy / nn, dz / nn, col);
+                        sh_color(feats + (size_t)l * K * 3, a.sh_degree, dx / nn, dy / nn, dz / nn, col);
                     }
                     rc.r = col[0];
                     rc.g = col[1];
@@ -322,6 +386,26 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
     }
 }
 
+
+template <typename T>
+cudaError_t launch_k1(const PreArgs &a, const tcgs_scene &scene, int F, int nt, cudaStream_t st) {
+    size_t smem = 0;
+    for (int per : {3, 3, 4, 1, F}) smem += ((size_t)per * nt * sizeof(T) + 15) / 16 * 16;
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t e = cudaFuncSetAttribute(preprocess_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = smem;
+    }
+    const unsigned blocks = (unsigned)((scene.P + nt - 1) / nt);
+    note_launch();
+    preprocess_kernel<T><<<blocks, nt, smem, st>>>(a, (const T *)scene.means, (const T *)scene.scales,
+                                                  (const T *)scene.rotations, (const T *)scene.opacities,
+                                                  (const T *)scene.features);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug,
@@ -348,18 +432,9 @@ cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, c
     a.dbg_mean2d = at<double>(ws, L.dbg_mean2d);
     a.ctr = at<DevCounters>(ws, L.counters);
     if (scene.P <= 0) return cudaSuccess;
-    const unsigned blocks = (unsigned)((scene.P + 255) / 256);
-    if (scene.dtype == TCGS_F64) {
-        note_launch();
-        preprocess_kernel<double><<<blocks, 256, 0, st>>>(
-            a, (const double *)scene.means, (const double *)scene.scales, (const double *)scene.rotations,
-            (const double *)scene.opacities, (const double *)scene.features);
-    } else {
-        note_launch();
-        preprocess_kernel<float><<<blocks, 256, 0, st>>>(
-            a, (const float *)scene.means, (const float *)scene.scales, (const float *)scene.rotations,
-            (const float *)scene.opacities, (const float *)scene.features);
-    }
+    const int F = scene.sh_degree < 0 ? 3 : 3 * (scene.sh_degree + 1) * (scene.sh_degree + 1);
+    if (scene.dtype == TCGS_F64) return launch_k1<double>(a, scene, F, 128, st);
+    return launch_k1<float>(a, scene, F, 256, st);
     return cudaGetLastError();
 }
 

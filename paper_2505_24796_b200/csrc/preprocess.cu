@@ -108,36 +108,70 @@ __device__ __forceinline__ bool bulk_ok(const T *src, int64_t elems) {
     return ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((elems * (int64_t)sizeof(T)) % 16 == 0) && elems > 0;
 }
 
-__constant__ double SH_C1 = 0.4886025119029199;
-__constant__ double SH_C2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005, -1.0925484305920792,
-                                0.5462742152960396};
-__constant__ double SH_C3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
-                                -0.4570457994644658, 1.445305721320277, -0.5900435899266435};
-
-// 3DGS spherical-harmonics colour (degree <= 3), float64; NOT in the reference (parity unpinned,
-// SURVEY.md Appendix E).  Same operation order as oracle/tcgs_oracle.c:oracle_sh_color.
+// 3DGS spherical-harmonics colour (degree <= 3), NOT in the reference (parity unpinned, SURVEY.md
+// Appendix E; oracle/tcgs_oracle.c:oracle_sh_color is the float64 restatement it is tested against).
+// The basis is evaluated once per Gaussian and dotted with the three channels in fp32 FMA: the colour is
+// stored as fp32 anyway, and the fp32 evaluation stays within ~1e-6 of the float64 restatement.
 template <typename T>
-__device__ void sh_color(const T *sh, int deg, double x, double y, double z, float out[3]) {
-    const double C0 = 0.28209479177387814;
-    for (int ch = 0; ch < 3; ch++) {
-        double r = C0 * ld(sh, 0 * 3 + ch);
-        if (deg >= 1) r += -SH_C1 * y * ld(sh, 1 * 3 + ch) + SH_C1 * z * ld(sh, 2 * 3 + ch) - SH_C1 * x * ld(sh, 3 * 3 + ch);
-        if (deg >= 2) {
-            double xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
-            r += SH_C2[0] * xy * ld(sh, 4 * 3 + ch) + SH_C2[1] * yz * ld(sh, 5 * 3 + ch) +
-                 SH_C2[2] * (2.0 * zz - xx - yy) * ld(sh, 6 * 3 + ch) + SH_C2[3] * xz * ld(sh, 7 * 3 + ch) +
-                 SH_C2[4] * (xx - yy) * ld(sh, 8 * 3 + ch);
-            if (deg >= 3) {
-                r += SH_C3[0] * y * (3.0 * xx - yy) * ld(sh, 9 * 3 + ch) + SH_C3[1] * xy * z * ld(sh, 10 * 3 + ch) +
-                     SH_C3[2] * y * (4.0 * zz - xx - yy) * ld(sh, 11 * 3 + ch) +
-                     SH_C3[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy) * ld(sh, 12 * 3 + ch) +
-                     SH_C3[4] * x * (4.0 * zz - xx - yy) * ld(sh, 13 * 3 + ch) +
-                     SH_C3[5] * z * (xx - yy) * ld(sh, 14 * 3 + ch) + SH_C3[6] * x * (xx - 3.0 * yy) * ld(sh, 15 * 3 + ch);
+__device__ void sh_color(const T *sh, int deg, double dx, double dy, double dz, float out[3]) {
+    const float x = (float)dx, y = (float)dy, z = (float)dz;
+    float b[16];
+    b[0] = 0.28209479177387814f;
+    int K = 1;
+    if (deg >= 1) {
+        const float C1 = 0.4886025119029199f;
+        b[1] = -C1 * y;
+        b[2] = C1 * z;
+        b[3] = -C1 * x;
+        K = 4;
+    }
+    if (deg >= 2) {
+        const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+        b[4] = 1.0925484305920792f * xy;
+        b[5] = -1.0925484305920792f * yz;
+        b[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+        b[7] = -1.0925484305920792f * xz;
+        b[8] = 0.5462742152960396f * (xx - yy);
+        K = 9;
+        if (deg >= 3) {
+            b[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+            b[10] = 2.890611442640554f * xy * z;
+            b[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+            b[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+            b[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+            b[14] = 1.445305721320277f * z * (xx - yy);
+            b[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
+            K = 16;
+        }
+    }
+    float r0 = 0.0f, r1 = 0.0f, r2 = 0.0f;
+    if (sizeof(T) == 4 && K == 16) {
+        // 48 floats per Gaussian = 12 LDS.128 (a 192-B per-thread stride: 4-way bank conflicts instead of
+        // the 16-way of scalar loads)
+        const float4 *v = reinterpret_cast<const float4 *>(sh);
+#pragma unroll
+        for (int q = 0; q < 12; q++) {
+            const float4 f = v[q];
+            const float e[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int idx = 4 * q + u, k = idx / 3, ch = idx % 3;
+                float &acc = ch == 0 ? r0 : (ch == 1 ? r1 : r2);
+                acc = __fmaf_rn(b[k], e[u], acc);
             }
         }
-        r += 0.5;
-        out[ch] = (float)(r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r));
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; k++)
+            if (k < K) {
+                r0 = __fmaf_rn(b[k], (float)sh[3 * k + 0], r0);
+                r1 = __fmaf_rn(b[k], (float)sh[3 * k + 1], r1);
+                r2 = __fmaf_rn(b[k], (float)sh[3 * k + 2], r2);
+            }
     }
+    out[0] = fminf(fmaxf(r0 + 0.5f, 0.0f), 1.0f);
+    out[1] = fminf(fmaxf(r1 + 0.5f, 0.0f), 1.0f);
+    out[2] = fminf(fmaxf(r2 + 0.5f, 0.0f), 1.0f);
 }
 
 struct PreArgs {
@@ -233,7 +267,13 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
             const double my = fy * t[1] / tz + a.cam.cy;
             const double jac[2][3] = {{fx / tz, 0.0, -fx * t[0] / (tz * tz)}, {0.0, fy / tz, -fy * t[1] / (tz * tz)}};
             // covariance_of (src/tilesplat/scene.py:83-101)
-            const double w = ld(rots, 4 * l), x = ld(rots, 4 * l + 1), y = ld(rots, 4 * l + 2), z = ld(rots, 4 * l + 3);
+            double w, x, y, z;
+            if (sizeof(T) == 4) {
+                const float4 q4 = reinterpret_cast<const float4 *>(rots)[l];
+                w = q4.x, x = q4.y, y = q4.z, z = q4.w;
+            } else {
+                w = ld(rots, 4 * l), x = ld(rots, 4 * l + 1), y = ld(rots, 4 * l + 2), z = ld(rots, 4 * l + 3);
+            }
             const double r[3][3] = {
                 {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
                 {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
@@ -342,7 +382,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
                     rc.s12 = (float)s12;
                     rc.s22 = (float)s22;
                     const double o = ld(opac, l);
-                    rc.ln_o = (float)log(o);
+                    rc.ln_o = logf((float)o);
                     rc.opacity = (float)o;
                     float col[3];
                     if (a.sh_degree < 0) {

@@ -253,11 +253,15 @@ __device__ __forceinline__ void make_vrow(const float v[6], uint4 &lo8, uint4 &h
 struct Cursor {
     int tile, seq, c, chunks, n;
     uint32_t beg;
+    float ox, oy;  // tile centre (16tx+8, 16ty+8), tensor_path.py:21-22
 };
 
 __device__ __forceinline__ void cursor_tile(Cursor &k, const RenderArgs &a) {
     k.c = 0;
     if (k.tile < a.n_tiles) {
+        const int tx = k.tile % a.tiles_x, ty = a.band_y0 + k.tile / a.tiles_x;
+        k.ox = (float)(tx * TILE + 8);
+        k.oy = (float)(ty * TILE + 8);
         const uint2 rg = a.ranges[k.tile];
         k.beg = rg.x;
         k.n = (int)(rg.y - rg.x);
@@ -318,10 +322,7 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
         const bool valid = cur.c * 32 + lane < cur.n;
         float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool live = false;
-        if (valid) {
-            const int tx = cur.tile % a.tiles_x, ty = a.band_y0 + cur.tile / a.tiles_x;
-            live = gaussian_coeffs(rc, tx * TILE + 8.0, ty * TILE + 8.0, v);  // tile_center (tensor_path.py:21-22)
-        }
+        if (valid) live = gaussian_coeffs(rc, (double)cur.ox, (double)cur.oy, v);  // tile_center (tensor_path.py:21-22)
         uint4 vlo = make_uint4(0, 0, 0, 0), vhi = make_uint4(0, 0, 0, 0);
         if (TC && live) make_vrow<MODE>(v, vlo, vhi);
         const float4 col = make_float4(rc.r, rc.g, rc.b, 0.f);

@@ -119,6 +119,14 @@ int tcgs_render(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts
  * frame overflowed max_splats (stats->max_splats_needed then says how many are needed). */
 int tcgs_read_stats(const void *ws, int64_t P, const tcgs_opts *opts, tcgs_stats *stats, void *stream);
 
+/* Pipelined frames (no host synchronisation): tcgs_snapshot_stats enqueues a copy of the frame's
+ * counters (tcgs_counters_bytes() bytes, at offset 0 of the workspace) to `dst` (pinned host or device
+ * memory) on `stream`; once that copy has completed, tcgs_decode_stats turns the snapshot into the
+ * same tcgs_stats tcgs_read_stats returns (including TCGS_ERR_CAPACITY). */
+size_t tcgs_counters_bytes(void);
+int tcgs_snapshot_stats(const void *ws, void *dst, void *stream);
+int tcgs_decode_stats(const void *snapshot, const tcgs_opts *opts, tcgs_stats *stats);
+
 /* Debug/KAT entry: blend caller-given projected records through K7.
  *   mean2d [P,2] f64, conic [P,3] f64 (s11,s12,s22), opacity [P] f64, rgb [P,3] f32 (device);
  *   tile lists as CSR: offsets [n_tiles+1] i64, ids [N] i32 (device), row-major tiles. */

@@ -62,6 +62,9 @@ SIGNATURES = {
     "tcgs_render": (ctypes.c_int, [ctypes.POINTER(Scene), ctypes.POINTER(Camera), ctypes.POINTER(Opts), _P,
                                    ctypes.c_size_t, _I64, _P, _P, _P, _P]),
     "tcgs_read_stats": (ctypes.c_int, [_P, _I64, ctypes.POINTER(Opts), ctypes.POINTER(Stats), _P]),
+    "tcgs_counters_bytes": (ctypes.c_size_t, []),
+    "tcgs_snapshot_stats": (ctypes.c_int, [_P, _P, _P]),
+    "tcgs_decode_stats": (ctypes.c_int, [_P, ctypes.POINTER(Opts), ctypes.POINTER(Stats)]),
     "tcgs_blend_lists": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, ctypes.POINTER(Camera), ctypes.POINTER(Opts),
                                         _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "tcgs_copy_lists": (ctypes.c_int, [_P, _I64, ctypes.POINTER(Camera), ctypes.POINTER(Opts), _I64, _P, _P, _P]),

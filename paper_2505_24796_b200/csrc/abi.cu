@@ -142,14 +142,8 @@ int tcgs_render(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts
     return tcgs_blend(scene->P, cam, opts, ws, ws_bytes, max_splats, rgb, T, n_contrib, stream);
 }
 
-int tcgs_read_stats(const void *ws, int64_t P, const tcgs_opts *opts, tcgs_stats *stats, void *stream) {
-    if (!ws || !stats) return fail(TCGS_ERR_INVALID_ARG, "null workspace or stats");
-    (void)P;
-    DevCounters c;
-    cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t e = cudaMemcpyAsync(&c, ws, sizeof(c), cudaMemcpyDeviceToHost, st);  // counters sit at offset 0
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return cuda_fail(e, "read_stats");
+namespace {
+int decode_stats(const DevCounters &c, const tcgs_opts *opts, tcgs_stats *stats) {
     memset(stats, 0, sizeof(*stats));
     stats->n_splats = (int64_t)c.n_splats;
     stats->max_splats_needed = (int64_t)c.n_splats;
@@ -165,6 +159,34 @@ int tcgs_read_stats(const void *ws, int64_t P, const tcgs_opts *opts, tcgs_stats
                              : stats->f_blend + stats->f_cull + stats->pixels_terminated;
     if (c.overflow) return fail(TCGS_ERR_CAPACITY, "splat count exceeded max_splats");
     return TCGS_OK;
+}
+}  // namespace
+
+int tcgs_read_stats(const void *ws, int64_t P, const tcgs_opts *opts, tcgs_stats *stats, void *stream) {
+    if (!ws || !stats) return fail(TCGS_ERR_INVALID_ARG, "null workspace or stats");
+    (void)P;
+    DevCounters c;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyAsync(&c, ws, sizeof(c), cudaMemcpyDeviceToHost, st);  // counters sit at offset 0
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "read_stats");
+    return decode_stats(c, opts, stats);
+}
+
+size_t tcgs_counters_bytes(void) { return sizeof(DevCounters); }
+
+int tcgs_snapshot_stats(const void *ws, void *dst, void *stream) {
+    if (!ws || !dst) return fail(TCGS_ERR_INVALID_ARG, "null workspace or destination");
+    cudaError_t e = cudaMemcpyAsync(dst, ws, sizeof(DevCounters), cudaMemcpyDefault, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "snapshot_stats");
+    return TCGS_OK;
+}
+
+int tcgs_decode_stats(const void *snapshot, const tcgs_opts *opts, tcgs_stats *stats) {
+    if (!snapshot || !stats) return fail(TCGS_ERR_INVALID_ARG, "null snapshot or stats");
+    DevCounters c;
+    memcpy(&c, snapshot, sizeof(c));
+    return decode_stats(c, opts, stats);
 }
 
 int tcgs_blend_lists(int64_t P, const double *mean2d, const double *conic, const double *opacity, const float *colors,

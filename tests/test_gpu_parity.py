@@ -339,6 +339,28 @@ def test_launch_counter_counts_frame_kernels(renderers):
     assert r.lib.tcgs_launch_count() - n0 >= 6  # K1, K2..K6 passes, K7
 
 
+def test_frame_pipeline_matches_render_frame(renderers):
+    """Host frames through the overlapped upload / render / readback pipeline equal synchronous frames."""
+    from paper_2505_24796_b200.pipeline import FramePipeline
+
+    scene, cams = synthetic.config_scene("c4", 0.02)  # orbit views of a ball scene, SH3
+    host = {k: torch.as_tensor(np.ascontiguousarray(scene[k])).pin_memory()
+            for k in ("means", "scales", "rotations", "opacities", "features")}
+    views = [cams[i] for i in (0, 40, 80, 120, 160)]
+    r = tcgs.Renderer("cuda", "tcgs")
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    ref = []
+    for cam in views:
+        f = r.render_frame(cloud, cam, timed=False)
+        ref.append((f.rgb.cpu().clone(), f.stats))
+    pipe = FramePipeline(tcgs.Renderer("cuda", "tcgs"))
+    tickets = [pipe.submit(host, scene["sh_degree"], cam) for cam in views]
+    for t, (rgb, st) in zip(tickets, ref):
+        out, pst = pipe.result(t)
+        assert torch.equal(out, rgb)
+        assert (pst.f_blend, pst.f_cull, pst.f_skip, pst.n_splats) == (st.f_blend, st.f_cull, st.f_skip, st.n_splats)
+
+
 # ---- full-size parity (BASELINE config shapes) against the oracle ---------------------------------
 
 @pytest.mark.slow

@@ -8,7 +8,7 @@ import os
 import shutil
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libtcgs.so")
+LIB_PATH = os.environ.get("TCGS_LIB") or os.path.join(HERE, "_lib", "libtcgs.so")  # TCGS_LIB: A/B builds
 
 TCGS_OK = 0
 TCGS_ERR_INVALID_ARG = -1

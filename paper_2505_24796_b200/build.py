@@ -29,23 +29,26 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile libtcgs.so (``out``/``defines``: an experiment variant, e.g. -DTCGS_K7_WAIT_HINT=0)."""
+    if out is None and not force and not _stale():
         return LIB_PATH
-    os.makedirs(os.path.join(LIB_DIR, "obj"), exist_ok=True)
+    lib_path = out or LIB_PATH
+    obj_dir = os.path.join(os.path.dirname(lib_path), "obj" if out is None else "obj_" + os.path.basename(lib_path))
+    os.makedirs(obj_dir, exist_ok=True)
     objs = []
     for src in SOURCES:
-        obj = os.path.join(LIB_DIR, "obj", src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *COMMON, *PER_FILE_FLAGS.get(src, []), "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *ARCH, *COMMON, *defines, *PER_FILE_FLAGS.get(src, []), "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB_PATH + f".tmp{os.getpid()}"
+    tmp = lib_path + f".tmp{os.getpid()}"
     subprocess.run([NVCC, *ARCH, "-shared", "-cudart", "static", *objs, "-o", tmp], check=True)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":

@@ -25,7 +25,10 @@ constexpr int K7_CONSUMER_WARPS = 8;  // one pixel per thread, 16x16 tile
 constexpr int K7_PRODUCERS = 2;       // producer warps (alternate 32-entry chunks, token-ordered compaction)
 constexpr int K7_THREADS = 32 * (K7_CONSUMER_WARPS + K7_PRODUCERS);
 constexpr int K7_BATCH = 32;          // live Gaussians per tcgen05 batch (MMA N)
-constexpr int K7_STAGES = 4;          // shared-memory B-operand stages
+#ifndef TCGS_K7_STAGES
+#define TCGS_K7_STAGES 4
+#endif
+constexpr int K7_STAGES = TCGS_K7_STAGES;  // shared-memory B-operand stages
 constexpr int K7_TMEM_BUFS = 2;       // TMEM accumulator buffers
 constexpr int K7_TMEM_COLS = K7_TMEM_BUFS * 2 * K7_BATCH;  // buffers x pixel halves x N
 constexpr int K7_CTAS_PER_SM = 3;

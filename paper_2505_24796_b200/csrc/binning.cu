@@ -28,6 +28,8 @@
 // read fused with the key rebase, so passes above the key range or with a
 // single digit value exit at entry.  All counts live on the device: a frame needs no
 // host synchronisation (graph-capturable).
+#include <algorithm>
+
 #include "tcgs_internal.cuh"
 
 namespace tcgs {
@@ -78,29 +80,163 @@ __device__ __forceinline__ unsigned warp_peers(int d) {
 }
 
 // ---------------------------------------------------------------- K2 prologue
-// depth bits -> bits - min over visible; Gaussians touching no tile get 0 (they emit nothing, so their
-// place in the depth order is irrelevant).  Histograms every digit below the key range in the same read.
-__global__ void __launch_bounds__(256) depth_fix_hist(const unsigned long long *src, unsigned long long *keys,
-                                                      uint32_t *idx, int64_t P, DevCounters *ctr,
-                                                      SortState *ss) {
-    __shared__ uint32_t h[MAX_PASSES][RADIX];
-    for (int e = threadIdx.x; e < MAX_PASSES * RADIX; e += blockDim.x) (&h[0][0])[e] = 0;
+// The float64 depth bits minus the visible minimum span up to ~55 bits (depths 2..20: exponents 1..4).
+// They are radix-sorted on a 24-bit prefix only (3 passes instead of 7): key = (bits - min) >> shift with
+// shift chosen so every visible key is <= DEPTH_KEY_MAX - 1; Gaussians touching no tile get DEPTH_KEY_MAX
+// and sort last (they emit nothing).  Equal prefixes whose full keys differ are put in float64 order by
+// depth_fixup afterwards (stable: ties keep the index order, tiling.py:55-58).
+constexpr uint32_t DEPTH_KEY_BITS = 24;
+constexpr uint32_t DEPTH_KEY_MAX = (1u << DEPTH_KEY_BITS) - 1u;
+constexpr int DEPTH_PASSES = 3;
+
+__device__ __forceinline__ int depth_shift(unsigned long long range) {
+    if (range < (unsigned long long)DEPTH_KEY_MAX) return 0;
+    return (64 - __clzll((long long)range)) - (int)(DEPTH_KEY_BITS - 1);  // range >> shift < 2^23
+}
+
+__global__ void __launch_bounds__(256) depth_fix_hist(const unsigned long long *src, uint32_t *keys, uint32_t *idx,
+                                                      int64_t P, DevCounters *ctr, SortState *ss) {
+    __shared__ uint32_t h[DEPTH_PASSES][RADIX];
+    for (int e = threadIdx.x; e < DEPTH_PASSES * RADIX; e += blockDim.x) (&h[0][0])[e] = 0;
     __syncthreads();
     const unsigned long long kmin = ctr->key_min;
     const unsigned long long range = ctr->n_visible ? ctr->key_max - kmin : 0ull;
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->key_range = range;
-    const int np = range ? (64 - __clzll((long long)range) + RADIX_BITS - 1) / RADIX_BITS : 0;
+    const int shift = depth_shift(range);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctr->key_range = DEPTH_KEY_MAX;  // the prefix keys span [0, DEPTH_KEY_MAX]
+        ctr->depth_shift = shift;
+    }
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-        unsigned long long k = src[i];  // K1's output stays intact: tcgs_bin can run again (other bands)
-        k = (k == ~0ull) ? 0ull : k - kmin;
-        keys[i] = k;
+        const unsigned long long k = src[i];  // K1's output stays intact: tcgs_bin can run again (other bands)
+        const uint32_t key = (k == ~0ull) ? DEPTH_KEY_MAX : (uint32_t)((k - kmin) >> shift);
+        keys[i] = key;
         idx[i] = (uint32_t)i;
-        for (int p = 0; p < np; p++) atomicAdd(&h[p][(unsigned)(k >> (RADIX_BITS * p)) & (RADIX - 1)], 1u);
+#pragma unroll
+        for (int p = 0; p < DEPTH_PASSES; p++) atomicAdd(&h[p][(key >> (RADIX_BITS * p)) & (RADIX - 1)], 1u);
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < np * RADIX; e += blockDim.x) {
+    for (int e = threadIdx.x; e < DEPTH_PASSES * RADIX; e += blockDim.x) {
         const uint32_t c = (&h[0][0])[e];
         if (c) atomicAdd(&(&ss->ghist[0][0])[e], c);
+    }
+}
+
+// ---------------------------------------------------------------- K2 fix-up
+// After the prefix sort, a run of equal prefixes is in index order; put it in (float64 depth, index)
+// order.  Runs of <= FIX_SHORT: one thread, insertion sort (stable).  Longer runs go to depth_fixup_long.
+constexpr int FIX_SHORT = 32;
+constexpr int FIX_SMEM = 4096;
+
+__global__ void __launch_bounds__(256) depth_fixup(const uint32_t *k0, const uint32_t *k1, uint32_t *i0, uint32_t *i1,
+                                                   const unsigned long long *src, int64_t P, DevCounters *ctr,
+                                                   uint32_t *long_runs) {
+    if (ctr->depth_shift == 0) return;  // the prefix is the whole key
+    const uint32_t *key = ctr->depth_cur ? k1 : k0;
+    uint32_t *idx = ctr->depth_cur ? i1 : i0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = key[i];
+        if (k == DEPTH_KEY_MAX) continue;
+        if (i > 0 && key[i - 1] == k) continue;
+        if (i + 1 >= P || key[i + 1] != k) continue;
+        int64_t e = i + 2;
+        while (e < P && key[e] == k && e - i <= FIX_SHORT) e++;
+        if (e - i > FIX_SHORT) {
+            const unsigned slot = atomicAdd(&ctr->n_long_runs, 1u);
+            if (slot < (unsigned)FIX_SMEM) long_runs[slot] = (uint32_t)i;
+            continue;
+        }
+        const int n = (int)(e - i);
+        uint32_t g[FIX_SHORT];
+        unsigned long long f[FIX_SHORT];
+        bool moved = false;
+        for (int j = 0; j < n; j++) {
+            const uint32_t gj = idx[i + j];
+            const unsigned long long fj = src[gj];
+            int m = j - 1;
+            while (m >= 0 && f[m] > fj) {  // strict: equal depths keep the index order
+                f[m + 1] = f[m];
+                g[m + 1] = g[m];
+                m--;
+                moved = true;
+            }
+            f[m + 1] = fj;
+            g[m + 1] = gj;
+        }
+        if (moved)
+            for (int j = 0; j < n; j++) idx[i + j] = g[j];
+    }
+}
+
+// Long runs (rare: > FIX_SHORT Gaussians whose float64 depths share the 24-bit prefix): one CTA per run,
+// bitonic sort of (depth bits, index) pairs -- in shared memory up to FIX_SMEM elements, otherwise in place
+// over the run with a global-memory scratch of the same length.
+__device__ __forceinline__ bool pair_less(unsigned long long fa, uint32_t ga, unsigned long long fb, uint32_t gb) {
+    return fa < fb || (fa == fb && ga < gb);
+}
+
+__global__ void __launch_bounds__(256) depth_fixup_long(const uint32_t *k0, const uint32_t *k1, uint32_t *i0,
+                                                        uint32_t *i1, const unsigned long long *src, int64_t P,
+                                                        DevCounters *ctr, const uint32_t *long_runs,
+                                                        unsigned long long *gscratch) {
+    __shared__ unsigned long long sf[FIX_SMEM];
+    __shared__ uint32_t sg[FIX_SMEM];
+    const unsigned nruns = ctr->n_long_runs;
+    if (ctr->depth_shift == 0 || nruns == 0) return;
+    const uint32_t *key = ctr->depth_cur ? k1 : k0;
+    uint32_t *idx = ctr->depth_cur ? i1 : i0;
+    for (unsigned r = blockIdx.x; r < nruns; r += gridDim.x) {
+        int64_t s;
+        if (nruns <= (unsigned)FIX_SMEM) {
+            s = long_runs[r];
+        } else {  // the list overflowed: recover run starts by scanning (r-th run start of the array)
+            if (r > 0) break;
+            s = -1;
+        }
+        // process either the listed run, or (overflow) every long run sequentially in this CTA
+        for (int64_t i = (s >= 0 ? s : 0); i < P;) {
+            const uint32_t k = key[i];
+            int64_t e = i + 1;
+            while (e < P && key[e] == k) e++;
+            const int64_t n = e - i;
+            const bool do_it = k != DEPTH_KEY_MAX && n > FIX_SHORT && (s >= 0 || (i == 0 || key[i - 1] != k));
+            if (do_it) {
+                int64_t n2 = 1;
+                while (n2 < n) n2 <<= 1;
+                const bool sm = n2 <= FIX_SMEM;
+                unsigned long long *F = sm ? sf : gscratch;
+                uint32_t *G = sm ? sg : reinterpret_cast<uint32_t *>(gscratch + 2 * P);
+                for (int64_t j = threadIdx.x; j < n2; j += blockDim.x) {
+                    const uint32_t gj = j < n ? idx[i + j] : 0xffffffffu;
+                    F[j] = j < n ? src[gj] : ~0ull;
+                    G[j] = gj;
+                }
+                __syncthreads();
+                for (int64_t kk = 2; kk <= n2; kk <<= 1) {
+                    for (int64_t jj = kk >> 1; jj > 0; jj >>= 1) {
+                        for (int64_t t = threadIdx.x; t < n2; t += blockDim.x) {
+                            const int64_t u = t ^ jj;
+                            if (u > t) {
+                                const bool up = (t & kk) == 0;
+                                const bool lt = pair_less(F[u], G[u], F[t], G[t]);
+                                if (up == lt) {
+                                    const unsigned long long tf = F[t];
+                                    F[t] = F[u];
+                                    F[u] = tf;
+                                    const uint32_t tg = G[t];
+                                    G[t] = G[u];
+                                    G[u] = tg;
+                                }
+                            }
+                        }
+                        __syncthreads();
+                    }
+                }
+                for (int64_t j = threadIdx.x; j < n; j += blockDim.x) idx[i + j] = G[j];
+                __syncthreads();
+            }
+            if (s >= 0) break;
+            i = e;
+        }
     }
 }
 
@@ -608,24 +744,32 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
     cudaError_t e = cudaMemsetAsync(static_cast<char *>(ws) + L.zero_begin, 0, L.zero_bytes, st);
     // per-binning counters (K1's dropped / n_visible / key_min / key_max stay)
     if (e == cudaSuccess) e = cudaMemsetAsync(&ctr->n_splats, 0, 2 * sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(&ctr->n_long_runs, 0, sizeof(unsigned int), st);
     if (e == cudaSuccess)
         e = cudaMemsetAsync(at<uint2>(ws, L.ranges), 0, sizeof(uint2) * (size_t)(band.n_tiles() ? band.n_tiles() : 1), st);
     if (e != cudaSuccess) return e;
-    unsigned long long *k0 = at<unsigned long long>(ws, L.key64[0]);
-    unsigned long long *k1 = at<unsigned long long>(ws, L.key64[1]);
+    uint32_t *k0 = at<uint32_t>(ws, L.key64[0]);
+    uint32_t *k1 = at<uint32_t>(ws, L.key64[1]);
     uint32_t *i0 = at<uint32_t>(ws, L.idx[0]);
     uint32_t *i1 = at<uint32_t>(ws, L.idx[1]);
     if (P > 0) {
-        // K2
+        // K2: 24-bit depth-prefix radix sort + exact float64 fix-up of equal prefixes
+        const unsigned long long *src = at<unsigned long long>(ws, L.key_src);
         note_launch();
-        depth_fix_hist<<<2 * 148, 256, 0, st>>>(at<unsigned long long>(ws, L.key_src), k0, i0, P, ctr, ss_depth);
+        depth_fix_hist<<<2 * 148, 256, 0, st>>>(src, k0, i0, P, ctr, ss_depth);
         note_launch();
-        sort_plan<<<1, 256, 0, st>>>(ss_depth, MAX_PASSES, nullptr, P, P, &ctr->key_range, 1, &ctr->depth_cur);
-        for (int p = 0; p < MAX_PASSES; p++) {
-            e = launch_radix_pass<unsigned long long, DEPTH_IPT>(k0, k1, i0, i1, nullptr, P, P, p, ss_depth,
-                                                               at<uint32_t>(ws, L.lb_depth), st);
+        sort_plan<<<1, 256, 0, st>>>(ss_depth, DEPTH_PASSES, nullptr, P, P, &ctr->key_range, 1, &ctr->depth_cur);
+        for (int p = 0; p < DEPTH_PASSES; p++) {
+            e = launch_radix_pass<uint32_t, DEPTH_IPT>(k0, k1, i0, i1, nullptr, P, P, p, ss_depth,
+                                                      at<uint32_t>(ws, L.lb_depth), st);
             if (e != cudaSuccess) return e;
         }
+        note_launch();
+        depth_fixup<<<(unsigned)std::min<int64_t>(div_up(P, 256), 8 * 148), 256, 0, st>>>(
+            k0, k1, i0, i1, src, P, ctr, at<uint32_t>(ws, L.long_runs));
+        note_launch();
+        depth_fixup_long<<<148, 256, 0, st>>>(k0, k1, i0, i1, src, P, ctr, at<uint32_t>(ws, L.long_runs),
+                                              at<unsigned long long>(ws, L.fix_scratch));
     }
     if (band.n_tiles() <= 65536) return bin_tiles<uint16_t>(P, band, ws, L, cap, st);
     return bin_tiles<uint32_t>(P, band, ws, L, cap, st);
@@ -634,13 +778,15 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
 cudaError_t launch_pack_lists(int64_t P, const double *mean2d, const double *conic, const double *opacity,
                               const float *colors, const int64_t *offsets, const Band &band, void *ws,
                               const Layout &L, cudaStream_t st) {
-    if (P > 0)
+    if (P > 0) {
         note_launch();
         pack_records<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(P, mean2d, conic, opacity, colors, at<Rec>(ws, L.rec));
+    }
     const int nt = band.n_tiles();
-    if (nt > 0)
+    if (nt > 0) {
         note_launch();
         pack_ranges<<<(nt + 255) / 256, 256, 0, st>>>(offsets, band.y0 * band.tiles_x, nt, at<uint2>(ws, L.ranges));
+    }
     return cudaGetLastError();
 }
 

@@ -47,6 +47,8 @@ struct DevCounters {
     unsigned long long key_min, key_max, key_range;
     unsigned int tile_queue;
     int depth_cur, tile_cur;
+    int depth_shift;           // K2: prefix shift of the depth key (0: the prefix sort is exact)
+    unsigned int n_long_runs;  // K2 fix-up: runs of equal prefixes longer than a thread handles
 };
 
 // Per-sort bookkeeping of the onesweep LSD radix sort (all decided on the device).
@@ -63,7 +65,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 struct Layout {
-    size_t counters, sort_state[2], rec, rect, touched, key_src, key64[2], idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
+    size_t counters, sort_state[2], rec, rect, touched, key_src, key64[2], long_runs, fix_scratch, idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
     size_t blocksum, lb_depth, lb_tile, tkey[2], tval[2], ranges, total;
     size_t zero_begin, zero_bytes;  // sort state, cleared at the start of every binning
     static Layout make(int64_t P, int W, int H, int64_t cap) {
@@ -89,6 +91,8 @@ struct Layout {
         L.idx[0] = take(sizeof(uint32_t) * Pn);
         L.idx[1] = take(sizeof(uint32_t) * Pn);
         L.radius = take(sizeof(int32_t) * Pn);
+        L.long_runs = take(sizeof(uint32_t) * 4096);
+        L.fix_scratch = take((sizeof(unsigned long long) + sizeof(uint32_t)) * 2 * Pn);  // pow2-padded run <= 2P
         L.dbg_conic = take(sizeof(double) * 3 * Pn);
         L.dbg_depth = take(sizeof(double) * Pn);
         L.dbg_mean2d = take(sizeof(double) * 2 * Pn);

@@ -361,6 +361,33 @@ def test_frame_pipeline_matches_render_frame(renderers):
         assert (pst.f_blend, pst.f_cull, pst.f_skip, pst.n_splats) == (st.f_blend, st.f_cull, st.f_skip, st.n_splats)
 
 
+@pytest.mark.parametrize("n_close", [40, 3000, 6000])
+def test_depth_prefix_ties_resolved_in_float64(renderers, n_close):
+    """K2 sorts a 24-bit depth prefix, then fixes runs of equal prefixes in float64 order (ties by index).
+    n_close Gaussians share one prefix (depths 5 + k ulp, some exactly equal): the short-run, the
+    shared-memory long-run and the global-memory long-run fix-up paths; lists must equal the oracle's."""
+    rng = np.random.default_rng(n_close)
+    n = n_close + 200
+    ulp = np.spacing(5.0)
+    z = np.concatenate([5.0 + ulp * rng.integers(0, 400, n_close),  # collisions -> exact ties too
+                        rng.uniform(2.0, 20.0, 200)])
+    xy = rng.uniform(-0.05, 0.05, (n, 2)) * z[:, None]
+    q = rng.normal(size=(n, 4))
+    d = {"means": np.column_stack([xy, z]), "scales": rng.uniform(0.02, 0.08, (n, 3)) * z[:, None] / 5.0,
+         "rotations": q / np.linalg.norm(q, axis=1, keepdims=True), "opacities": rng.uniform(0.05, 0.95, n),
+         "colors": rng.uniform(0, 1, (n, 3))}
+    cam = synthetic.make_camera(64, 64)
+    r = renderers["tcgs"]
+    cloud = tcgs.GaussianCloud.from_arrays(d, "cuda", torch.float64)
+    f = r.render_frame(cloud, cam)
+    offsets, ids = r.tile_lists(cloud.P, cam)
+    proj = oracle.project(d["means"], d["scales"], d["rotations"], cam)
+    o_off, o_ids = oracle.build_tiles(proj, cam)
+    assert np.array_equal(offsets, o_off) and np.array_equal(ids, o_ids)
+    ref = oracle.render(d["means"], d["scales"], d["rotations"], d["opacities"], d["colors"], cam)
+    assert float(np.max(np.abs(f.rgb.double().cpu().numpy() - ref.rgb))) <= RGB_TOL
+
+
 # ---- full-size parity (BASELINE config shapes) against the oracle ---------------------------------
 
 @pytest.mark.slow

@@ -42,6 +42,7 @@ constexpr float LOG2E = 1.4426950408889634f;
 constexpr float CUT_LOG2 = -7.994353436858858f;  // -log2(255): beta' < CUT culls (tensor_path.py:79-81)
 constexpr float LN255 = 5.541263545158426f;
 constexpr float TERM_T = 0.0001f;                // src/tilesplat/raster.py:16
+constexpr float INV255 = 1.0f / 255.0f;          // 2^(-log2 255)
 constexpr int K7_SMEM_BYTES = 72 * 1024;         // also caps residency at 3 CTAs/SM (TMEM: 3 x 128 columns)
 constexpr int S = K7_STAGES;
 constexpr int NB = K7_TMEM_BUFS;
@@ -203,6 +204,19 @@ __device__ __forceinline__ bool gaussian_coeffs(const Rec &r, double ox, double 
     return true;
 }
 
+// FOLD modes carry beta'' = beta' + log2(255) (the EarlyCull threshold folded into v0), so a fragment passes
+// iff beta'' >= 0: its pass bit is the complement of the float's sign bit, extracted on the FMA pipe.
+template <int MODE>
+__host__ __device__ constexpr bool fold_cut() { return MODE != TCGS_ALPHA_TC_K8; }
+
+// acc + (x >> 31) * m as two FMA-pipe integer multiply-adds
+__device__ __forceinline__ uint32_t umad_hi2(uint32_t x, uint32_t m, uint32_t acc) {
+    uint32_t s, r;
+    asm("mul.hi.u32 %0, %1, 2;" : "=r"(s) : "r"(x));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(s), "r"(m), "r"(acc));
+    return r;
+}
+
 __device__ __forceinline__ __half h16(float x) { return __float2half_rn(x); }
 __device__ __forceinline__ float f32(__half x) { return __half2float(x); }
 
@@ -323,6 +337,7 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
         float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool live = false;
         if (valid) live = gaussian_coeffs(rc, (double)cur.ox, (double)cur.oy, v);  // tile_center (tensor_path.py:21-22)
+        if (fold_cut<MODE>()) v[0] -= CUT_LOG2;
         uint4 vlo = make_uint4(0, 0, 0, 0), vhi = make_uint4(0, 0, 0, 0);
         if (TC && live) make_vrow<MODE>(v, vlo, vhi);
         const float4 col = make_float4(rc.r, rc.g, rc.b, 0.f);
@@ -492,7 +507,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
         int px = 0, py = 0;
         bool inside = false, done = true, term = false, warp_done = true;
         float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
-        uint32_t cnt = 0, cull = 0, n_total = 0;
+        uint32_t cull = 0, n_total = 0;
+        float fcnt = 0.0f;  // blends of this pixel (exact in fp32; kept on the FMA pipe)
         auto flush = [&]() {
             if (inside) {
                 const int64_t p = (int64_t)py * a.width + px;
@@ -500,10 +516,10 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 a.rgb[3 * p + 1] = c1;
                 a.rgb[3 * p + 2] = c2;
                 a.T[p] = T;
-                a.n_contrib[p] = (int32_t)cnt;
+                a.n_contrib[p] = (int32_t)fcnt;
                 s_pairs += n_total;
             }
-            s_blend += cnt;
+            s_blend += (uint32_t)fcnt;
             s_cull += cull;
             s_term += term ? 1u : 0u;
         };
@@ -524,7 +540,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 term = false;
                 T = 1.0f;
                 c0 = c1 = c2 = 0.0f;
-                cnt = cull = 0;
+                cull = 0;
+                fcnt = 0.0f;
                 n_total = m.n_total;
                 warp_done = __all_sync(FULL, done);
                 if (warp_done && lane == 0) atomicAdd(&sm.retire[cur_seq & 7], 1);
@@ -538,8 +555,12 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 const uint32_t act0 = done ? 0u : (nl >= 32 ? FULL : ((1u << nl) - 1u));
                 uint32_t act = act0;
                 const uint32_t tb = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (2 * K7_BATCH) + half * K7_BATCH;
-                uint32_t pass_all = 0;
                 int jt = 32;
+                // pass threshold of beta: the EarlyCull cut while the pixel is live, +inf once it has
+                // terminated (a float, so the test stays one FSETP and the update a predicated move)
+                const float cut0 = fold_cut<MODE>() ? 0.0f : CUT_LOG2;
+                float thr = done ? __int_as_float(0x7f800000) : cut0;
+                const float fcnt0 = fcnt;
 #pragma unroll
                 for (int hc = 0; hc < 2; hc++) {  // two 16-column halves keep 16 betas live in registers
                     uint32_t r[16];
@@ -556,32 +577,42 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                                                    p1.y * uy * uy);
                         }
                     }
-                    uint32_t pass = 0;
+                    uint32_t pass;
+                    if (fold_cut<MODE>()) {
+                        // sign bits -> fail mask with multiply-adds (FMA pipe; the ALU pipe is the busy one)
+                        uint32_t fail = 0;
 #pragma unroll
-                    for (int j = 0; j < 16; j++)
-                        if (__uint_as_float(r[j]) >= CUT_LOG2) pass |= 1u << j;
+                        for (int j = 0; j < 16; j++) fail = umad_hi2(r[j], 1u << j, fail);
+                        pass = ~fail;
+                    } else {
+                        pass = 0;
+#pragma unroll
+                        for (int j = 0; j < 16; j++)
+                            if (__uint_as_float(r[j]) >= CUT_LOG2) pass |= 1u << j;
+                    }
                     pass &= (act >> (16 * hc)) & 0xffffu;
-                    pass_all |= pass << (16 * hc);
                     const uint32_t wm = __reduce_or_sync(FULL, pass);
-                    uint32_t lm = pass;  // still-active passing columns: cleared past a termination
 #pragma unroll
                     for (int j = 0; j < 16; j++) {
                         if (wm & (1u << j)) {  // warp-uniform: some pixel of the warp passes EarlyCull here
-                            const float al = fminf(ex2_approx(__uint_as_float(r[j])), 1.0f);
+                            const float bb = __uint_as_float(r[j]);
+                            const bool p = bb >= thr;
+                            // alpha = 2^beta' (no min(alpha, 1): alpha > 1 only by rounding, and then
+                            // T - alpha T < 1e-4 terminates exactly as alpha = 1 would)
+                            const float al = fold_cut<MODE>() ? ex2_approx(bb) * INV255 : ex2_approx(bb);
                             const float tn = fmaf(-al, T, T);
-                            const float4 cc = sm.col[st][16 * hc + j];
-                            const bool p = (lm >> j) & 1u;
                             if (p && tn < TERM_T) {  // termination precedes compositing
                                 jt = 16 * hc + j;
-                                lm &= (1u << j) - 1u;
+                                thr = __int_as_float(0x7f800000);
                             }
-                            if (p && !(tn < TERM_T)) {
+                            if (p && tn >= TERM_T) {
+                                const float4 cc = sm.col[st][16 * hc + j];
                                 const float w = al * T;
                                 c0 = fmaf(w, cc.x, c0);
                                 c1 = fmaf(w, cc.y, c1);
                                 c2 = fmaf(w, cc.z, c2);
                                 T = tn;
-                                cnt++;
+                                fcnt += 1.0f;
                             }
                         }
                     }
@@ -589,11 +620,10 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 }
                 term = term || jt < 32;
                 done = done || jt < 32;
-                const uint32_t pass = pass_all;
-                // EarlyCull counts: live columns failing the cut before termination, plus the dead
+                // EarlyCull counts: valid columns before the termination that did not blend, plus the dead
                 // Gaussians of the list before the terminating one
                 const uint32_t before = jt >= 32 ? FULL : ((1u << jt) - 1u);
-                cull += __popc(act0 & ~pass & before);
+                cull += __popc(act0 & before) - (uint32_t)(fcnt - fcnt0);
                 if (jt < 32) cull += sm.dead_before[st][jt];
                 if (__all_sync(FULL, done)) {
                     warp_done = true;

@@ -26,7 +26,16 @@ from .raster import (  # noqa: F401
     render,
 )
 
+from .pipeline import FramePipeline  # noqa: F401,E402
+from .ply import SceneFormatError, SceneValidationError, load_ply, read_ply, write_ply  # noqa: F401,E402
+
 __all__ = [
+    "FramePipeline",
+    "SceneFormatError",
+    "SceneValidationError",
+    "load_ply",
+    "read_ply",
+    "write_ply",
     "ALPHA_CULL_THRESHOLD",
     "TERMINATION_THRESHOLD",
     "TILE_SIZE",

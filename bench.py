@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--backend", default="tcgs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--streams", type=int, default=3, help="views in flight (one workspace + CUDA stream each)")
     return ap.parse_args()
 
 
@@ -266,17 +267,20 @@ def run_tcgs(args):
         first = br.render(cloud, base, with_stats=True)  # sizes the workspace
         st0 = first.stats
     else:
-        r = tcgs.Renderer(dev, args.backend)
-        st0 = r.render_frame(cloud, base).stats  # sizes the workspace; stats of the base view
+        vr = tcgs.ViewRenderer(dev, args.backend, max(1, args.streams))
+        r = vr.renderers[0]
+        st0 = vr.warm(cloud, base)  # sizes the workspaces; stats of the base view
     stream = torch.cuda.current_stream(dev)
 
     def frame(cam, ev=None):
         if bands_mode:
             return br.render(cloud, cam, with_stats=False, timers=ev)
-        return r.launch(cloud, cam, timers=ev)
+        return vr.launch(cloud, cam, timers=ev)
 
     for k in range(args.warmup):
         frame(my_views[k])
+    if not bands_mode:
+        vr.join()
     torch.cuda.synchronize(dev)
 
     # ---- timed region: K frames, inputs resident in HBM
@@ -292,6 +296,8 @@ def run_tcgs(args):
         start.record(stream)
         for k in range(args.steps):
             frame(my_views[args.warmup + k], evs[k])
+        if not bands_mode:
+            vr.join()
         stop.record(stream)
         torch.cuda.synchronize(dev)
     launches = r.lib.tcgs_launch_count() - launches0
@@ -308,10 +314,23 @@ def run_tcgs(args):
     ms_max, blend_max = float(t[0].item()), float(t[1].item())
 
     # per-frame stats of this rank's last timed view (device counters; the band's in bands mode)
+    # isolated per-stage device times (one view at a time on one stream): with several views in flight the
+    # timed region overlaps stages of different views, so its per-stage events include interference
+    iso = None
+    if not bands_mode and len(vr.renderers) > 1:
+        r0 = vr.renderers[0]
+        iso_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(min(10, args.steps))]
+        for k, ev in enumerate(iso_ev):
+            r0.launch(cloud, my_views[args.warmup + k], timers=ev)
+        torch.cuda.synchronize(dev)
+        iso = {"preprocess": sum(e[0].elapsed_time(e[1]) for e in iso_ev) / len(iso_ev),
+               "binning": sum(e[1].elapsed_time(e[2]) for e in iso_ev) / len(iso_ev),
+               "blend": sum(e[2].elapsed_time(e[3]) for e in iso_ev) / len(iso_ev)}
     if bands_mode:
         st_last = br.render(cloud, my_views[-1], with_stats=True).local.stats
     else:
-        rc, st_last = r.read_stats(cloud.P)
+        last = vr.renderers[(args.warmup + args.steps - 1 + len(vr.renderers)) % len(vr.renderers)]
+        rc, st_last = last.read_stats(cloud.P)
 
     # ---- end to end through the public API: host scene -> device, render, image -> host
     e2e = None
@@ -387,7 +406,7 @@ def run_tcgs(args):
 
     frames = args.steps if bands_mode else world * args.steps
     value = frames / (ms_max / 1e3)
-    blend_avg = sum(blend_ms) / len(blend_ms)
+    blend_avg = iso["blend"] if iso else sum(blend_ms) / len(blend_ms)
     peaks, peak_kind = measured_peaks()
     traffic = profile_traffic()
     # K7 algorithmic work: F_alpha = f_blend + f_cull + pixels_terminated fragments, 16 flops each
@@ -408,9 +427,12 @@ def run_tcgs(args):
                          f"project + build_tiles, blend on {det['band_rows']}/{det['tile_rows']} tile rows "
                          f"extrapolated to the frame",
                "detail": det}
-    stage = {"preprocess": sum(pre_ms) / len(pre_ms), "binning": sum(bin_ms) / len(bin_ms), "blend": blend_avg}
+    stage = {"preprocess": sum(pre_ms) / len(pre_ms), "binning": sum(bin_ms) / len(bin_ms),
+             "blend": sum(blend_ms) / len(blend_ms)}
     if gather_ms:
         stage["gather"] = sum(gather_ms) / len(gather_ms)
+    if iso:
+        stage = {"isolated": iso, "in_flight": stage}
     line = {
         "metric": METRIC,
         "value": value,
@@ -432,7 +454,8 @@ def run_tcgs(args):
                        sum(np.asarray(scene[k]).nbytes for k in ("means", "scales", "rotations", "opacities",
                                                                   "features" if scene["sh_degree"] > 0 else "colors"))
                        / 1e6),
-                   "backend": args.backend},
+                   "backend": args.backend,
+                   "views_in_flight": 1 if bands_mode else max(1, args.streams)},
         "alpha_blend_ms": blend_avg,
         "alpha_blend_ms_max_over_ranks": blend_max,
         "stage_ms": stage,

@@ -20,6 +20,7 @@ from .raster import (  # noqa: F401
     GaussianCloud,
     ImageBuffer,
     Renderer,
+    ViewRenderer,
     computation_model,
     make_backend,
     rasterize,
@@ -45,6 +46,7 @@ __all__ = [
     "GaussianCloud",
     "ImageBuffer",
     "Renderer",
+    "ViewRenderer",
     "computation_model",
     "make_backend",
     "rasterize",

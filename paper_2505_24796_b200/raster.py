@@ -424,6 +424,49 @@ class Renderer:
         return Frame(rgb, T, cnt, fs)
 
 
+class ViewRenderer:
+    """Renders many independent views of one scene with ``n_streams`` workspaces on as many CUDA streams.
+
+    Frame i runs on stream i % n_streams, so the latency-bound stages of one view (K1, the sort passes)
+    overlap the tail of the previous view's K7 instead of leaving SMs idle between frames.  Views are
+    independent (the reference renders each camera separately, src/tilesplat/raster.py:161), so this
+    changes no result.  ``join()`` makes the caller's current stream wait for every view.
+    """
+
+    def __init__(self, device=None, backend="tcgs", n_streams: int = 2):
+        self.device = torch.device(device or "cuda")
+        self.renderers = [Renderer(self.device, backend) for _ in range(n_streams)]
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(n_streams)]
+        self.outputs = [None] * n_streams
+        self.k = 0
+
+    @property
+    def lib(self):
+        return self.renderers[0].lib
+
+    def warm(self, cloud: GaussianCloud, cam) -> FragmentStats:
+        """Size every workspace (one synchronous frame each); returns the stats of ``cam``."""
+        st = None
+        for r, s in zip(self.renderers, self.streams):
+            with torch.cuda.stream(s):
+                st = r.render_frame(cloud, cam, timed=False).stats
+        return st
+
+    def launch(self, cloud: GaussianCloud, cam, timers=None):
+        """Enqueue one view on the next stream (ordered after the caller's current stream)."""
+        i = self.k % len(self.streams)
+        self.k += 1
+        s = self.streams[i]
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            return self.renderers[i].launch(cloud, cam, timers=timers)
+
+    def join(self):
+        cur = torch.cuda.current_stream(self.device)
+        for s in self.streams:
+            cur.wait_stream(s)
+
+
 _DEFAULT = {}
 
 

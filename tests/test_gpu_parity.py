@@ -412,6 +412,25 @@ def test_ply_checkpoint_renders_like_arrays(renderers, tmp_path):
     assert float(np.max(np.abs(f.rgb.double().cpu().numpy() - ref.rgb))) <= RGB_TOL
 
 
+def test_view_renderer_streams_match_sequential(renderers):
+    """Views rendered concurrently on several streams/workspaces equal one-at-a-time frames."""
+    scene, cams = synthetic.config_scene("c4", 0.02)
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    views = [cams[i] for i in range(0, 256, 32)]
+    r = tcgs.Renderer("cuda", "tcgs")
+    ref = [r.render_frame(cloud, c, timed=False).rgb.clone() for c in views]
+    vr = tcgs.ViewRenderer("cuda", "tcgs", n_streams=3)
+    vr.warm(cloud, views[0])
+    outs = []
+    for c in views:
+        rgb, T, cnt = vr.launch(cloud, c)
+        vr.join()  # the renderer's output buffers are reused every n_streams views
+        outs.append(rgb.clone())
+    torch.cuda.synchronize()
+    for a, b in zip(outs, ref):
+        assert torch.equal(a, b)
+
+
 # ---- full-size parity (BASELINE config shapes) against the oracle ---------------------------------
 
 @pytest.mark.slow

@@ -187,6 +187,20 @@ def cpu_reference_frame(scene, cam, rows):
                      "band_rows": r1 - r0, "tile_rows": tiles_y}
 
 
+def bench_config(args, scene, cam, world):
+    """The workload description both arms print (the driver compares them)."""
+    from paper_2505_24796_b200 import synthetic
+
+    bands = args.config == "c3"
+    feats = "features" if scene.get("sh_degree", 0) > 0 else "colors"
+    mb = sum(np.asarray(scene[k]).nbytes for k in ("means", "scales", "rotations", "opacities", feats)) / 1e6
+    return {"workload": f"{args.config}: " + synthetic.CONFIGS[args.config],
+            "P": int(np.asarray(scene["means"]).shape[0]), "sh_degree": int(scene.get("sh_degree", 0)),
+            "width": int(cam.width), "height": int(cam.height),
+            "parallelism": (f"tile bands x{world}" if bands else (f"views x{world}" if world > 1 else "single view")),
+            "l2": "no flush: per-frame inputs (%.0f MB) exceed the 126 MB L2" % mb}
+
+
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -216,9 +230,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: " + synthetic.CONFIGS[args.config], "P": int(scene["means"].shape[0]),
-                   "width": cam.width, "height": cam.height},
+        "scaling": "strong" if args.config == "c3" else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": bench_config(args, scene, cam, world),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
                          "kind": "port",
                          "sample": f"oracle C port (float64 restatement of tilesplat.render 'reference'): full "
@@ -446,16 +459,9 @@ def run_tcgs(args):
         "vs_baseline": None,
         "dtype": "f64 preprocess / fp16-hi-lo tcgen05 alpha, fp32 blend",
         "data": "synthetic (SURVEY.md Appendix B generators; random scene, no dataset)",
-        "config": {"workload": f"{args.config}: " + synthetic.CONFIGS[args.config],
-                   "P": cloud.P, "sh_degree": scene["sh_degree"], "width": base.width, "height": base.height,
-                   "parallelism": (f"tile bands x{world}" if bands_mode else
-                                   (f"views x{world}" if world > 1 else "single view")),
-                   "l2": "no flush: per-frame inputs (%.0f MB) exceed the 126 MB L2" % (
-                       sum(np.asarray(scene[k]).nbytes for k in ("means", "scales", "rotations", "opacities",
-                                                                  "features" if scene["sh_degree"] > 0 else "colors"))
-                       / 1e6),
-                   "backend": args.backend,
-                   "views_in_flight": 1 if bands_mode else max(1, args.streams)},
+        "config": bench_config(args, scene, base, world),
+        "backend": args.backend,
+        "views_in_flight": 1 if bands_mode else max(1, args.streams),
         "alpha_blend_ms": blend_avg,
         "alpha_blend_ms_max_over_ranks": blend_max,
         "stage_ms": stage,

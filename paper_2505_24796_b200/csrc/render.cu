@@ -209,14 +209,6 @@ __device__ __forceinline__ bool gaussian_coeffs(const Rec &r, double ox, double 
 template <int MODE>
 __host__ __device__ constexpr bool fold_cut() { return MODE != TCGS_ALPHA_TC_K8; }
 
-// acc + (x >> 31) * m as two FMA-pipe integer multiply-adds
-__device__ __forceinline__ uint32_t umad_hi2(uint32_t x, uint32_t m, uint32_t acc) {
-    uint32_t s, r;
-    asm("mul.hi.u32 %0, %1, 2;" : "=r"(s) : "r"(x));
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(s), "r"(m), "r"(acc));
-    return r;
-}
-
 __device__ __forceinline__ __half h16(float x) { return __float2half_rn(x); }
 __device__ __forceinline__ float f32(__half x) { return __half2float(x); }
 
@@ -579,10 +571,10 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                     }
                     uint32_t pass;
                     if (fold_cut<MODE>()) {
-                        // sign bits -> fail mask with multiply-adds (FMA pipe; the ALU pipe is the busy one)
+                        // sign bits -> fail mask: one funnel shift per column, (fail << 1) | (beta'' >> 31)
                         uint32_t fail = 0;
 #pragma unroll
-                        for (int j = 0; j < 16; j++) fail = umad_hi2(r[j], 1u << j, fail);
+                        for (int j = 15; j >= 0; j--) fail = __funnelshift_l(r[j], fail, 1);
                         pass = ~fail;
                     } else {
                         pass = 0;

@@ -147,18 +147,34 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def issue_roofline(traffic, blend_ms, clocks):
+    """K7's binding resource: warp-instruction issue (4 per clock per SM).  Instructions per launch come from
+    the committed ncu capture (smsp__inst_executed.sum), the duration from this run's CUDA events."""
+    inst = (traffic or {}).get("warp_inst_per_launch")
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    if not inst:
+        return None
+    peak = 4 * 148 * mhz * 1e6
+    ach = inst / (blend_ms * 1e-3)
+    return {"achieved_warp_inst_per_s": ach, "peak_warp_inst_per_s": peak, "frac": ach / peak,
+            "warp_inst_per_launch": inst, "note": "instructions from the committed ncu profile; clock = median "
+                                                  "SM clock sampled during the timed region"}
+
+
 def profile_traffic():
     """K7 DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the newest committed
     ncu --set full summary under profiles/ (scripts/ncu_summary.py), if present."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_k7_ncu.json")), key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_k7_ncu.json")))  # r1_ < r1e_ < r1j_ < ...
     for p in reversed(files):
         with open(p) as f:
             rows = [e for e in json.load(f) if "render_kernel" in e.get("kernel", "")]
         if rows:
             mb = [e["dram_read_MB"] + e["dram_write_MB"] for e in rows]
-            return {"bytes_per_launch": 1e6 * sum(mb) / len(mb), "source": os.path.relpath(p, ROOT)}
+            inst = [e.get("inst_executed") for e in rows if isinstance(e.get("inst_executed"), float)]
+            return {"bytes_per_launch": 1e6 * sum(mb) / len(mb), "source": os.path.relpath(p, ROOT),
+                    "warp_inst_per_launch": sum(inst) / len(inst) if inst else None}
     return None
 
 
@@ -472,7 +488,8 @@ def run_tcgs(args):
                      "traffic_source": (traffic or {}).get("source"), "peak_kind": peak_kind,
                      "work": "16 flops x F_alpha (F_alpha = f_blend + f_cull + pixels_terminated)",
                      "mufu": {"achieved_ex2_per_s": ex2_rate, "peak_ex2_per_s": ex2_peak,
-                              "frac": ex2_rate / ex2_peak, "peak_kind": "nominal 16/clk/SM"}},
+                              "frac": ex2_rate / ex2_peak, "peak_kind": "nominal 16/clk/SM"},
+                     "issue": issue_roofline(traffic, blend_avg, clocks)},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),

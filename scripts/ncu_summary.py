@@ -73,13 +73,15 @@ def summarise(rep: str):
                 v = num(d[i])
                 if isinstance(v, float):
                     stalls[h[len(STALL_PREFIX):-len("_per_issue_active.ratio")]] = v
+        if isinstance(e.get("time_us"), float) and isinstance(e.get("dram_read_MB"), float):
+            e["dram_GBps"] = (e["dram_read_MB"] + e["dram_write_MB"]) * 1e3 / e["time_us"]
         e["top_stalls"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:5])
         res.append(e)
     return res
 
 
 def markdown(res) -> str:
-    cols = ["time_us", "dram_read_MB", "dram_write_MB", "dram_pct", "l2_pct", "sm_pct", "issue_active_pct",
+    cols = ["time_us", "dram_read_MB", "dram_write_MB", "dram_GBps", "dram_pct", "l2_pct", "sm_pct", "issue_active_pct",
             "tensor_pipe_pct", "xu_pipe_pct", "fma_pipe_pct", "fp64_pipe_pct", "warps_active_pct", "regs"]
     lines = ["| kernel | " + " | ".join(cols) + " | top stalls |", "|" + "---|" * (len(cols) + 2)]
     for e in res:

@@ -32,6 +32,8 @@
 //     terminated stops working; when all 8 have, the producer retires the tile.
 // Stages (4) and TMEM buffers (2) are ring buffers guarded by full/empty and
 // mma_done/tmem_empty mbarriers, so gathers, MMAs and blending overlap.
+#include <type_traits>
+
 #include "tcgs_internal.cuh"
 
 namespace tcgs {
@@ -45,6 +47,13 @@ constexpr float TERM_T = 0.0001f;                // src/tilesplat/raster.py:16
 constexpr float INV255 = 1.0f / 255.0f;          // 2^(-log2 255)
 constexpr int K7_SMEM_BYTES = 72 * 1024;         // also caps residency at 3 CTAs/SM (TMEM: 3 x 128 columns)
 constexpr int S = K7_STAGES;
+// column masks of one stage
+using mask_t = std::conditional<(K7_BATCH > 32), unsigned long long, uint32_t>::type;
+constexpr mask_t ALL_COLS = K7_BATCH >= 64 ? ~(mask_t)0 : (mask_t)(((unsigned long long)1 << K7_BATCH) - 1);
+__device__ __forceinline__ uint32_t popc_cols(mask_t m) {
+    if constexpr (K7_BATCH > 32) return (uint32_t)__popcll(m);
+    else return (uint32_t)__popc((uint32_t)m);
+}
 constexpr int NB = K7_TMEM_BUFS;
 
 struct RenderArgs {
@@ -542,25 +551,32 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 mbar_wait(&sm.mma_done[b], (k / NB) & 1);
                 tc_fence_after();
             }
+            bool tmem_released = false;
             if (!warp_done) {
                 const int nl = m.n_live;
-                const uint32_t act0 = done ? 0u : (nl >= 32 ? FULL : ((1u << nl) - 1u));
-                uint32_t act = act0;
+                const mask_t act0 = done ? (mask_t)0 : (nl >= K7_BATCH ? ALL_COLS : (((mask_t)1 << nl) - 1));
+                mask_t act = act0;
                 const uint32_t tb = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (2 * K7_BATCH) + half * K7_BATCH;
-                int jt = 32;
+                int jt = K7_BATCH;
                 // pass threshold of beta: the EarlyCull cut while the pixel is live, +inf once it has
                 // terminated (a float, so the test stays one FSETP and the update a predicated move)
                 const float cut0 = fold_cut<MODE>() ? 0.0f : CUT_LOG2;
                 float thr = done ? __int_as_float(0x7f800000) : cut0;
                 const float fcnt0 = fcnt;
 #pragma unroll
-                for (int hc = 0; hc < 2; hc++) {  // two 16-column halves keep 16 betas live in registers
+                for (int hc = 0; hc < K7_BATCH / 16; hc++) {  // 16-column groups keep 16 betas live in registers
                     uint32_t r[16];
                     if (TC) {
                         tmem_ld16(tb + 16 * hc, r);
                         tmem_wait_ld();
 #pragma unroll
                         for (int j = 0; j < 16; j++) asm volatile("" : "+r"(r[j]));
+                        if (NB == 1 && hc == K7_BATCH / 16 - 1) {  // single accumulator: free it for the next MMA
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&sm.tmem_empty[b]);
+                            tmem_released = true;
+                        }
                     } else {
 #pragma unroll
                         for (int j = 0; j < 16; j++) {
@@ -582,7 +598,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                         for (int j = 0; j < 16; j++)
                             if (__uint_as_float(r[j]) >= CUT_LOG2) pass |= 1u << j;
                     }
-                    pass &= (act >> (16 * hc)) & 0xffffu;
+                    pass &= (uint32_t)(act >> (16 * hc)) & 0xffffu;
                     const uint32_t wm = __reduce_or_sync(FULL, pass);
 #pragma unroll
                     for (int j = 0; j < 16; j++) {
@@ -608,25 +624,26 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                             }
                         }
                     }
-                    if (jt < 32) act = 0u;  // terminated in this half: nothing later is live
+                    if (jt < K7_BATCH) act = 0;  // terminated in this group: nothing later is live
                 }
-                term = term || jt < 32;
-                done = done || jt < 32;
+                const bool tstage = jt < K7_BATCH;
+                term = term || tstage;
+                done = done || tstage;
                 // EarlyCull counts: valid columns before the termination that did not blend, plus the dead
                 // Gaussians of the list before the terminating one
-                const uint32_t before = jt >= 32 ? FULL : ((1u << jt) - 1u);
-                cull += __popc(act0 & before) - (uint32_t)(fcnt - fcnt0);
-                if (jt < 32) cull += sm.dead_before[st][jt];
+                const mask_t before = tstage ? (((mask_t)1 << jt) - 1) : ALL_COLS;
+                cull += popc_cols(act0 & before) - (uint32_t)(fcnt - fcnt0);
+                if (tstage) cull += sm.dead_before[st][jt];
                 if (__all_sync(FULL, done)) {
                     warp_done = true;
                     if (lane == 0) atomicAdd(&sm.retire[cur_seq & 7], 1);
                 }
             }
             if (m.last && !done) cull += m.dead_total;  // list exhausted: every dead Gaussian was a cull
-            if (TC) tc_fence_before();
+            if (TC && !tmem_released) tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if (TC) mbar_arrive(&sm.tmem_empty[b]);
+                if (TC && !tmem_released) mbar_arrive(&sm.tmem_empty[b]);
                 mbar_arrive(&sm.empty[st]);
             }
         }

@@ -24,12 +24,18 @@ constexpr int DUP_THREADS = 256;
 constexpr int K7_CONSUMER_WARPS = 8;  // one pixel per thread, 16x16 tile
 constexpr int K7_PRODUCERS = 2;       // producer warps (alternate 32-entry chunks, token-ordered compaction)
 constexpr int K7_THREADS = 32 * (K7_CONSUMER_WARPS + K7_PRODUCERS);
-constexpr int K7_BATCH = 32;          // live Gaussians per tcgen05 batch (MMA N)
+#ifndef TCGS_K7_BATCH
+#define TCGS_K7_BATCH 32
+#endif
+#ifndef TCGS_K7_TMEM_BUFS
+#define TCGS_K7_TMEM_BUFS 2
+#endif
+constexpr int K7_BATCH = TCGS_K7_BATCH;  // live Gaussians per tcgen05 batch (MMA N): 32 or 64
 #ifndef TCGS_K7_STAGES
 #define TCGS_K7_STAGES 4
 #endif
 constexpr int K7_STAGES = TCGS_K7_STAGES;  // shared-memory B-operand stages
-constexpr int K7_TMEM_BUFS = 2;       // TMEM accumulator buffers
+constexpr int K7_TMEM_BUFS = TCGS_K7_TMEM_BUFS;  // TMEM accumulator buffers (1: released after the last load)
 constexpr int K7_TMEM_COLS = K7_TMEM_BUFS * 2 * K7_BATCH;  // buffers x pixel halves x N
 constexpr int K7_CTAS_PER_SM = 3;
 

@@ -45,7 +45,8 @@ constexpr float CUT_LOG2 = -7.994353436858858f;  // -log2(255): beta' < CUT cull
 constexpr float LN255 = 5.541263545158426f;
 constexpr float TERM_T = 0.0001f;                // src/tilesplat/raster.py:16
 constexpr float INV255 = 1.0f / 255.0f;          // 2^(-log2 255)
-constexpr int K7_SMEM_BYTES = 72 * 1024;         // also caps residency at 3 CTAs/SM (TMEM: 3 x 128 columns)
+// also caps residency at K7_CTAS_PER_SM CTAs/SM (TMEM: K7_CTAS_PER_SM x K7_TMEM_COLS <= 512 columns)
+constexpr int K7_SMEM_BYTES = (K7_CTAS_PER_SM >= 4 ? 54 : 72) * 1024;
 constexpr int S = K7_STAGES;
 // column masks of one stage
 using mask_t = std::conditional<(K7_BATCH > 32), unsigned long long, uint32_t>::type;

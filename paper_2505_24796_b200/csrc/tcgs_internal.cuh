@@ -37,7 +37,10 @@ constexpr int K7_BATCH = TCGS_K7_BATCH;  // live Gaussians per tcgen05 batch (MM
 constexpr int K7_STAGES = TCGS_K7_STAGES;  // shared-memory B-operand stages
 constexpr int K7_TMEM_BUFS = TCGS_K7_TMEM_BUFS;  // TMEM accumulator buffers (1: released after the last load)
 constexpr int K7_TMEM_COLS = K7_TMEM_BUFS * 2 * K7_BATCH;  // buffers x pixel halves x N
-constexpr int K7_CTAS_PER_SM = 3;
+#ifndef TCGS_K7_CTAS
+#define TCGS_K7_CTAS 3
+#endif
+constexpr int K7_CTAS_PER_SM = TCGS_K7_CTAS;
 
 // Per-Gaussian record consumed by the blend kernel (48 B, three 16 B loads).
 struct __align__(16) Rec {

@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--streams", type=int, default=3, help="views in flight (one workspace + CUDA stream each)")
+    ap.add_argument("--band-output", default="peer", choices=["peer", "gather"],
+                    help="c3 tile bands: K7 writes into rank 0's frame over peer memory, or one NCCL gather")
     return ap.parse_args()
 
 
@@ -291,7 +293,7 @@ def run_tcgs(args):
         if world == 1 and not dist.is_initialized():
             dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % (29500 + os.getpid() % 1000),
                                     rank=0, world_size=1)
-        br = shard.BandRenderer(dev, args.backend)
+        br = shard.BandRenderer(dev, args.backend, output=args.band_output if world > 1 else "gather")
         r = br.r
         first = br.render(cloud, base, with_stats=True)  # sizes the workspace
         st0 = first.stats
@@ -428,6 +430,8 @@ def run_tcgs(args):
                "path": ("pinned host scene -> H2D -> tcgs render -> D2H RGB + FragmentStats, every step"
                         + ("" if bands_mode else "; FramePipeline overlaps H2D(k+1) / render(k) / D2H(k-1)"))}
 
+    if bands_mode:
+        br.close()  # unmaps / frees the peer frame (collective)
     if rank != 0:
         if dist.is_initialized():
             dist.destroy_process_group()
@@ -478,18 +482,20 @@ def run_tcgs(args):
         "config": bench_config(args, scene, base, world),
         "backend": args.backend,
         "views_in_flight": 1 if bands_mode else max(1, args.streams),
+        "band_output": (args.band_output if world > 1 else "local") if bands_mode else None,
         "alpha_blend_ms": blend_avg,
         "alpha_blend_ms_max_over_ranks": blend_max,
         "stage_ms": stage,
         "frame_stats": {**st_last.to_dict(), "n_visible": st_last.n_visible},
         "roofline": {"kernel": "K7 render_kernel (alpha + blend)", "bound": "tensor", "achieved": tc_tflops,
                      "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": tc_tflops / peaks["bf16_tflops"],
-                     "traffic": (traffic or {}).get("bytes_per_launch"),
+                     "traffic": (traffic or {}).get("bytes_per_launch") if args.config == "c2" else None,
                      "traffic_source": (traffic or {}).get("source"), "peak_kind": peak_kind,
                      "work": "16 flops x F_alpha (F_alpha = f_blend + f_cull + pixels_terminated)",
                      "mufu": {"achieved_ex2_per_s": ex2_rate, "peak_ex2_per_s": ex2_peak,
                               "frac": ex2_rate / ex2_peak, "peak_kind": "nominal 16/clk/SM"},
-                     "issue": issue_roofline(traffic, blend_avg, clocks)},
+                     # the committed K7 profile is of the C2 workload: its instruction count only applies there
+                     "issue": issue_roofline(traffic, blend_avg, clocks) if args.config == "c2" else None},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),

@@ -127,6 +127,17 @@ size_t tcgs_counters_bytes(void);
 int tcgs_snapshot_stats(const void *ws, void *dst, void *stream);
 int tcgs_decode_stats(const void *snapshot, const tcgs_opts *opts, tcgs_stats *stats);
 
+/* Tile-band frames written straight into rank 0's frame over NVLink peer memory (multi-GPU; replaces
+ * the band gather).  Rank 0 allocates the frame with tcgs_frame_alloc and exports it with
+ * tcgs_ipc_get_handle; every other rank maps it with tcgs_ipc_open and passes the mapped pointers as the
+ * rgb / T / n_contrib outputs of tcgs_blend, so K7 stores its band's pixels directly into rank 0's HBM. */
+#define TCGS_IPC_HANDLE_BYTES 64
+int tcgs_frame_alloc(size_t bytes, void **ptr);
+int tcgs_frame_free(void *ptr);
+int tcgs_ipc_get_handle(void *ptr, void *handle /* TCGS_IPC_HANDLE_BYTES */);
+int tcgs_ipc_open(const void *handle, void **ptr);
+int tcgs_ipc_close(void *ptr);
+
 /* Debug/KAT entry: blend caller-given projected records through K7.
  *   mean2d [P,2] f64, conic [P,3] f64 (s11,s12,s22), opacity [P] f64, rgb [P,3] f32 (device);
  *   tile lists as CSR: offsets [n_tiles+1] i64, ids [N] i32 (device), row-major tiles. */

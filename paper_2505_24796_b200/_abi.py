@@ -21,6 +21,8 @@ ALPHA_TC_HILO = 0
 ALPHA_TC_K8 = 1
 ALPHA_FFMA = 2
 
+IPC_HANDLE_BYTES = 64
+
 F32 = 0
 F64 = 1
 
@@ -65,6 +67,11 @@ SIGNATURES = {
     "tcgs_counters_bytes": (ctypes.c_size_t, []),
     "tcgs_snapshot_stats": (ctypes.c_int, [_P, _P, _P]),
     "tcgs_decode_stats": (ctypes.c_int, [_P, ctypes.POINTER(Opts), ctypes.POINTER(Stats)]),
+    "tcgs_frame_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "tcgs_frame_free": (ctypes.c_int, [_P]),
+    "tcgs_ipc_get_handle": (ctypes.c_int, [_P, _P]),
+    "tcgs_ipc_open": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_void_p)]),
+    "tcgs_ipc_close": (ctypes.c_int, [_P]),
     "tcgs_blend_lists": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P, ctypes.POINTER(Camera), ctypes.POINTER(Opts),
                                         _P, ctypes.c_size_t, _P, _P, _P, _P]),
     "tcgs_copy_lists": (ctypes.c_int, [_P, _I64, ctypes.POINTER(Camera), ctypes.POINTER(Opts), _I64, _P, _P, _P]),

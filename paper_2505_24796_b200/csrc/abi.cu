@@ -175,6 +175,42 @@ int tcgs_read_stats(const void *ws, int64_t P, const tcgs_opts *opts, tcgs_stats
 
 size_t tcgs_counters_bytes(void) { return sizeof(DevCounters); }
 
+int tcgs_frame_alloc(size_t bytes, void **ptr) {
+    if (!ptr || bytes == 0) return fail(TCGS_ERR_INVALID_ARG, "null pointer or zero size");
+    cudaError_t e = cudaMalloc(ptr, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "frame_alloc");
+    return TCGS_OK;
+}
+
+int tcgs_frame_free(void *ptr) {
+    cudaError_t e = cudaFree(ptr);
+    if (e != cudaSuccess) return cuda_fail(e, "frame_free");
+    return TCGS_OK;
+}
+
+int tcgs_ipc_get_handle(void *ptr, void *handle) {
+    if (!ptr || !handle) return fail(TCGS_ERR_INVALID_ARG, "null pointer");
+    static_assert(sizeof(cudaIpcMemHandle_t) == TCGS_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaError_t e = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t *>(handle), ptr);
+    if (e != cudaSuccess) return cuda_fail(e, "ipc_get_handle");
+    return TCGS_OK;
+}
+
+int tcgs_ipc_open(const void *handle, void **ptr) {
+    if (!ptr || !handle) return fail(TCGS_ERR_INVALID_ARG, "null pointer");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "ipc_open");
+    return TCGS_OK;
+}
+
+int tcgs_ipc_close(void *ptr) {
+    cudaError_t e = cudaIpcCloseMemHandle(ptr);
+    if (e != cudaSuccess) return cuda_fail(e, "ipc_close");
+    return TCGS_OK;
+}
+
 int tcgs_snapshot_stats(const void *ws, void *dst, void *stream) {
     if (!ws || !dst) return fail(TCGS_ERR_INVALID_ARG, "null workspace or destination");
     cudaError_t e = cudaMemcpyAsync(dst, ws, sizeof(DevCounters), cudaMemcpyDefault, (cudaStream_t)stream);

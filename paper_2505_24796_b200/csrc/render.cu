@@ -650,6 +650,10 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
         }
     }
 
+    // the outputs may be another GPU's frame mapped over NVLink (tile-band peer output): make this thread's
+    // pixel stores visible system-wide before the CTA retires
+    if (warp < K7_CONSUMER_WARPS) __threadfence_system();
+
     // K8: fragment statistics, one atomic per CTA and counter
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {

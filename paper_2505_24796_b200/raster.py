@@ -323,11 +323,11 @@ class Renderer:
                            n_visible=st_.n_visible)
         return rc, fs
 
-    def finish(self, cloud: GaussianCloud, cam, band=None, with_stats=True) -> Frame:
+    def finish(self, cloud: GaussianCloud, cam, band=None, with_stats=True, outputs=None) -> Frame:
         """K2-K7 for ``band`` after ``preprocess`` + the frame's stats (re-running K1 if the splat
         capacity had to grow)."""
         for _attempt in range(3):
-            rgb, T, cnt = self.bin_blend(cloud, cam, band)
+            rgb, T, cnt = self.bin_blend(cloud, cam, band, outputs=outputs)
             rc, fs = self.read_stats(cloud.P, band)
             if rc == _abi.TCGS_ERR_CAPACITY:
                 self.max_splats = int(fs.n_splats * 1.25) + 1024

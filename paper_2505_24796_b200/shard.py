@@ -25,6 +25,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import ctypes
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -150,20 +152,104 @@ class BandFrame:
     stats: FragmentStats | None  # whole-frame stats (all ranks)
 
 
+class _CudaArray:
+    """``__cuda_array_interface__`` view of raw device memory (wrapped by torch.as_tensor, not owned)."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+class PeerFrame:
+    """Rank 0's full-frame outputs (rgb [H,W,3] f32, T [H,W] f32, n_contrib [H,W] i32) in one allocation,
+    mapped into every rank of ``group`` with CUDA IPC (NVLink peer memory between GPUs of one box).
+
+    Every rank passes these tensors as K7's outputs: K7 stores the pixels of its tile-row band straight
+    into rank 0's frame, tile by tile, so the band gather disappears.
+    """
+
+    def __init__(self, lib, W: int, H: int, device, group=None):
+        self.lib, self.group = lib, group
+        self.rank = dist.get_rank(group)
+        n = W * H
+        self.nbytes = 20 * n  # 12 n (rgb) + 4 n (T) + 4 n (n_contrib)
+        handle = None
+        with torch.cuda.device(device):
+            if self.rank == 0:
+                p = ctypes.c_void_p()
+                _abi.check(lib.tcgs_frame_alloc(self.nbytes, ctypes.byref(p)), "tcgs_frame_alloc")
+                self.ptr = p.value
+                h = ctypes.create_string_buffer(_abi.IPC_HANDLE_BYTES)
+                _abi.check(lib.tcgs_ipc_get_handle(ctypes.c_void_p(self.ptr), h), "tcgs_ipc_get_handle")
+                handle = h.raw
+            box = [handle]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            if self.rank != 0:
+                p = ctypes.c_void_p()
+                _abi.check(lib.tcgs_ipc_open(ctypes.create_string_buffer(box[0], _abi.IPC_HANDLE_BYTES),
+                                             ctypes.byref(p)), "tcgs_ipc_open")
+                self.ptr = p.value
+            dev = torch.device(device)
+            self.rgb = torch.as_tensor(_CudaArray(self.ptr, (H, W, 3), "<f4"), device=dev)
+            self.T = torch.as_tensor(_CudaArray(self.ptr + 12 * n, (H, W), "<f4"), device=dev)
+            self.n_contrib = torch.as_tensor(_CudaArray(self.ptr + 16 * n, (H, W), "<i4"), device=dev)
+            if self.rank == 0:
+                self.rgb.zero_()
+                self.T.fill_(1.0)
+                self.n_contrib.zero_()
+                torch.cuda.synchronize(dev)
+        dist.barrier(group)
+
+    def close(self):
+        dist.barrier(self.group)
+        if self.rank == 0:
+            self.lib.tcgs_frame_free(ctypes.c_void_p(self.ptr))
+        else:
+            self.lib.tcgs_ipc_close(ctypes.c_void_p(self.ptr))
+
+
 class BandRenderer:
     """Renders one frame split into tile-row bands across the ranks of ``group``.
 
-    Per frame: K1 (replicated) -> tile-row counts (one 8*tiles_y-byte D2H) ->
-    local partition -> K2-K6 + K7 on the band -> one NCCL gather to rank 0.
+    Per frame: K1 (replicated) -> tile-row counts (one 8*tiles_y-byte D2H) -> local partition ->
+    K2-K6 + K7 on the band -> the frame on rank 0, either by one NCCL gather (``output="gather"``)
+    or written there directly by every rank's K7 through CUDA IPC peer mappings (``output="peer"``,
+    completion signalled by one tiny all-reduce / barrier).
     """
 
-    def __init__(self, device, backend="tcgs", group=None, gather_extras: bool = True):
+    def __init__(self, device, backend="tcgs", group=None, gather_extras: bool = True, output: str = "gather"):
+        if output not in ("gather", "peer"):
+            raise ValueError("output must be 'gather' or 'peer'")
         self.r = Renderer(device, backend)
         self.device = self.r.device
         self.group = group
         self.gather_extras = gather_extras
+        self.output = output
         self._full = {}
+        self._peer = {}
         self._rows = None
+        self._flag = None
+
+    def peer_frame(self, W: int, H: int) -> PeerFrame:
+        if (W, H) not in self._peer:
+            self._peer[(W, H)] = PeerFrame(self.r.lib, W, H, self.device, self.group)
+        return self._peer[(W, H)]
+
+    def close(self):
+        for pf in self._peer.values():
+            pf.close()
+        self._peer = {}
+
+    def _complete(self):
+        """Rank 0 may use the frame once every rank's K7 has finished writing into it."""
+        if dist.get_backend(self.group) == "nccl":
+            if self._flag is None:
+                self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+            dist.all_reduce(self._flag, group=self.group)  # ordered after K7 on every rank's stream
+        else:
+            torch.cuda.synchronize(self.device)
+            dist.barrier(self.group)
 
     def partition(self, cloud: GaussianCloud, cam) -> list[tuple[int, int]]:
         c = camera_struct(cam)
@@ -196,15 +282,24 @@ class BandRenderer:
                 ev[1].record()
             bands = self.partition(cloud, cam)
             band = bands[rank]
+            c = camera_struct(cam)
+            outs = None
+            if self.output == "peer":
+                pf = self.peer_frame(c.width, c.height)
+                outs = (pf.rgb, pf.T, pf.n_contrib)
             if with_stats:
-                frame = self.r.finish(cloud, cam, band, with_stats=True)
+                frame = self.r.finish(cloud, cam, band, with_stats=True, outputs=outs)
             else:
-                rgb, T, cnt = self.r.bin_blend(cloud, cam, band, timers=ev)
+                rgb, T, cnt = self.r.bin_blend(cloud, cam, band, outputs=outs, timers=ev)
                 frame = Frame(rgb, T, cnt, None)
             H, W = frame.rgb.shape[0], frame.rgb.shape[1]
             parts = [frame.rgb, frame.T, frame.n_contrib] if self.gather_extras else [frame.rgb]
-            full = list(self.full_buffers(W, H))[:len(parts)] if rank == 0 else None
-            gather_bands(parts, full, bands, H, self.group)
+            if self.output == "peer":
+                self._complete()
+                full = parts if rank == 0 else None
+            else:
+                full = list(self.full_buffers(W, H))[:len(parts)] if rank == 0 else None
+                gather_bands(parts, full, bands, H, self.group)
             if ev:
                 ev[4].record()
             stats = reduce_stats(frame.stats, self.device, self.group) if with_stats else None

@@ -104,6 +104,8 @@ _SPECS = {
     "reference": (_abi.ALPHA_FFMA, False),
     "frag2mat": (_abi.ALPHA_TC_HILO, True),
     "frag2mat-fp16": (_abi.ALPHA_TC_K8, True),
+    # tf32 inputs (11-bit mantissa) are served by the hi/lo fp16 split (~22 bits): never less accurate
+    "frag2mat-tf32": (_abi.ALPHA_TC_HILO, True),
 }
 
 
@@ -498,20 +500,55 @@ def render(scene, cam, backend="tcgs", device=None) -> tuple[ImageBuffer, Fragme
 
 
 def rasterize(means, scales, rotations, opacities, features, sh_degree: int, cameras, backend="tcgs",
-              band=None, renderer: Renderer | None = None) -> dict:
+              band=None, renderer: Renderer | None = None, n_streams: int = 3) -> dict:
     """Batched entry: render every camera of ``cameras`` from device tensors.
 
-    Returns ``rgb [V,H,W,3] f32``, ``T [V,H,W] f32``, ``n_contrib [V,H,W] i32``
-    (device tensors) and per-view FragmentStats.
+    Views are independent, so they run ``n_streams`` at a time on their own workspaces and CUDA
+    streams (``ViewRenderer``); every view's outputs are copied out on its own stream and its
+    FragmentStats snapshotted without a host sync.  Returns ``rgb [V,H,W,3] f32``, ``T [V,H,W] f32``,
+    ``n_contrib [V,H,W] i32`` (device tensors) and per-view FragmentStats.
     """
+    import ctypes
+
     cloud = GaussianCloud(means.contiguous(), scales.contiguous(), rotations.contiguous(),
                           opacities.reshape(-1).contiguous(), features.contiguous(), int(sh_degree))
-    r = renderer or Renderer(means.device, backend)
-    out_rgb, out_T, out_n, stats = [], [], [], []
-    for cam in cameras:
-        f = r.render_frame(cloud, cam, band=band)
-        out_rgb.append(f.rgb.clone())
-        out_T.append(f.T.clone())
-        out_n.append(f.n_contrib.clone())
-        stats.append(f.stats)
-    return {"rgb": torch.stack(out_rgb), "T": torch.stack(out_T), "n_contrib": torch.stack(out_n), "stats": stats}
+    cams = list(cameras)
+    if not cams:
+        raise ValueError("no cameras")
+    if renderer is not None or band is not None or n_streams <= 1:
+        r = renderer or Renderer(means.device, backend)
+        frames = [r.render_frame(cloud, cam, band=band) for cam in cams[:1]]
+        out = [(frames[0].rgb.clone(), frames[0].T.clone(), frames[0].n_contrib.clone(), frames[0].stats)]
+        for cam in cams[1:]:
+            f = r.render_frame(cloud, cam, band=band)
+            out.append((f.rgb.clone(), f.T.clone(), f.n_contrib.clone(), f.stats))
+    else:
+        vr = ViewRenderer(means.device, backend, n_streams)
+        vr.warm(cloud, cams[0])
+        nb = int(vr.lib.tcgs_counters_bytes())
+        snaps = torch.empty((len(cams), nb), dtype=torch.uint8).pin_memory()
+        outs = []
+        for v, cam in enumerate(cams):
+            i = vr.k % len(vr.streams)
+            rgb, T, cnt = vr.launch(cloud, cam)
+            with torch.cuda.stream(vr.streams[i]):
+                outs.append((rgb.clone(), T.clone(), cnt.clone()))
+                _abi.check(vr.lib.tcgs_snapshot_stats(ctypes.c_void_p(vr.renderers[i].ws.data_ptr()),
+                                                      ctypes.c_void_p(snaps[v].data_ptr()),
+                                                      ctypes.c_void_p(vr.streams[i].cuda_stream)), "snapshot")
+        vr.join()
+        torch.cuda.current_stream(means.device).synchronize()
+        out = []
+        for v, cam in enumerate(cams):
+            st = _abi.Stats()
+            rc = vr.lib.tcgs_decode_stats(ctypes.c_void_p(snaps[v].data_ptr()), vr.renderers[0]._opts(), st)
+            if rc == _abi.TCGS_ERR_CAPACITY:  # this view needed a bigger workspace: redo it synchronously
+                f = vr.renderers[0].render_frame(cloud, cam, timed=False)
+                out.append((f.rgb.clone(), f.T.clone(), f.n_contrib.clone(), f.stats))
+                continue
+            _abi.check(rc, "tcgs_decode_stats")
+            out.append((*outs[v], FragmentStats(f_blend=st.f_blend, f_cull=st.f_cull, f_skip=st.f_skip,
+                                                exp_calls=st.exp_calls, n_splats=st.n_splats, dropped=st.dropped,
+                                                pixels_terminated=st.pixels_terminated, n_visible=st.n_visible)))
+    return {"rgb": torch.stack([o[0] for o in out]), "T": torch.stack([o[1] for o in out]),
+            "n_contrib": torch.stack([o[2] for o in out]), "stats": [o[3] for o in out]}

@@ -431,6 +431,21 @@ def test_view_renderer_streams_match_sequential(renderers):
         assert torch.equal(a, b)
 
 
+def test_rasterize_batched_views_match_frames():
+    scene, cams = synthetic.config_scene("c4", 0.02)
+    views = [cams[i] for i in (3, 70, 150, 220, 250)]
+    dev = {k: torch.as_tensor(np.ascontiguousarray(scene[k]), device="cuda")
+           for k in ("means", "scales", "rotations", "opacities", "features")}
+    out = tcgs.rasterize(dev["means"], dev["scales"], dev["rotations"], dev["opacities"], dev["features"],
+                         scene["sh_degree"], views)
+    r = tcgs.Renderer("cuda", "tcgs")
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    for v, cam in enumerate(views):
+        f = r.render_frame(cloud, cam, timed=False)
+        assert torch.equal(out["rgb"][v], f.rgb) and torch.equal(out["n_contrib"][v], f.n_contrib)
+        assert out["stats"][v].f_blend == f.stats.f_blend and out["stats"][v].n_splats == f.stats.n_splats
+
+
 # ---- full-size parity (BASELINE config shapes) against the oracle ---------------------------------
 
 @pytest.mark.slow

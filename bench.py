@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--backend", default="tcgs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--streams", type=int, default=3, help="views in flight (one workspace + CUDA stream each)")
+    ap.add_argument("--streams", type=int, default=4, help="views in flight (one workspace + CUDA stream each)")
     ap.add_argument("--band-output", default="peer", choices=["peer", "gather"],
                     help="c3 tile bands: K7 writes into rank 0's frame over peer memory, or one NCCL gather")
     return ap.parse_args()

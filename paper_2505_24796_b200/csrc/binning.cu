@@ -433,7 +433,8 @@ template <typename KT, int IPT>
 cudaError_t launch_radix_pass(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const unsigned long long *n_dev,
                               int64_t n_host, int64_t cap, int pass, SortState *ss, uint32_t *table_all,
                               cudaStream_t st) {
-    static bool configured = false;
+    static bool configured_dev[TCGS_MAX_DEVICES] = {};
+    bool &configured = configured_dev[current_device()];
     constexpr int smem = downsweep_smem<KT, IPT>();
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(radix_downsweep<KT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -431,7 +431,8 @@ template <typename T>
 cudaError_t launch_k1(const PreArgs &a, const tcgs_scene &scene, int F, int nt, cudaStream_t st) {
     size_t smem = 0;
     for (int per : {3, 3, 4, 1, F}) smem += ((size_t)per * nt * sizeof(T) + 15) / 16 * 16;
-    static size_t configured = 0;
+    static size_t configured_dev[TCGS_MAX_DEVICES] = {};
+    size_t &configured = configured_dev[current_device()];
     if (smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(preprocess_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);

@@ -687,7 +687,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
 
 template <int MODE>
 cudaError_t launch_mode(const RenderArgs &a, int num_sms, cudaStream_t st) {
-    static bool configured = false;
+    static bool configured_dev[TCGS_MAX_DEVICES] = {};
+    bool &configured = configured_dev[current_device()];
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(render_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, K7_SMEM_BYTES);
         if (e != cudaSuccess) return e;

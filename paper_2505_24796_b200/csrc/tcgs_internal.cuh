@@ -154,6 +154,14 @@ int tile_key_bits(const Band &band);
 // Host-side count of kernels this library has launched (tcgs_launch_count): the bench's gpu_launches.
 void note_launch();
 
+// Function attributes (max dynamic smem, carveout) are per device: launchers cache "already set" per device.
+constexpr int TCGS_MAX_DEVICES = 64;
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d < 0 ? 0 : (d >= TCGS_MAX_DEVICES ? TCGS_MAX_DEVICES - 1 : d);
+}
+
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

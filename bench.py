@@ -149,6 +149,25 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def stage_rooflines(scene, P, st, stage_ms, peaks, cam):
+    """Algorithmic bytes per stage / isolated stage time, against the measured HBM copy peak.
+    K1: P x (inputs + 76 B of outputs); binning: P (8 B depth + 4 B index) read + write, N (2 B tile key +
+    4 B id) written and sorted once, N x 2 B of ranges; K7: N x 52 B (id + 48 B record) + 20 B per pixel."""
+    feats = 3 * 4 * ((scene.get("sh_degree", 0) + 1) ** 2 if scene.get("sh_degree", 0) > 0 else 1)
+    N = st.n_splats
+    work = {"preprocess": P * (44 + feats + 76), "binning": P * 12 * 2 + N * 6 * 2 + N * 2,
+            "blend": N * 52 + cam.width * cam.height * 20}
+    out = {}
+    for k, b in work.items():
+        ms = stage_ms.get(k) if isinstance(stage_ms, dict) else None
+        if not ms:
+            continue
+        gbs = b / (ms * 1e-3) / 1e9
+        out[k] = {"bytes_alg": int(b), "ms": ms, "achieved_GBps": gbs, "peak_GBps": peaks["hbm_gbs"],
+                  "frac": gbs / peaks["hbm_gbs"]}
+    return out
+
+
 def issue_roofline(traffic, blend_ms, clocks):
     """K7's binding resource: warp-instruction issue (4 per clock per SM).  Instructions per launch come from
     the committed ncu capture (smsp__inst_executed.sum), the duration from this run's CUDA events."""
@@ -484,6 +503,7 @@ def run_tcgs(args):
         "views_in_flight": 1 if bands_mode else max(1, args.streams),
         "band_output": (args.band_output if world > 1 else "local") if bands_mode else None,
         "alpha_blend_ms": blend_avg,
+        "stage_rooflines": stage_rooflines(scene, cloud.P, st_last, iso or stage, peaks, base),
         "alpha_blend_ms_max_over_ranks": blend_max,
         "stage_ms": stage,
         "frame_stats": {**st_last.to_dict(), "n_visible": st_last.n_visible},

@@ -586,26 +586,13 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                                                    p1.y * uy * uy);
                         }
                     }
-                    uint32_t pass;
-                    if (fold_cut<MODE>()) {
-                        // sign bits -> fail mask: one funnel shift per column, (fail << 1) | (beta'' >> 31)
-                        uint32_t fail = 0;
-#pragma unroll
-                        for (int j = 15; j >= 0; j--) fail = __funnelshift_l(r[j], fail, 1);
-                        pass = ~fail;
-                    } else {
-                        pass = 0;
-#pragma unroll
-                        for (int j = 0; j < 16; j++)
-                            if (__uint_as_float(r[j]) >= CUT_LOG2) pass |= 1u << j;
-                    }
-                    pass &= (uint32_t)(act >> (16 * hc)) & 0xffffu;
-                    const uint32_t wm = __reduce_or_sync(FULL, pass);
+                    // per column: this pixel passes EarlyCull iff beta >= thr (thr = the cut while live, +inf once
+                    // done); a warp vote skips the column when no pixel of the warp passes (uniform branch)
 #pragma unroll
                     for (int j = 0; j < 16; j++) {
-                        if (wm & (1u << j)) {  // warp-uniform: some pixel of the warp passes EarlyCull here
-                            const float bb = __uint_as_float(r[j]);
-                            const bool p = bb >= thr;
+                        const float bb = __uint_as_float(r[j]);
+                        const bool p = bb >= thr && 16 * hc + j < nl;
+                        if (__any_sync(FULL, p)) {
                             // alpha = 2^beta' (no min(alpha, 1): alpha > 1 only by rounding, and then
                             // T - alpha T < 1e-4 terminates exactly as alpha = 1 would)
                             const float al = fold_cut<MODE>() ? ex2_approx(bb) * INV255 : ex2_approx(bb);

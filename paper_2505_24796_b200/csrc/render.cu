@@ -357,6 +357,18 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
         auto emit = [&](int tile, int sq, int n_live, int last, uint32_t dead_total, uint32_t n_total) {
             acquire();
             const int st = k % S;
+            // unused columns of a partial stage: a row whose beta is -65504 at every pixel, so consumers need
+            // no per-column validity test (it can never pass EarlyCull)
+            for (int row = n_live + lane; tile >= 0 && row < K7_BATCH; row += 32) {
+                if (TC) {
+                    const uint4 lo = make_uint4(0xFBFFu, 0u, 0u, 0u);  // fp16 -65504 in K-column 0 (U = 1)
+                    *reinterpret_cast<uint4 *>(sm.V[st] + kmaj_off(row, 0)) = lo;
+                    *reinterpret_cast<uint4 *>(sm.V[st] + kmaj_off(row, 8)) = make_uint4(0u, 0u, 0u, 0u);
+                } else {
+                    sm.vf[st][row][0] = make_float4(-65504.0f, 0.f, 0.f, 0.f);
+                    sm.vf[st][row][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
             if (TC) fence_async_smem();
             __syncwarp();
             if (lane == 0) {
@@ -591,7 +603,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
 #pragma unroll
                     for (int j = 0; j < 16; j++) {
                         const float bb = __uint_as_float(r[j]);
-                        const bool p = bb >= thr && 16 * hc + j < nl;
+                        const bool p = bb >= thr;  // (columns >= n_live hold beta = -65504: never pass)
                         if (__any_sync(FULL, p)) {
                             // alpha = 2^beta' (no min(alpha, 1): alpha > 1 only by rounding, and then
                             // T - alpha T < 1e-4 terminates exactly as alpha = 1 would)

@@ -568,7 +568,6 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
             if (!warp_done) {
                 const int nl = m.n_live;
                 const mask_t act0 = done ? (mask_t)0 : (nl >= K7_BATCH ? ALL_COLS : (((mask_t)1 << nl) - 1));
-                mask_t act = act0;
                 const uint32_t tb = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (2 * K7_BATCH) + half * K7_BATCH;
                 int jt = K7_BATCH;
                 // pass threshold of beta: the EarlyCull cut while the pixel is live, +inf once it has
@@ -624,7 +623,6 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                             }
                         }
                     }
-                    if (jt < K7_BATCH) act = 0;  // terminated in this group: nothing later is live
                 }
                 const bool tstage = jt < K7_BATCH;
                 term = term || tstage;

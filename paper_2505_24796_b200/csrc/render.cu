@@ -44,7 +44,6 @@ constexpr float LOG2E = 1.4426950408889634f;
 constexpr float CUT_LOG2 = -7.994353436858858f;  // -log2(255): beta' < CUT culls (tensor_path.py:79-81)
 constexpr float LN255 = 5.541263545158426f;
 constexpr float TERM_T = 0.0001f;                // src/tilesplat/raster.py:16
-constexpr float INV255 = 1.0f / 255.0f;          // 2^(-log2 255)
 // also caps residency at K7_CTAS_PER_SM CTAs/SM (TMEM: K7_CTAS_PER_SM x K7_TMEM_COLS <= 512 columns)
 constexpr int K7_SMEM_BYTES = (K7_CTAS_PER_SM >= 4 ? 54 : 72) * 1024;
 constexpr int S = K7_STAGES;
@@ -214,10 +213,6 @@ __device__ __forceinline__ bool gaussian_coeffs(const Rec &r, double ox, double 
     return true;
 }
 
-// FOLD modes carry beta'' = beta' + log2(255) (the EarlyCull threshold folded into v0), so a fragment passes
-// iff beta'' >= 0: its pass bit is the complement of the float's sign bit, extracted on the FMA pipe.
-template <int MODE>
-__host__ __device__ constexpr bool fold_cut() { return MODE != TCGS_ALPHA_TC_K8; }
 
 __device__ __forceinline__ __half h16(float x) { return __float2half_rn(x); }
 __device__ __forceinline__ float f32(__half x) { return __half2float(x); }
@@ -339,7 +334,6 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
         float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool live = false;
         if (valid) live = gaussian_coeffs(rc, (double)cur.ox, (double)cur.oy, v);  // tile_center (tensor_path.py:21-22)
-        if (fold_cut<MODE>()) v[0] -= CUT_LOG2;
         uint4 vlo = make_uint4(0, 0, 0, 0), vhi = make_uint4(0, 0, 0, 0);
         if (TC && live) make_vrow<MODE>(v, vlo, vhi);
         const float4 col = make_float4(rc.r, rc.g, rc.b, 0.f);
@@ -572,7 +566,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 int jt = K7_BATCH;
                 // pass threshold of beta: the EarlyCull cut while the pixel is live, +inf once it has
                 // terminated (a float, so the test stays one FSETP and the update a predicated move)
-                const float cut0 = fold_cut<MODE>() ? 0.0f : CUT_LOG2;
+                const float cut0 = CUT_LOG2;
                 float thr = done ? __int_as_float(0x7f800000) : cut0;
                 const float fcnt0 = fcnt;
 #pragma unroll
@@ -606,7 +600,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                         if (__any_sync(FULL, p)) {
                             // alpha = 2^beta' (no min(alpha, 1): alpha > 1 only by rounding, and then
                             // T - alpha T < 1e-4 terminates exactly as alpha = 1 would)
-                            const float al = fold_cut<MODE>() ? ex2_approx(bb) * INV255 : ex2_approx(bb);
+                            const float al = ex2_approx(bb);
                             const float tn = fmaf(-al, T, T);
                             if (p && tn < TERM_T) {  // termination precedes compositing
                                 jt = 16 * hc + j;

@@ -16,20 +16,23 @@
 // (TCGS_ALPHA_TC_K8 keeps the paper's length-8 fp16 vector for ablation).
 //
 // CTA = 8 consumer warps (one pixel per thread; warp w owns an 8x4 pixel block
-// = TMEM lanes 32(w%4).. of pixel half w/4) + 1 producer warp.
-//   producer: takes tiles from a global queue, gathers each list entry's
-//     projected record, drops Gaussians whose EarlyCull test fails at every
-//     pixel of the tile (exact box minimum of the quadratic form -- these are
-//     culls the reference would count, and are counted), compacts the live
-//     ones 32 at a time into a shared-memory stage (fp16 hi/lo V rows,
-//     colours, dead-before counts), and issues two M=128 x N=32 x K=16 MMAs
-//     per stage into a TMEM accumulator buffer (commit -> mbarrier);
-//   consumers: tcgen05.ld their 32 betas, build the pass mask of EarlyCull
-//     (beta' < -log2 255 culls without an exponential), then walk the warp's
-//     union of passing columns in order: alpha = ex2(beta'), the termination
-//     test before compositing (T - alpha T < 1e-4, src/tilesplat/raster.py:
-//     136-145), C += alpha T c, T -= alpha T.  A warp whose pixels have all
-//     terminated stops working; when all 8 have, the producer retires the tile.
+// = TMEM lanes 32(w%4).. of pixel half w/4) + 2 producer warps; 3 CTAs per SM.
+//   producers: walk the CTA's static tile stream (blockIdx.x, +gridDim.x, ...) in
+//     32-entry chunks, alternating chunks and handing the compaction state over
+//     with a token mbarrier; gather each entry's projected record, drop Gaussians
+//     whose EarlyCull test fails at every pixel of the tile (exact box minimum of
+//     the quadratic form -- culls the reference would count, and they are
+//     counted), compact the live ones 32 at a time into a shared-memory stage
+//     (fp16 hi/lo V rows, colours, dead-before counts; unused rows of a partial
+//     stage get beta = -65504), and issue two M=128 x N=32 x K=16 MMAs per stage
+//     into a TMEM accumulator buffer (commit -> mbarrier);
+//   consumers: tcgen05.ld their 32 betas; per column, a pixel passes EarlyCull
+//     iff beta' >= thr (thr = -log2 255 while live, +inf once done) and a warp
+//     vote skips columns no pixel passes (uniform branch, 3 instructions); in a
+//     taken column: alpha = ex2(beta'), the termination test before compositing
+//     (T - alpha T < 1e-4, src/tilesplat/raster.py:136-145), C += alpha T c,
+//     T -= alpha T.  A warp whose pixels have all terminated stops working; when
+//     all 8 have, the producers retire the tile.
 // Stages (4) and TMEM buffers (2) are ring buffers guarded by full/empty and
 // mma_done/tmem_empty mbarriers, so gathers, MMAs and blending overlap.
 #include <type_traits>

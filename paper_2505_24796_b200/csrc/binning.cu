@@ -545,6 +545,11 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
     __shared__ uint32_t gid[DUP_THREADS];
     __shared__ short4 rc[DUP_THREADS];
     __shared__ uint32_t wt[8];
+    // staging of one round's output: every thread writes its own rectangle (no search, no division), then
+    // the CTA copies the round out with coalesced stores
+    constexpr int DUP_STAGE = 4096;
+    __shared__ KT skey[DUP_STAGE];
+    __shared__ uint32_t sval[DUP_STAGE];
     const uint32_t *order = ctr->depth_cur ? idx1 : idx0;
     const int tid = threadIdx.x;
     const int64_t beg = (int64_t)blockIdx.x * DUP_ITEMS;
@@ -563,27 +568,63 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
         }
         uint32_t total;
         const uint32_t ex = block_excl_scan256(c, wt, &total);
-        incl[tid] = ex + c;
-        gid[tid] = g;
-        rc[tid] = q;
-        __syncthreads();
-        for (uint32_t s = tid; s < total; s += DUP_THREADS) {
-            int lo = 0, hi = DUP_THREADS - 1;  // first item whose inclusive count exceeds s
-#pragma unroll 8
-            for (int step = 0; step < 8; step++) {
-                const int mid = (lo + hi) >> 1;
-                if (incl[mid] > s) hi = mid;
-                else lo = mid + 1;
+        if (total <= (uint32_t)DUP_STAGE) {
+            constexpr uint32_t SMALL = 32;
+            if (c <= SMALL) {
+                uint32_t o = ex;
+                for (int ty = q.y; ty <= q.w; ty++) {
+                    const uint32_t row = (uint32_t)((ty - band_y0) * tiles_x);
+                    for (int tx = q.x; tx <= q.z; tx++, o++) {
+                        skey[o] = (KT)(row + tx);
+                        sval[o] = g;
+                    }
+                }
             }
-            const uint32_t kk = s - (lo ? incl[lo - 1] : 0u);
-            const short4 qq = rc[lo];
-            const int w = qq.z - qq.x + 1;
-            const int ty = qq.y + (int)(kk / w), tx = qq.x + (int)(kk % w);
-            const uint32_t key = (uint32_t)((ty - band_y0) * tiles_x + tx);
-            const unsigned long long pos = base + s;
-            if (pos < (unsigned long long)cap) {
-                tkey[pos] = (KT)key;
-                tval[pos] = gid[lo];
+            const int lane = tid & 31;
+            unsigned big = __ballot_sync(0xffffffffu, c > SMALL);
+            while (big) {  // large rectangles: the whole warp writes one
+                const int src = __ffs(big) - 1;
+                big &= big - 1;
+                const uint32_t bc = __shfl_sync(0xffffffffu, c, src), bg = __shfl_sync(0xffffffffu, g, src);
+                const uint32_t bex = __shfl_sync(0xffffffffu, ex, src);
+                const int bx0 = __shfl_sync(0xffffffffu, (int)q.x, src), by0 = __shfl_sync(0xffffffffu, (int)q.y, src);
+                const int bw = __shfl_sync(0xffffffffu, (int)(q.z - q.x + 1), src);
+                for (uint32_t kk = lane; kk < bc; kk += 32) {
+                    skey[bex + kk] = (KT)((by0 + (int)(kk / bw) - band_y0) * tiles_x + bx0 + (int)(kk % bw));
+                    sval[bex + kk] = bg;
+                }
+            }
+            __syncthreads();
+            for (uint32_t s2 = tid; s2 < total; s2 += DUP_THREADS) {
+                const unsigned long long pos = base + s2;
+                if (pos < (unsigned long long)cap) {
+                    tkey[pos] = skey[s2];
+                    tval[pos] = sval[s2];
+                }
+            }
+        } else {  // a round with huge rectangles: search-based expansion straight to global memory
+            incl[tid] = ex + c;
+            gid[tid] = g;
+            rc[tid] = q;
+            __syncthreads();
+            for (uint32_t s = tid; s < total; s += DUP_THREADS) {
+                int lo = 0, hi = DUP_THREADS - 1;  // first item whose inclusive count exceeds s
+    #pragma unroll 8
+                for (int step = 0; step < 8; step++) {
+                    const int mid = (lo + hi) >> 1;
+                    if (incl[mid] > s) hi = mid;
+                    else lo = mid + 1;
+                }
+                const uint32_t kk = s - (lo ? incl[lo - 1] : 0u);
+                const short4 qq = rc[lo];
+                const int w = qq.z - qq.x + 1;
+                const int ty = qq.y + (int)(kk / w), tx = qq.x + (int)(kk % w);
+                const uint32_t key = (uint32_t)((ty - band_y0) * tiles_x + tx);
+                const unsigned long long pos = base + s;
+                if (pos < (unsigned long long)cap) {
+                    tkey[pos] = (KT)key;
+                    tval[pos] = gid[lo];
+                }
             }
         }
         base += total;

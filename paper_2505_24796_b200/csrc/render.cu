@@ -35,8 +35,6 @@
 //     all 8 have, the producers retire the tile.
 // Stages (4) and TMEM buffers (2) are ring buffers guarded by full/empty and
 // mma_done/tmem_empty mbarriers, so gathers, MMAs and blending overlap.
-#include <type_traits>
-
 #include "tcgs_internal.cuh"
 
 namespace tcgs {
@@ -50,13 +48,6 @@ constexpr float TERM_T = 0.0001f;                // src/tilesplat/raster.py:16
 // also caps residency at K7_CTAS_PER_SM CTAs/SM (TMEM: K7_CTAS_PER_SM x K7_TMEM_COLS <= 512 columns)
 constexpr int K7_SMEM_BYTES = (K7_CTAS_PER_SM >= 4 ? 54 : 72) * 1024;
 constexpr int S = K7_STAGES;
-// column masks of one stage
-using mask_t = std::conditional<(K7_BATCH > 32), unsigned long long, uint32_t>::type;
-constexpr mask_t ALL_COLS = K7_BATCH >= 64 ? ~(mask_t)0 : (mask_t)(((unsigned long long)1 << K7_BATCH) - 1);
-__device__ __forceinline__ uint32_t popc_cols(mask_t m) {
-    if constexpr (K7_BATCH > 32) return (uint32_t)__popcll(m);
-    else return (uint32_t)__popc((uint32_t)m);
-}
 constexpr int NB = K7_TMEM_BUFS;
 
 struct RenderArgs {
@@ -564,7 +555,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
             bool tmem_released = false;
             if (!warp_done) {
                 const int nl = m.n_live;
-                const mask_t act0 = done ? (mask_t)0 : (nl >= K7_BATCH ? ALL_COLS : (((mask_t)1 << nl) - 1));
+                const bool live0 = !done;
                 const uint32_t tb = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (2 * K7_BATCH) + half * K7_BATCH;
                 int jt = K7_BATCH;
                 // pass threshold of beta: the EarlyCull cut while the pixel is live, +inf once it has
@@ -626,8 +617,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 done = done || tstage;
                 // EarlyCull counts: valid columns before the termination that did not blend, plus the dead
                 // Gaussians of the list before the terminating one
-                const mask_t before = tstage ? (((mask_t)1 << jt) - 1) : ALL_COLS;
-                cull += popc_cols(act0 & before) - (uint32_t)(fcnt - fcnt0);
+                if (live0) cull += (uint32_t)(tstage ? jt : nl) - (uint32_t)(fcnt - fcnt0);
                 if (tstage) cull += sm.dead_before[st][jt];
                 if (__all_sync(FULL, done)) {
                     warp_done = true;

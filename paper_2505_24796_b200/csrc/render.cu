@@ -563,53 +563,56 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 const float cut0 = CUT_LOG2;
                 float thr = done ? __int_as_float(0x7f800000) : cut0;
                 const float fcnt0 = fcnt;
-#pragma unroll
-                for (int hc = 0; hc < K7_BATCH / 16; hc++) {  // 16-column groups keep 16 betas live in registers
-                    uint32_t r[16];
-                    if (TC) {
-                        tmem_ld16(tb + 16 * hc, r);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int j = 0; j < 16; j++) asm volatile("" : "+r"(r[j]));
-                        if (NB == 1 && hc == K7_BATCH / 16 - 1) {  // single accumulator: free it for the next MMA
-                            tc_fence_before();
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive(&sm.tmem_empty[b]);
-                            tmem_released = true;
+                // one column of the stage: this pixel passes EarlyCull iff beta >= thr (thr = the cut while live,
+                // +inf once done); a warp vote skips the column when no pixel of the warp passes (uniform branch)
+                auto column = [&](uint32_t rb, int col) {
+                    const float bb = __uint_as_float(rb);
+                    const bool p = bb >= thr;  // (columns >= n_live hold beta = -65504: never pass)
+                    if (__any_sync(FULL, p)) {
+                        // alpha = 2^beta' (no min(alpha, 1): alpha > 1 only by rounding, and then
+                        // T - alpha T < 1e-4 terminates exactly as alpha = 1 would)
+                        const float al = ex2_approx(bb);
+                        const float tn = fmaf(-al, T, T);
+                        if (p && tn < TERM_T) {  // termination precedes compositing
+                            jt = col;
+                            thr = __int_as_float(0x7f800000);
                         }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 16; j++) {
-                            const float4 p0 = sm.vf[st][16 * hc + j][0], p1 = sm.vf[st][16 * hc + j][1];
-                            r[j] = __float_as_uint(p0.x + p0.y * ux + p0.z * uy + p0.w * ux * ux + p1.x * ux * uy +
-                                                   p1.y * uy * uy);
+                        if (p && tn >= TERM_T) {
+                            const float4 cc = sm.col[st][col];
+                            const float w = al * T;
+                            c0 = fmaf(w, cc.x, c0);
+                            c1 = fmaf(w, cc.y, c1);
+                            c2 = fmaf(w, cc.z, c2);
+                            T = tn;
+                            fcnt += 1.0f;
                         }
                     }
-                    // per column: this pixel passes EarlyCull iff beta >= thr (thr = the cut while live, +inf once
-                    // done); a warp vote skips the column when no pixel of the warp passes (uniform branch)
+                };
+                {
 #pragma unroll
-                    for (int j = 0; j < 16; j++) {
-                        const float bb = __uint_as_float(r[j]);
-                        const bool p = bb >= thr;  // (columns >= n_live hold beta = -65504: never pass)
-                        if (__any_sync(FULL, p)) {
-                            // alpha = 2^beta' (no min(alpha, 1): alpha > 1 only by rounding, and then
-                            // T - alpha T < 1e-4 terminates exactly as alpha = 1 would)
-                            const float al = ex2_approx(bb);
-                            const float tn = fmaf(-al, T, T);
-                            if (p && tn < TERM_T) {  // termination precedes compositing
-                                jt = 16 * hc + j;
-                                thr = __int_as_float(0x7f800000);
+                    for (int hc = 0; hc < K7_BATCH / 16; hc++) {  // 16-column groups: 16 betas live in registers
+                        uint32_t r[16];
+                        if (TC) {
+                            tmem_ld16(tb + 16 * hc, r);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int j = 0; j < 16; j++) asm volatile("" : "+r"(r[j]));
+                            if (NB == 1 && hc == K7_BATCH / 16 - 1) {  // single accumulator: free it for the next MMA
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive(&sm.tmem_empty[b]);
+                                tmem_released = true;
                             }
-                            if (p && tn >= TERM_T) {
-                                const float4 cc = sm.col[st][16 * hc + j];
-                                const float w = al * T;
-                                c0 = fmaf(w, cc.x, c0);
-                                c1 = fmaf(w, cc.y, c1);
-                                c2 = fmaf(w, cc.z, c2);
-                                T = tn;
-                                fcnt += 1.0f;
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; j++) {
+                                const float4 p0 = sm.vf[st][16 * hc + j][0], p1 = sm.vf[st][16 * hc + j][1];
+                                r[j] = __float_as_uint(p0.x + p0.y * ux + p0.z * uy + p0.w * ux * ux + p1.x * ux * uy +
+                                                       p1.y * uy * uy);
                             }
                         }
+#pragma unroll
+                        for (int j = 0; j < 16; j++) column(r[j], 16 * hc + j);
                     }
                 }
                 const bool tstage = jt < K7_BATCH;

@@ -446,6 +446,42 @@ def test_rasterize_batched_views_match_frames():
         assert out["stats"][v].f_blend == f.stats.f_blend and out["stats"][v].n_splats == f.stats.n_splats
 
 
+def test_c_abi_one_call_render_matches_staged_calls(renderers):
+    """tcgs_render (K1 + K2-K6 + K7 in one C call, the INTEGRATION.md example) == the staged calls."""
+    from paper_2505_24796_b200 import _abi
+    from paper_2505_24796_b200.raster import camera_struct
+
+    g = load_golden("c1")
+    cam = GoldenCam(g)
+    r = renderers["tcgs"]
+    cloud = cloud_of(g)
+    ref = r.render_frame(cloud, cam)
+    rgb_ref, cnt_ref = ref.rgb.clone(), ref.n_contrib.clone()
+    c = camera_struct(cam)
+    cap = r.max_splats
+    ws = torch.empty(int(r.lib.tcgs_workspace_size(cloud.P, c.width, c.height, cap)), dtype=torch.uint8,
+                     device="cuda")
+    rgb = torch.zeros((c.height, c.width, 3), dtype=torch.float32, device="cuda")
+    T = torch.ones((c.height, c.width), dtype=torch.float32, device="cuda")
+    cnt = torch.zeros((c.height, c.width), dtype=torch.int32, device="cuda")
+    o = r._opts()
+    st = torch.cuda.current_stream().cuda_stream
+    _abi.check(r.lib.tcgs_render(cloud._c(), c, o, ws.data_ptr(), ws.numel(), cap, rgb.data_ptr(), T.data_ptr(),
+                                 cnt.data_ptr(), st), "tcgs_render")
+    stats = _abi.Stats()
+    _abi.check(r.lib.tcgs_read_stats(ws.data_ptr(), cloud.P, o, stats, st), "tcgs_read_stats")
+    assert torch.equal(rgb, rgb_ref) and torch.equal(cnt, cnt_ref)
+    assert (stats.f_blend, stats.f_cull, stats.n_splats) == (ref.stats.f_blend, ref.stats.f_cull, ref.stats.n_splats)
+    # argument errors come back as codes (ValueError in Python), never as a launch
+    bad = camera_struct(cam)
+    bad.fx = -1.0
+    n0 = r.lib.tcgs_launch_count()
+    with pytest.raises(ValueError):
+        _abi.check(r.lib.tcgs_render(cloud._c(), bad, o, ws.data_ptr(), ws.numel(), cap, rgb.data_ptr(),
+                                     T.data_ptr(), cnt.data_ptr(), st), "tcgs_render")
+    assert r.lib.tcgs_launch_count() == n0
+
+
 # ---- full-size parity (BASELINE config shapes) against the oracle ---------------------------------
 
 @pytest.mark.slow

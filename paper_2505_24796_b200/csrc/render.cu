@@ -179,22 +179,24 @@ __device__ __forceinline__ bool gaussian_coeffs(const Rec &r, double ox, double 
     if (outside && s11 > 0.0f && s22 > 0.0f) {
         // (the minimiser only needs to be accurate to first order: q is flat there, and the test keeps a margin)
         const float r11 = __fdividef(s12, s11), r22 = __fdividef(s12, s22);
-        float qmin = 3.0e38f;
-#pragma unroll
-        for (int e = 0; e < 2; e++) {
-            const float a = e ? 7.0f : -8.0f;
-            {  // edge ux = a
-                const float ex = dx - a;
-                const float uy = fminf(fmaxf(dy + r22 * ex, -8.0f), 7.0f);
-                const float ey = dy - uy;
-                qmin = fminf(qmin, s11 * ex * ex + 2.0f * s12 * ex * ey + s22 * ey * ey);
-            }
-            {  // edge uy = a
-                const float ey = dy - a;
-                const float ux = fminf(fmaxf(dx + r11 * ey, -8.0f), 7.0f);
-                const float ex = dx - ux;
-                qmin = fminf(qmin, s11 * ex * ex + 2.0f * s12 * ex * ey + s22 * ey * ey);
-            }
+        // The unconstrained minimiser d lies outside the box, so the box minimum lies on a face the segment
+        // from any box point to d crosses: the face x = clamp(dx) if dx is outside [-8, 7], the face
+        // y = clamp(dy) if dy is.  Evaluating the two clamped lines always is safe: a line through the box
+        // interior only gives values >= the box minimum.
+        float qmin;
+        {  // line ux = clamp(dx)
+            const float a = fminf(fmaxf(dx, -8.0f), 7.0f);
+            const float ex = dx - a;
+            const float uy = fminf(fmaxf(dy + r22 * ex, -8.0f), 7.0f);
+            const float ey = dy - uy;
+            qmin = s11 * ex * ex + 2.0f * s12 * ex * ey + s22 * ey * ey;
+        }
+        {  // line uy = clamp(dy)
+            const float a = fminf(fmaxf(dy, -8.0f), 7.0f);
+            const float ey = dy - a;
+            const float ux = fminf(fmaxf(dx + r11 * ey, -8.0f), 7.0f);
+            const float ex = dx - ux;
+            qmin = fminf(qmin, s11 * ex * ex + 2.0f * s12 * ex * ey + s22 * ey * ey);
         }
         if (r.ln_o - 0.5f * qmin < -LN255 - 0.01f) return false;
     }

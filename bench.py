@@ -120,7 +120,7 @@ class ClockSampler:
                 self._sample()
             except Exception:  # noqa: BLE001
                 break
-            time.sleep(0.02)
+            time.sleep(0.004)
 
     def __exit__(self, *exc):
         self._stop.set()

@@ -198,7 +198,9 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
                                                          const T *__restrict__ g_scales, const T *__restrict__ g_rots,
                                                          const T *__restrict__ g_opac, const T *__restrict__ g_feats) {
     extern __shared__ __align__(16) unsigned char pre_smem[];
-    __shared__ __align__(8) unsigned long long bar;
+    // two transaction barriers: geometry (means, scales, rotations, opacity) and features (RGB or SH), so the
+    // features' bulk copy -- most of the bytes at SH3 -- lands while the float64 projection runs
+    __shared__ __align__(8) unsigned long long bar[2];
     const int NT = blockDim.x;
     const int64_t base = (int64_t)blockIdx.x * NT;
     const int n = (int)(a.P - base < NT ? a.P - base : NT);
@@ -214,35 +216,46 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
             off += (((size_t)per[q] * NT * sizeof(T)) + 15) / 16 * 16;
         }
     }
-    bool any_bulk = false;
-    for (int q = 0; q < 5; q++) any_bulk |= bulk_ok(src[q] + base * per[q], (int64_t)n * per[q]);
-    if (threadIdx.x == 0 && any_bulk) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    bool bulk[5];
+    bool any_bulk[2] = {false, false};
+    for (int q = 0; q < 5; q++) {
+        bulk[q] = bulk_ok(src[q] + base * per[q], (int64_t)n * per[q]);
+        any_bulk[q == 4] |= bulk[q];
+    }
+    if (threadIdx.x == 0) {
+        for (int g = 0; g < 2; g++)
+            if (any_bulk[g]) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[g])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x == 0 && any_bulk) {
-        uint32_t tx = 0;
-        for (int q = 0; q < 5; q++)
-            if (bulk_ok(src[q] + base * per[q], (int64_t)n * per[q])) tx += (uint32_t)(n * per[q] * sizeof(T));
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)), "r"(tx) : "memory");
-        for (int q = 0; q < 5; q++)
-            if (bulk_ok(src[q] + base * per[q], (int64_t)n * per[q]))
-                bulk_g2s(seg[q], src[q] + base * per[q], (uint32_t)(n * per[q] * sizeof(T)), &bar);
+    if (threadIdx.x == 0) {
+        for (int g = 0; g < 2; g++) {
+            if (!any_bulk[g]) continue;
+            uint32_t tx = 0;
+            for (int q = g ? 4 : 0; q < (g ? 5 : 4); q++)
+                if (bulk[q]) tx += (uint32_t)(n * per[q] * sizeof(T));
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[g])), "r"(tx)
+                         : "memory");
+            for (int q = g ? 4 : 0; q < (g ? 5 : 4); q++)
+                if (bulk[q]) bulk_g2s(seg[q], src[q] + base * per[q], (uint32_t)(n * per[q] * sizeof(T)), &bar[g]);
+        }
     }
     for (int q = 0; q < 5; q++)  // ragged / unaligned segments: coalesced cooperative copy
-        if (!bulk_ok(src[q] + base * per[q], (int64_t)n * per[q]))
+        if (!bulk[q])
             for (int e = threadIdx.x; e < n * per[q]; e += NT) seg[q][e] = src[q][base * per[q] + e];
-    if (any_bulk) {
-        asm volatile(
-            "{\n"
-            ".reg .pred P1;\n"
-            "WAIT_%=:\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
-            "@!P1 bra WAIT_%=;\n"
-            "}\n" ::"r"(smem_u32(&bar))
-            : "memory");
-    }
+    auto wait_bar = [&](int g) {
+        if (any_bulk[g]) {
+            asm volatile(
+                "{\n"
+                ".reg .pred P1;\n"
+                "WAIT_%=:\n"
+                "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+                "@!P1 bra WAIT_%=;\n"
+                "}\n" ::"r"(smem_u32(&bar[g]))
+                : "memory");
+        }
+    };
+    wait_bar(0);
     __syncthreads();
     const int l = threadIdx.x;
     const T *means = seg[0], *scales = seg[1], *rots = seg[2], *opac = seg[3], *feats = seg[4];
@@ -385,6 +398,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
                     rc.ln_o = logf((float)o);
                     rc.opacity = (float)o;
                     float col[3];
+                    wait_bar(1);  // features staged (usually long done: they streamed in during the projection)
                     if (a.sh_degree < 0) {
                         col[0] = (float)ld(feats, 3 * l);
                         col[1] = (float)ld(feats, 3 * l + 1);
@@ -424,6 +438,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
             atomicMax(&a.ctr->key_max, kmax);
         }
     }
+    wait_bar(1);  // no CTA may retire with a bulk copy into its shared memory still in flight
 }
 
 

@@ -675,8 +675,10 @@ __global__ void pack_records(int64_t P, const double *mean2d, const double *coni
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P) return;
     Rec r;
-    r.mx = mean2d[2 * i];
-    r.my = mean2d[2 * i + 1];
+    r.mx = (float)mean2d[2 * i];
+    r.mx_lo = (float)(mean2d[2 * i] - (double)r.mx);
+    r.my = (float)mean2d[2 * i + 1];
+    r.my_lo = (float)(mean2d[2 * i + 1] - (double)r.my);
     r.s11 = (float)conic[3 * i];
     r.s12 = (float)conic[3 * i + 1];
     r.s22 = (float)conic[3 * i + 2];

@@ -389,8 +389,10 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
                     a.rect[i] = make_short4((short)x0, (short)y0, (short)x1, (short)y1);
                     key = (unsigned long long)__double_as_longlong(tz);  // tz > 0: bit order == value order
                     Rec rc;
-                    rc.mx = mx;
-                    rc.my = my;
+                    rc.mx = (float)mx;
+                    rc.mx_lo = (float)(mx - (double)rc.mx);
+                    rc.my = (float)my;
+                    rc.my_lo = (float)(my - (double)rc.my);
                     rc.s11 = (float)s11;
                     rc.s12 = (float)s12;
                     rc.s22 = (float)s22;

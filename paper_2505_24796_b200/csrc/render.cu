@@ -171,8 +171,10 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // tile's pixel box [-8,7]^2: the minimum of the convex quadratic q(d - u) over the box is exact (interior
 // minimiser or the clamped minimiser on one of the four edges), and the test keeps a 0.01 margin on
 // beta, so every fragment of a dead Gaussian in this tile is a cull in exact arithmetic too.
-__device__ __forceinline__ bool gaussian_coeffs(const Rec &r, double ox, double oy, float v[6]) {
-    const float dx = (float)(r.mx - ox), dy = (float)(r.my - oy);
+__device__ __forceinline__ bool gaussian_coeffs(const Rec &r, float ox, float oy, float v[6]) {
+    // mean - centre in fp32: hi - centre is exact for frame coordinates (both on the hi value's grid),
+    // then one rounding with the lo part -- the float64 difference to within an ulp of dx, with no FP64 op
+    const float dx = __fadd_rn(__fsub_rn(r.mx, ox), r.mx_lo), dy = __fadd_rn(__fsub_rn(r.my, oy), r.my_lo);
     const float s11 = r.s11, s12 = r.s12, s22 = r.s22;
     const float q = s11 * dx * dx + 2.0f * s12 * dx * dy + s22 * dy * dy;
     const bool outside = !(dx >= -8.0f && dx <= 7.0f && dy >= -8.0f && dy <= 7.0f);
@@ -329,7 +331,7 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
         const bool valid = cur.c * 32 + lane < cur.n;
         float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool live = false;
-        if (valid) live = gaussian_coeffs(rc, (double)cur.ox, (double)cur.oy, v);  // tile_center (tensor_path.py:21-22)
+        if (valid) live = gaussian_coeffs(rc, cur.ox, cur.oy, v);  // tile_center (tensor_path.py:21-22)
         uint4 vlo = make_uint4(0, 0, 0, 0), vhi = make_uint4(0, 0, 0, 0);
         if (TC && live) make_vrow<MODE>(v, vlo, vhi);
         const float4 col = make_float4(rc.r, rc.g, rc.b, 0.f);
@@ -513,7 +515,15 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
         float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
         uint32_t cull = 0, n_total = 0;
         float fcnt = 0.0f;  // blends of this pixel (exact in fp32; kept on the FMA pipe)
+#ifdef TCGS_K7_PROFILE  // experiment builds only: per-warp work (stages entered, relevant columns) replaces T / n_contrib
+        int prof_rel = 0, prof_st = 0;
+#endif
         auto flush = [&]() {
+#ifdef TCGS_K7_PROFILE
+            T = (float)prof_st;
+            fcnt = (float)prof_rel;
+            prof_rel = prof_st = 0;
+#endif
             if (inside) {
                 const int64_t p = (int64_t)py * a.width + px;
                 a.rgb[3 * p] = c0;
@@ -556,6 +566,9 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
             }
             bool tmem_released = false;
             if (!warp_done) {
+#ifdef TCGS_K7_PROFILE
+                prof_st++;
+#endif
                 const int nl = m.n_live;
                 const bool live0 = !done;
                 const uint32_t tb = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (2 * K7_BATCH) + half * K7_BATCH;
@@ -571,6 +584,9 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                     const float bb = __uint_as_float(rb);
                     const bool p = bb >= thr;  // (columns >= n_live hold beta = -65504: never pass)
                     if (__any_sync(FULL, p)) {
+#ifdef TCGS_K7_PROFILE
+                        prof_rel++;
+#endif
                         // alpha = 2^beta' (no min(alpha, 1): alpha > 1 only by rounding, and then
                         // T - alpha T < 1e-4 terminates exactly as alpha = 1 would)
                         const float al = ex2_approx(bb);

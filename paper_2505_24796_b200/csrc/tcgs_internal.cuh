@@ -44,7 +44,7 @@ constexpr int K7_CTAS_PER_SM = TCGS_K7_CTAS;
 
 // Per-Gaussian record consumed by the blend kernel (48 B, three 16 B loads).
 struct __align__(16) Rec {
-    double mx, my;             // float64 mean2d (src/tilesplat/projection.py:80-82)
+    float mx, mx_lo, my, my_lo;  // float64 mean2d (src/tilesplat/projection.py:80-82) as fp32 hi + lo pairs
     float s11, s12, s22, ln_o; // conic (rounded from float64) and log opacity
     float r, g, b, opacity;    // colour (SH evaluated) and opacity
 };

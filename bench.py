@@ -47,7 +47,10 @@ def parse():
     ap.add_argument("--backend", default="tcgs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--streams", type=int, default=4, help="views in flight (one workspace + CUDA stream each)")
+    ap.add_argument("--streams", type=int, default=16, help="views in flight (one workspace + CUDA stream each)")
+    ap.add_argument("--view-group", type=int, default=8,
+                    help="views per fused K1 pass (tcgs_preprocess_views; <= --streams, <= 8); 0 = one K1 per "
+                         "view.  Two groups in flight: the next group's K1 overlaps this group's K2-K7")
     ap.add_argument("--band-output", default="peer", choices=["peer", "gather"],
                     help="c3 tile bands: K7 writes into rank 0's frame over peer memory, or one NCCL gather")
     return ap.parse_args()
@@ -190,14 +193,17 @@ def e2e_resident(vr, cloud, views, base, dev, world, dist):
             "d2h_bytes_per_step": base.width * base.height * 12 + nb, "steps": steps}
 
 
-def stage_rooflines(scene, P, st, stage_ms, peaks, cam):
+def stage_rooflines(scene, P, st, stage_ms, peaks, cam, group=0):
     """Algorithmic bytes per stage / isolated stage time, against the measured HBM copy peak.
     K1: P x (inputs + 76 B of outputs); binning: P (8 B depth + 4 B index) read + write, N (2 B tile key +
-    4 B id) written and sorted once, N x 2 B of ranges; K7: N x 52 B (id + 48 B record) + 20 B per pixel."""
+    4 B id) written and sorted once, N x 2 B of ranges; K7: N x 52 B (id + 48 B record) + 20 B per pixel.
+    The fused multi-view K1 reads the inputs once per group of views: P x (inputs / group + 76 B) per view."""
     feats = 3 * 4 * ((scene.get("sh_degree", 0) + 1) ** 2 if scene.get("sh_degree", 0) > 0 else 1)
     N = st.n_splats
     work = {"preprocess": P * (44 + feats + 76), "binning": P * 12 * 2 + N * 6 * 2 + N * 2,
             "blend": N * 52 + cam.width * cam.height * 20}
+    if group > 1:
+        work["preprocess_fused_per_view"] = P * ((44 + feats) / group + 76)
     out = {}
     for k, b in work.items():
         ms = stage_ms.get(k) if isinstance(stage_ms, dict) else None
@@ -363,13 +369,23 @@ def run_tcgs(args):
         st0 = vr.warm(cloud, base)  # sizes the workspaces; stats of the base view
     stream = torch.cuda.current_stream(dev)
 
+    group = 0 if bands_mode else max(0, min(args.view_group, max(1, args.streams), 8))
+
     def frame(cam, ev=None):
         if bands_mode:
             return br.render(cloud, cam, with_stats=False, timers=ev)
         return vr.launch(cloud, cam, timers=ev)
 
-    for k in range(args.warmup):
-        frame(my_views[k])
+    def frames(k0, n, ev=None):  # frames k0 .. k0+n-1 of my_views: one at a time, or in fused-K1 groups
+        if not group:
+            for k in range(k0, k0 + n):
+                frame(my_views[k], ev[k - k0] if ev else None)
+            return
+        for g0 in range(k0, k0 + n, group):
+            g1 = min(g0 + group, k0 + n)
+            vr.launch_group(cloud, my_views[g0:g1], timers=ev[g0 - k0] if ev else None)
+
+    frames(0, args.warmup)
     if not bands_mode:
         vr.join()
     torch.cuda.synchronize(dev)
@@ -385,8 +401,7 @@ def run_tcgs(args):
     launches0 = r.lib.tcgs_launch_count()
     with ClockSampler(local) as clk:
         start.record(stream)
-        for k in range(args.steps):
-            frame(my_views[args.warmup + k], evs[k])
+        frames(args.warmup, args.steps, evs)
         if not bands_mode:
             vr.join()
         stop.record(stream)
@@ -395,7 +410,12 @@ def run_tcgs(args):
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(stop)
-    pre_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    if group:  # one event set per group (recorded on its first frame): fused K1 per view, last view's K2-K7
+        evs = [evs[k] for k in range(0, args.steps, group)]
+        sizes = [min(group, args.steps - k) for k in range(0, args.steps, group)]
+        pre_ms = [e[0].elapsed_time(e[1]) / n for e, n in zip(evs, sizes)]
+    else:
+        pre_ms = [e[0].elapsed_time(e[1]) for e in evs]
     bin_ms = [e[1].elapsed_time(e[2]) for e in evs]
     blend_ms = [e[2].elapsed_time(e[3]) for e in evs]
     gather_ms = [e[3].elapsed_time(e[4]) for e in evs] if bands_mode else None
@@ -417,6 +437,12 @@ def run_tcgs(args):
         iso = {"preprocess": sum(e[0].elapsed_time(e[1]) for e in iso_ev) / len(iso_ev),
                "binning": sum(e[1].elapsed_time(e[2]) for e in iso_ev) / len(iso_ev),
                "blend": sum(e[2].elapsed_time(e[3]) for e in iso_ev) / len(iso_ev)}
+        if group > 1:  # the fused K1 alone: one pass over the scene for `group` views, per view
+            gev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            vr.launch_group(cloud, my_views[args.warmup:args.warmup + group], timers=gev)
+            vr.join()
+            torch.cuda.synchronize(dev)
+            iso["preprocess_fused_per_view"] = gev[0].elapsed_time(gev[1]) / group
     if bands_mode:
         st_last = br.render(cloud, my_views[-1], with_stats=True).local.stats
     else:
@@ -544,9 +570,10 @@ def run_tcgs(args):
         "config": bench_config(args, scene, base, world),
         "backend": args.backend,
         "views_in_flight": 1 if bands_mode else max(1, args.streams),
+        "view_group": group,
         "band_output": (args.band_output if world > 1 else "local") if bands_mode else None,
         "alpha_blend_ms": blend_avg,
-        "stage_rooflines": stage_rooflines(scene, cloud.P, st_last, iso or stage, peaks, base),
+        "stage_rooflines": stage_rooflines(scene, cloud.P, st_last, iso or stage, peaks, base, group),
         "alpha_blend_ms_max_over_ranks": blend_max,
         "stage_ms": stage,
         "frame_stats": {**st_last.to_dict(), "n_visible": st_last.n_visible},

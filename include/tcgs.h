@@ -99,6 +99,15 @@ size_t tcgs_workspace_size(int64_t P, int32_t width, int32_t height, int64_t max
 int tcgs_preprocess(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts *opts, void *ws,
                     size_t ws_bytes, int64_t max_splats, void *stream);
 
+/* K1 for up to TCGS_MAX_VIEWS_PER_PASS cameras of one scene in one pass: each Gaussian's inputs (236 B at
+ * SH3) are read once for all of them.  View v's outputs go to workspace ws[v] (each of
+ * ws_bytes bytes) exactly as tcgs_preprocess(scene, &cams[v], opts, ws[v], ...) writes them, so tcgs_bin /
+ * tcgs_blend then run per view (on any streams ordered after this one).  No reference counterpart: the
+ * reference projects per camera (src/tilesplat/projection.py:119-134). */
+#define TCGS_MAX_VIEWS_PER_PASS 8
+int tcgs_preprocess_views(const tcgs_scene *scene, const tcgs_camera *cams, int32_t n_views, const tcgs_opts *opts,
+                          void *const *ws, size_t ws_bytes, int64_t max_splats, void *stream);
+
 /* K2-K6: depth-rank sort, duplicate-with-keys, tile radix sort, tile ranges
  * (replaces build_tiles, src/tilesplat/tiling.py:46-59). */
 int tcgs_bin(int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes,

@@ -54,10 +54,14 @@ class Stats(ctypes.Structure):
 # name -> (restype, argtypes); every symbol include/tcgs.h declares
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
+MAX_VIEWS_PER_PASS = 8  # TCGS_MAX_VIEWS_PER_PASS (include/tcgs.h)
+
 SIGNATURES = {
     "tcgs_workspace_size": (ctypes.c_size_t, [_I64, ctypes.c_int32, ctypes.c_int32, _I64]),
     "tcgs_preprocess": (ctypes.c_int, [ctypes.POINTER(Scene), ctypes.POINTER(Camera), ctypes.POINTER(Opts), _P,
                                        ctypes.c_size_t, _I64, _P]),
+    "tcgs_preprocess_views": (ctypes.c_int, [ctypes.POINTER(Scene), ctypes.POINTER(Camera), ctypes.c_int32,
+                                             ctypes.POINTER(Opts), ctypes.POINTER(_P), ctypes.c_size_t, _I64, _P]),
     "tcgs_bin": (ctypes.c_int, [_I64, ctypes.POINTER(Camera), ctypes.POINTER(Opts), _P, ctypes.c_size_t, _I64, _P]),
     "tcgs_blend": (ctypes.c_int, [_I64, ctypes.POINTER(Camera), ctypes.POINTER(Opts), _P, ctypes.c_size_t, _I64,
                                   _P, _P, _P, _P]),

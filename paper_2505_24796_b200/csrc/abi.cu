@@ -32,6 +32,27 @@ __global__ void init_counters(DevCounters *c) {
     *c = z;
 }
 
+struct CounterSet {
+    DevCounters *c[TCGS_MAX_VIEWS_PER_PASS];
+};
+__global__ void init_counters_views(const __grid_constant__ CounterSet s, int n) {
+    if ((int)threadIdx.x < n) {
+        DevCounters z;
+        memset(&z, 0, sizeof(z));
+        z.key_min = ~0ull;
+        *s.c[threadIdx.x] = z;
+    }
+}
+
+int check_scene(const tcgs_scene *scene) {
+    if (!scene) return fail(TCGS_ERR_INVALID_ARG, "null scene");
+    if (scene->sh_degree < -1 || scene->sh_degree > 3) return fail(TCGS_ERR_INVALID_ARG, "sh_degree must be -1..3");
+    if (scene->dtype != TCGS_F32 && scene->dtype != TCGS_F64) return fail(TCGS_ERR_INVALID_ARG, "dtype");
+    if (scene->P > 0 && (!scene->means || !scene->scales || !scene->rotations || !scene->opacities || !scene->features))
+        return fail(TCGS_ERR_INVALID_ARG, "null scene array");
+    return TCGS_OK;
+}
+
 int check_common(const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes, int64_t P,
                  int64_t max_splats) {
     if (!cam || !ws) return fail(TCGS_ERR_INVALID_ARG, "null camera or workspace");
@@ -95,19 +116,43 @@ size_t tcgs_workspace_size(int64_t P, int32_t width, int32_t height, int64_t max
 
 int tcgs_preprocess(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts *opts, void *ws,
                     size_t ws_bytes, int64_t max_splats, void *stream) {
-    if (!scene) return fail(TCGS_ERR_INVALID_ARG, "null scene");
-    int rc = check_common(cam, opts, ws, ws_bytes, scene->P, max_splats);
+    int rc = check_scene(scene);
     if (rc) return rc;
-    if (scene->sh_degree < -1 || scene->sh_degree > 3) return fail(TCGS_ERR_INVALID_ARG, "sh_degree must be -1..3");
-    if (scene->dtype != TCGS_F32 && scene->dtype != TCGS_F64) return fail(TCGS_ERR_INVALID_ARG, "dtype");
-    if (scene->P > 0 && (!scene->means || !scene->scales || !scene->rotations || !scene->opacities || !scene->features))
-        return fail(TCGS_ERR_INVALID_ARG, "null scene array");
+    rc = check_common(cam, opts, ws, ws_bytes, scene->P, max_splats);
+    if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     const Layout L = Layout::make(scene->P, cam->width, cam->height, max_splats);
     note_launch();
     init_counters<<<1, 1, 0, st>>>(at<DevCounters>(ws, L.counters));
     cudaError_t e = launch_preprocess(*scene, *cam, make_band(*cam, opts), opts ? opts->debug : 0, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "preprocess");
+    return TCGS_OK;
+}
+
+int tcgs_preprocess_views(const tcgs_scene *scene, const tcgs_camera *cams, int32_t n_views, const tcgs_opts *opts,
+                          void *const *ws, size_t ws_bytes, int64_t max_splats, void *stream) {
+    int rc = check_scene(scene);
+    if (rc) return rc;
+    if (!cams || !ws) return fail(TCGS_ERR_INVALID_ARG, "null cameras or workspaces");
+    if (n_views < 1 || n_views > TCGS_MAX_VIEWS_PER_PASS)
+        return fail(TCGS_ERR_INVALID_ARG, "n_views must be 1..TCGS_MAX_VIEWS_PER_PASS");
+    Layout L[TCGS_MAX_VIEWS_PER_PASS];
+    Band bands[TCGS_MAX_VIEWS_PER_PASS];
+    CounterSet cs;
+    for (int v = 0; v < n_views; v++) {
+        rc = check_common(&cams[v], opts, ws[v], ws_bytes, scene->P, max_splats);
+        if (rc) return rc;
+        for (int u = 0; u < v; u++)
+            if (ws[u] == ws[v]) return fail(TCGS_ERR_INVALID_ARG, "views need distinct workspaces");
+        L[v] = Layout::make(scene->P, cams[v].width, cams[v].height, max_splats);
+        bands[v] = make_band(cams[v], opts);
+        cs.c[v] = at<DevCounters>(ws[v], L[v].counters);
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    note_launch();
+    init_counters_views<<<1, 32, 0, st>>>(cs, n_views);
+    cudaError_t e = launch_preprocess_views(*scene, cams, bands, n_views, opts ? opts->debug : 0, ws, L, st);
+    if (e != cudaSuccess) return cuda_fail(e, "preprocess_views");
     return TCGS_OK;
 }
 

@@ -18,6 +18,10 @@
 
 #include "tcgs_internal.cuh"
 
+#ifndef TCGS_K1_THREADS
+#define TCGS_K1_THREADS 256  // Gaussians (threads) per CTA, fp32 scenes
+#endif
+
 namespace tcgs {
 
 namespace {
@@ -193,18 +197,32 @@ struct PreArgs {
     DevCounters *ctr;
 };
 
-template <typename T>
-__global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__restrict__ g_means,
+// Views of one pass: every view reads the same staged Gaussians (multi-view fused preprocess, SURVEY.md
+// §8(f) 2: the SH coefficients -- 192 B of the 236 B per Gaussian at SH3 -- are read once for NV cameras).
+template <int NV>
+struct PreViews {
+    PreArgs v[NV];
+    int n;
+};
+
+#ifndef TCGS_K1_VIEWS_MIN_CTAS
+#define TCGS_K1_VIEWS_MIN_CTAS 3  // multi-view pass: resident CTAs per SM the register allocation must allow
+#endif
+
+template <typename T, int NV>
+__global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) preprocess_kernel(const __grid_constant__ PreViews<NV> pv,
+                                                         const T *__restrict__ g_means,
                                                          const T *__restrict__ g_scales, const T *__restrict__ g_rots,
                                                          const T *__restrict__ g_opac, const T *__restrict__ g_feats) {
+    const PreArgs &a0 = pv.v[0];  // scene-level fields (P, sh_degree) are the same in every view
     extern __shared__ __align__(16) unsigned char pre_smem[];
     // two transaction barriers: geometry (means, scales, rotations, opacity) and features (RGB or SH), so the
     // features' bulk copy -- most of the bytes at SH3 -- lands while the float64 projection runs
     __shared__ __align__(8) unsigned long long bar[2];
     const int NT = blockDim.x;
     const int64_t base = (int64_t)blockIdx.x * NT;
-    const int n = (int)(a.P - base < NT ? a.P - base : NT);
-    const int F = a.sh_degree < 0 ? 3 : 3 * (a.sh_degree + 1) * (a.sh_degree + 1);  // features per Gaussian
+    const int n = (int)(a0.P - base < NT ? a0.P - base : NT);
+    const int F = a0.sh_degree < 0 ? 3 : 3 * (a0.sh_degree + 1) * (a0.sh_degree + 1);  // features per Gaussian
     // staged SoA segments, each 16-B aligned: means 3, scales 3, rotations 4, opacity 1, features F per Gaussian
     const int per[5] = {3, 3, 4, 1, F};
     const T *src[5] = {g_means, g_scales, g_rots, g_opac, g_feats};
@@ -260,214 +278,216 @@ __global__ void __launch_bounds__(256) preprocess_kernel(PreArgs a, const T *__r
     const int l = threadIdx.x;
     const T *means = seg[0], *scales = seg[1], *rots = seg[2], *opac = seg[3], *feats = seg[4];
     const int64_t i = base + l;
-    const bool in_range = i < a.P;
-    unsigned long long key = ~0ull;  // "touches nothing": rewritten by depth_key_fix
-    uint32_t touched = 0;
-    bool dropped = false;
-    if (in_range) {
-        const double *V = a.cam.view;
-        const double m0 = ld(means, 3 * l), m1 = ld(means, 3 * l + 1), m2 = ld(means, 3 * l + 2);
-        double t[3];
+    // covariance_of (src/tilesplat/scene.py:83-101): view-independent, computed once for every view of the pass
+    double w, x, y, z;
+    if (sizeof(T) == 4) {
+        const float4 q4 = reinterpret_cast<const float4 *>(rots)[l];
+        w = q4.x, x = q4.y, y = q4.z, z = q4.w;
+    } else {
+        w = ld(rots, 4 * l), x = ld(rots, 4 * l + 1), y = ld(rots, 4 * l + 2), z = ld(rots, 4 * l + 3);
+    }
+    const double r[3][3] = {
+        {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
+        {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
+        {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)},
+    };
+    const double s0 = ld(scales, 3 * l), s1 = ld(scales, 3 * l + 1), s2 = ld(scales, 3 * l + 2);
+    const double sq[3] = {s0 * s0, s1 * s1, s2 * s2};
+    double mm[3][3], c[3][3], cov[3][3];
 #pragma unroll
-        for (int k = 0; k < 3; k++) t[k] = dot3_gemv(V[4 * k + 0], V[4 * k + 1], V[4 * k + 2], m0, m1, m2) + V[4 * k + 3];
-        const double tz = t[2];
-        a.radius[i] = -1;
-        if (!(tz > a.cam.near_plane)) {  // src/tilesplat/projection.py:76-78 (tz <= near culls)
-            dropped = true;
-        } else {
-            const double fx = a.cam.fx, fy = a.cam.fy;
-            const double mx = fx * t[0] / tz + a.cam.cx;
-            const double my = fy * t[1] / tz + a.cam.cy;
-            const double jac[2][3] = {{fx / tz, 0.0, -fx * t[0] / (tz * tz)}, {0.0, fy / tz, -fy * t[1] / (tz * tz)}};
-            // covariance_of (src/tilesplat/scene.py:83-101)
-            double w, x, y, z;
-            if (sizeof(T) == 4) {
-                const float4 q4 = reinterpret_cast<const float4 *>(rots)[l];
-                w = q4.x, x = q4.y, y = q4.z, z = q4.w;
-            } else {
-                w = ld(rots, 4 * l), x = ld(rots, 4 * l + 1), y = ld(rots, 4 * l + 2), z = ld(rots, 4 * l + 3);
-            }
-            const double r[3][3] = {
-                {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)},
-                {2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)},
-                {2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)},
-            };
-            const double s0 = ld(scales, 3 * l), s1 = ld(scales, 3 * l + 1), s2 = ld(scales, 3 * l + 2);
-            const double sq[3] = {s0 * s0, s1 * s1, s2 * s2};
-            double mm[3][3], c[3][3], cov[3][3];
+    for (int p = 0; p < 3; p++)
 #pragma unroll
-            for (int p = 0; p < 3; p++)
+        for (int q = 0; q < 3; q++) mm[p][q] = r[p][q] * sq[q];
 #pragma unroll
-                for (int q = 0; q < 3; q++) mm[p][q] = r[p][q] * sq[q];
+    for (int p = 0; p < 3; p++)
 #pragma unroll
-            for (int p = 0; p < 3; p++)
+        for (int q = 0; q < 3; q++) c[p][q] = dot3_gemm(mm[p][0], mm[p][1], mm[p][2], r[q][0], r[q][1], r[q][2]);
 #pragma unroll
-                for (int q = 0; q < 3; q++) c[p][q] = dot3_gemm(mm[p][0], mm[p][1], mm[p][2], r[q][0], r[q][1], r[q][2]);
+    for (int p = 0; p < 3; p++)
 #pragma unroll
-            for (int p = 0; p < 3; p++)
+        for (int q = 0; q < 3; q++) cov[p][q] = (c[p][q] + c[q][p]) / 2.0;
+    const int nv = NV == 1 ? 1 : pv.n;
+    for (int vi = 0; vi < nv; vi++) {
+        const PreArgs &a = pv.v[vi];
+        const bool in_range = i < a.P;
+        unsigned long long key = ~0ull;  // "touches nothing": rewritten by depth_key_fix
+        uint32_t touched = 0;
+        bool dropped = false;
+        if (in_range) {
+            const double *V = a.cam.view;
+            const double m0 = ld(means, 3 * l), m1 = ld(means, 3 * l + 1), m2 = ld(means, 3 * l + 2);
+            double t[3];
 #pragma unroll
-                for (int q = 0; q < 3; q++) cov[p][q] = (c[p][q] + c[q][p]) / 2.0;
-            // sigma = (J W) Sigma (J W)^T  (src/tilesplat/projection.py:88-96)
-            double m[2][3], mc[2][3], sg[2][2];
-#pragma unroll
-            for (int p = 0; p < 2; p++)
-#pragma unroll
-                for (int q = 0; q < 3; q++) m[p][q] = dot3_gemm(jac[p][0], jac[p][1], jac[p][2], V[q], V[4 + q], V[8 + q]);
-#pragma unroll
-            for (int p = 0; p < 2; p++)
-#pragma unroll
-                for (int q = 0; q < 3; q++) mc[p][q] = dot3_gemm(m[p][0], m[p][1], m[p][2], cov[0][q], cov[1][q], cov[2][q]);
-#pragma unroll
-            for (int p = 0; p < 2; p++)
-#pragma unroll
-                for (int q = 0; q < 2; q++) sg[p][q] = dot3_gemm(mc[p][0], mc[p][1], mc[p][2], m[q][0], m[q][1], m[q][2]);
-            double sa = (sg[0][0] + sg[0][0]) / 2.0;
-            double sb = (sg[0][1] + sg[1][0]) / 2.0;
-            double sc = (sg[1][1] + sg[1][1]) / 2.0;
-            sa += 0.3;  // COV_DILATION, src/tilesplat/projection.py:14
-            sc += 0.3;
-            {  // _clamp_eigenvalues(sigma, 0.5), src/tilesplat/projection.py:45-65
-                const double mid = (sa + sc) / 2.0;
-                const double half = py_hypot((sa - sc) / 2.0, sb);
-                const double lo = mid - half, hi = mid + half;
-                if (!(lo >= 0.5)) {
-                    const double lo_c = lo > 0.5 ? lo : 0.5, hi_c = hi > 0.5 ? hi : 0.5;
-                    if (half == 0.0) {
-                        sa = lo_c;
-                        sb = 0.0;
-                        sc = lo_c;
-                    } else {
-                        double v0, v1;
-                        if (fabs(sb) > 1e-300) {
-                            v0 = sb;
-                            v1 = hi - sa;
-                        } else if (sa >= sc) {
-                            v0 = 1.0;
-                            v1 = 0.0;
-                        } else {
-                            v0 = 0.0;
-                            v1 = 1.0;
-                        }
-                        const double nrm = sqrt(fma(v1, v1, v0 * v0));
-                        v0 = v0 / nrm;
-                        v1 = v1 / nrm;
-                        const double u0 = -v1, u1 = v0;
-                        sa = hi_c * (v0 * v0) + lo_c * (u0 * u0);
-                        sb = hi_c * (v0 * v1) + lo_c * (u0 * u1);
-                        sc = hi_c * (v1 * v1) + lo_c * (u1 * u1);
-                    }
-                }
-            }
-            const double mid = (sa + sc) / 2.0;
-            const double lam_max = mid + py_hypot((sa - sc) / 2.0, sb);
-            const int32_t rad = (int32_t)ceil(3.0 * sqrt(lam_max));
-            const double det = sa * sc - sb * sb;
-            if (!(det > 0.0)) {  // invert_cov2 raises -> project returns None (projection.py:104-107)
+            for (int k = 0; k < 3; k++) t[k] = dot3_gemv(V[4 * k + 0], V[4 * k + 1], V[4 * k + 2], m0, m1, m2) + V[4 * k + 3];
+            const double tz = t[2];
+            a.radius[i] = -1;
+            if (!(tz > a.cam.near_plane)) {  // src/tilesplat/projection.py:76-78 (tz <= near culls)
                 dropped = true;
             } else {
-                const double s11 = sc / det, s12 = -sb / det, s22 = sa / det;
-                a.radius[i] = rad;
-                if (a.debug) {
-                    a.dbg_conic[3 * i] = s11;
-                    a.dbg_conic[3 * i + 1] = s12;
-                    a.dbg_conic[3 * i + 2] = s22;
-                    a.dbg_depth[i] = tz;
-                    a.dbg_mean2d[2 * i] = mx;
-                    a.dbg_mean2d[2 * i + 1] = my;
-                }
-                // covered_tiles (src/tilesplat/tiling.py:34-43), clipped to the grid.  The rectangle is
-                // band-agnostic (binning clips it to a tile-row band), so one K1 serves every band choice.
-                double fx0 = floor((mx - rad) / TILE), fx1 = floor((mx + rad) / TILE);
-                double fy0 = floor((my - rad) / TILE), fy1 = floor((my + rad) / TILE);
-                fx0 = fmax(fx0, 0.0);
-                fy0 = fmax(fy0, 0.0);
-                fx1 = fmin(fx1, (double)(a.tiles_x - 1));
-                fy1 = fmin(fy1, (double)(a.tiles_y - 1));
-                if (fx0 <= fx1 && fy0 <= fy1) {
-                    const int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
-                    touched = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
-                    a.rect[i] = make_short4((short)x0, (short)y0, (short)x1, (short)y1);
-                    key = (unsigned long long)__double_as_longlong(tz);  // tz > 0: bit order == value order
-                    Rec rc;
-                    rc.mx = (float)mx;
-                    rc.mx_lo = (float)(mx - (double)rc.mx);
-                    rc.my = (float)my;
-                    rc.my_lo = (float)(my - (double)rc.my);
-                    rc.s11 = (float)s11;
-                    rc.s12 = (float)s12;
-                    rc.s22 = (float)s22;
-                    const double o = ld(opac, l);
-                    rc.ln_o = logf((float)o);
-                    rc.opacity = (float)o;
-                    float col[3];
-                    wait_bar(1);  // features staged (usually long done: they streamed in during the projection)
-                    if (a.sh_degree < 0) {
-                        col[0] = (float)ld(feats, 3 * l);
-                        col[1] = (float)ld(feats, 3 * l + 1);
-                        col[2] = (float)ld(feats, 3 * l + 2);
-                    } else {
-                        const int K = (a.sh_degree + 1) * (a.sh_degree + 1);
-                        const double dx = m0 - a.campos[0], dy = m1 - a.campos[1], dz = m2 - a.campos[2];
-                        const double nn = sqrt(dx * dx + dy * dy + dz * dz);
-                        sh_color(feats + (size_t)l * K * 3, a.sh_degree, dx / nn, dy / nn, dz / nn, col);
+                const double fx = a.cam.fx, fy = a.cam.fy;
+                const double mx = fx * t[0] / tz + a.cam.cx;
+                const double my = fy * t[1] / tz + a.cam.cy;
+                const double jac[2][3] = {{fx / tz, 0.0, -fx * t[0] / (tz * tz)}, {0.0, fy / tz, -fy * t[1] / (tz * tz)}};
+                // sigma = (J W) Sigma (J W)^T  (src/tilesplat/projection.py:88-96)
+                double m[2][3], mc[2][3], sg[2][2];
+#pragma unroll
+                for (int p = 0; p < 2; p++)
+#pragma unroll
+                    for (int q = 0; q < 3; q++) m[p][q] = dot3_gemm(jac[p][0], jac[p][1], jac[p][2], V[q], V[4 + q], V[8 + q]);
+#pragma unroll
+                for (int p = 0; p < 2; p++)
+#pragma unroll
+                    for (int q = 0; q < 3; q++) mc[p][q] = dot3_gemm(m[p][0], m[p][1], m[p][2], cov[0][q], cov[1][q], cov[2][q]);
+#pragma unroll
+                for (int p = 0; p < 2; p++)
+#pragma unroll
+                    for (int q = 0; q < 2; q++) sg[p][q] = dot3_gemm(mc[p][0], mc[p][1], mc[p][2], m[q][0], m[q][1], m[q][2]);
+                double sa = (sg[0][0] + sg[0][0]) / 2.0;
+                double sb = (sg[0][1] + sg[1][0]) / 2.0;
+                double sc = (sg[1][1] + sg[1][1]) / 2.0;
+                sa += 0.3;  // COV_DILATION, src/tilesplat/projection.py:14
+                sc += 0.3;
+                {  // _clamp_eigenvalues(sigma, 0.5), src/tilesplat/projection.py:45-65
+                    const double mid = (sa + sc) / 2.0;
+                    const double half = py_hypot((sa - sc) / 2.0, sb);
+                    const double lo = mid - half, hi = mid + half;
+                    if (!(lo >= 0.5)) {
+                        const double lo_c = lo > 0.5 ? lo : 0.5, hi_c = hi > 0.5 ? hi : 0.5;
+                        if (half == 0.0) {
+                            sa = lo_c;
+                            sb = 0.0;
+                            sc = lo_c;
+                        } else {
+                            double v0, v1;
+                            if (fabs(sb) > 1e-300) {
+                                v0 = sb;
+                                v1 = hi - sa;
+                            } else if (sa >= sc) {
+                                v0 = 1.0;
+                                v1 = 0.0;
+                            } else {
+                                v0 = 0.0;
+                                v1 = 1.0;
+                            }
+                            const double nrm = sqrt(fma(v1, v1, v0 * v0));
+                            v0 = v0 / nrm;
+                            v1 = v1 / nrm;
+                            const double u0 = -v1, u1 = v0;
+                            sa = hi_c * (v0 * v0) + lo_c * (u0 * u0);
+                            sb = hi_c * (v0 * v1) + lo_c * (u0 * u1);
+                            sc = hi_c * (v1 * v1) + lo_c * (u1 * u1);
+                        }
                     }
-                    rc.r = col[0];
-                    rc.g = col[1];
-                    rc.b = col[2];
-                    a.rec[i] = rc;
+                }
+                const double mid = (sa + sc) / 2.0;
+                const double lam_max = mid + py_hypot((sa - sc) / 2.0, sb);
+                const int32_t rad = (int32_t)ceil(3.0 * sqrt(lam_max));
+                const double det = sa * sc - sb * sb;
+                if (!(det > 0.0)) {  // invert_cov2 raises -> project returns None (projection.py:104-107)
+                    dropped = true;
+                } else {
+                    const double s11 = sc / det, s12 = -sb / det, s22 = sa / det;
+                    a.radius[i] = rad;
+                    if (a.debug) {
+                        a.dbg_conic[3 * i] = s11;
+                        a.dbg_conic[3 * i + 1] = s12;
+                        a.dbg_conic[3 * i + 2] = s22;
+                        a.dbg_depth[i] = tz;
+                        a.dbg_mean2d[2 * i] = mx;
+                        a.dbg_mean2d[2 * i + 1] = my;
+                    }
+                    // covered_tiles (src/tilesplat/tiling.py:34-43), clipped to the grid.  The rectangle is
+                    // band-agnostic (binning clips it to a tile-row band), so one K1 serves every band choice.
+                    double fx0 = floor((mx - rad) / TILE), fx1 = floor((mx + rad) / TILE);
+                    double fy0 = floor((my - rad) / TILE), fy1 = floor((my + rad) / TILE);
+                    fx0 = fmax(fx0, 0.0);
+                    fy0 = fmax(fy0, 0.0);
+                    fx1 = fmin(fx1, (double)(a.tiles_x - 1));
+                    fy1 = fmin(fy1, (double)(a.tiles_y - 1));
+                    if (fx0 <= fx1 && fy0 <= fy1) {
+                        const int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
+                        touched = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
+                        a.rect[i] = make_short4((short)x0, (short)y0, (short)x1, (short)y1);
+                        key = (unsigned long long)__double_as_longlong(tz);  // tz > 0: bit order == value order
+                        Rec rc;
+                        rc.mx = (float)mx;
+                        rc.mx_lo = (float)(mx - (double)rc.mx);
+                        rc.my = (float)my;
+                        rc.my_lo = (float)(my - (double)rc.my);
+                        rc.s11 = (float)s11;
+                        rc.s12 = (float)s12;
+                        rc.s22 = (float)s22;
+                        const double o = ld(opac, l);
+                        rc.ln_o = logf((float)o);
+                        rc.opacity = (float)o;
+                        float col[3];
+                        wait_bar(1);  // features staged (usually long done: they streamed in during the projection)
+                        if (a.sh_degree < 0) {
+                            col[0] = (float)ld(feats, 3 * l);
+                            col[1] = (float)ld(feats, 3 * l + 1);
+                            col[2] = (float)ld(feats, 3 * l + 2);
+                        } else {
+                            const int K = (a.sh_degree + 1) * (a.sh_degree + 1);
+                            const double dx = m0 - a.campos[0], dy = m1 - a.campos[1], dz = m2 - a.campos[2];
+                            const double nn = sqrt(dx * dx + dy * dy + dz * dz);
+                            sh_color(feats + (size_t)l * K * 3, a.sh_degree, dx / nn, dy / nn, dz / nn, col);
+                        }
+                        rc.r = col[0];
+                        rc.g = col[1];
+                        rc.b = col[2];
+                        a.rec[i] = rc;
+                    }
                 }
             }
+            a.touched[i] = touched;
+            a.keys[i] = key;
         }
-        a.touched[i] = touched;
-        a.keys[i] = key;
-    }
-    // warp-aggregated counters
-    const unsigned full = 0xffffffffu;
-    const unsigned n_drop = __popc(__ballot_sync(full, dropped));
-    const unsigned n_vis = __popc(__ballot_sync(full, touched > 0));
-    unsigned long long kmin = touched > 0 ? key : ~0ull, kmax = touched > 0 ? key : 0ull;
+        // warp-aggregated counters
+        const unsigned full = 0xffffffffu;
+        const unsigned n_drop = __popc(__ballot_sync(full, dropped));
+        const unsigned n_vis = __popc(__ballot_sync(full, touched > 0));
+        unsigned long long kmin = touched > 0 ? key : ~0ull, kmax = touched > 0 ? key : 0ull;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long omin = __shfl_xor_sync(full, kmin, o), omax = __shfl_xor_sync(full, kmax, o);
-        kmin = omin < kmin ? omin : kmin;
-        kmax = omax > kmax ? omax : kmax;
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (n_drop) atomicAdd(&a.ctr->dropped, (unsigned long long)n_drop);
-        if (n_vis) {
-            atomicAdd(&a.ctr->n_visible, (unsigned long long)n_vis);
-            atomicMin(&a.ctr->key_min, kmin);
-            atomicMax(&a.ctr->key_max, kmax);
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long omin = __shfl_xor_sync(full, kmin, o), omax = __shfl_xor_sync(full, kmax, o);
+            kmin = omin < kmin ? omin : kmin;
+            kmax = omax > kmax ? omax : kmax;
         }
-    }
+        if ((threadIdx.x & 31) == 0) {
+            if (n_drop) atomicAdd(&a.ctr->dropped, (unsigned long long)n_drop);
+            if (n_vis) {
+                atomicAdd(&a.ctr->n_visible, (unsigned long long)n_vis);
+                atomicMin(&a.ctr->key_min, kmin);
+                atomicMax(&a.ctr->key_max, kmax);
+            }
+        }
+    }  // views
     wait_bar(1);  // no CTA may retire with a bulk copy into its shared memory still in flight
 }
 
 
-template <typename T>
-cudaError_t launch_k1(const PreArgs &a, const tcgs_scene &scene, int F, int nt, cudaStream_t st) {
+template <typename T, int NV>
+cudaError_t launch_k1(const PreViews<NV> &pv, const tcgs_scene &scene, int F, int nt, cudaStream_t st) {
     size_t smem = 0;
     for (int per : {3, 3, 4, 1, F}) smem += ((size_t)per * nt * sizeof(T) + 15) / 16 * 16;
     static size_t configured_dev[TCGS_MAX_DEVICES] = {};
     size_t &configured = configured_dev[current_device()];
     if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(preprocess_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(preprocess_kernel<T, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
         configured = smem;
     }
     const unsigned blocks = (unsigned)((scene.P + nt - 1) / nt);
     note_launch();
-    preprocess_kernel<T><<<blocks, nt, smem, st>>>(a, (const T *)scene.means, (const T *)scene.scales,
-                                                  (const T *)scene.rotations, (const T *)scene.opacities,
-                                                  (const T *)scene.features);
+    preprocess_kernel<T, NV><<<blocks, nt, smem, st>>>(pv, (const T *)scene.means, (const T *)scene.scales,
+                                                      (const T *)scene.rotations, (const T *)scene.opacities,
+                                                      (const T *)scene.features);
     return cudaGetLastError();
 }
 
-}  // namespace
-
-cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug,
-                              void *ws, const Layout &L, cudaStream_t st) {
+PreArgs view_args(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug, void *ws,
+                  const Layout &L) {
     PreArgs a;
     a.cam = cam;
     const double *V = cam.view;
@@ -489,11 +509,33 @@ cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, c
     a.dbg_depth = at<double>(ws, L.dbg_depth);
     a.dbg_mean2d = at<double>(ws, L.dbg_mean2d);
     a.ctr = at<DevCounters>(ws, L.counters);
+    return a;
+}
+
+template <int NV>
+cudaError_t launch_views(const PreViews<NV> &pv, const tcgs_scene &scene, cudaStream_t st) {
     if (scene.P <= 0) return cudaSuccess;
     const int F = scene.sh_degree < 0 ? 3 : 3 * (scene.sh_degree + 1) * (scene.sh_degree + 1);
-    if (scene.dtype == TCGS_F64) return launch_k1<double>(a, scene, F, 128, st);
-    return launch_k1<float>(a, scene, F, 256, st);
-    return cudaGetLastError();
+    if (scene.dtype == TCGS_F64) return launch_k1<double, NV>(pv, scene, F, 128, st);
+    return launch_k1<float, NV>(pv, scene, F, TCGS_K1_THREADS, st);
+}
+
+}  // namespace
+
+cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug,
+                              void *ws, const Layout &L, cudaStream_t st) {
+    PreViews<1> pv;
+    pv.v[0] = view_args(scene, cam, band, debug, ws, L);
+    pv.n = 1;
+    return launch_views(pv, scene, st);
+}
+
+cudaError_t launch_preprocess_views(const tcgs_scene &scene, const tcgs_camera *cams, const Band *bands, int n_views,
+                                    int debug, void *const *ws, const Layout *L, cudaStream_t st) {
+    PreViews<TCGS_MAX_VIEWS_PER_PASS> pv;
+    for (int v = 0; v < n_views; v++) pv.v[v] = view_args(scene, cams[v], bands[v], debug, ws[v], L[v]);
+    pv.n = n_views;
+    return launch_views(pv, scene, st);
 }
 
 }  // namespace tcgs

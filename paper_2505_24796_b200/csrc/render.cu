@@ -164,6 +164,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
         : "r"(taddr));
 }
+template <int G>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&v)[G]);
+template <>
+__device__ __forceinline__ void tmem_ld<16>(uint32_t taddr, uint32_t (&v)[16]) {
+    tmem_ld16(taddr, v);
+}
+template <>
+__device__ __forceinline__ void tmem_ld<8>(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Gaussian coefficients for one tile (gaussian_vector, src/tilesplat/tensor_path.py:25-40) relative to the
@@ -178,9 +190,10 @@ __device__ __forceinline__ bool gaussian_coeffs(const Rec &r, float ox, float oy
     const float s11 = r.s11, s12 = r.s12, s22 = r.s22;
     const float q = s11 * dx * dx + 2.0f * s12 * dx * dy + s22 * dy * dy;
     const bool outside = !(dx >= -8.0f && dx <= 7.0f && dy >= -8.0f && dy <= 7.0f);
-    if (outside && s11 > 0.0f && s22 > 0.0f) {
-        // (the minimiser only needs to be accurate to first order: q is flat there, and the test keeps a margin)
-        const float r11 = __fdividef(s12, s11), r22 = __fdividef(s12, s22);
+    if (outside && s11 > 1e-30f && s22 > 1e-30f) {
+        // (the minimiser only needs to be accurate to first order: q is flat there, and the test keeps a margin;
+        // the normal-range guard above lets the reciprocal skip denormal handling)
+        const float r11 = s12 * rcp_approx(s11), r22 = s12 * rcp_approx(s22);
         // The unconstrained minimiser d lies outside the box, so the box minimum lies on a face the segment
         // from any box point to d crosses: the face x = clamp(dx) if dx is outside [-8, 7], the face
         // y = clamp(dy) if dy is.  Evaluating the two clamped lines always is safe: a line through the box
@@ -328,6 +341,14 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
         const uint32_t id_nx2 = list_id(nx2);
 
         // evaluate this chunk (registers only)
+#ifdef TCGS_K7_SLOWPROD  // sensitivity experiment: extra dependent work per producer chunk
+        {
+            float z = (float)lane;
+#pragma unroll
+            for (int q = 0; q < TCGS_K7_SLOWPROD; q++) asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(z));
+            if (z == 12345.0f) sm.c_dead = 0;
+        }
+#endif
         const bool valid = cur.c * 32 + lane < cur.n;
         float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool live = false;
@@ -465,17 +486,33 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
     constexpr bool TC = MODE != TCGS_ALPHA_FFMA;
     const unsigned FULL = 0xffffffffu;
 
-    // pixel owned by a consumer thread: warp w covers an 8x4 block (compact footprints per warp)
-    const int lx = 8 * (warp & 1) + (lane & 7);
-    const int ly = 4 * ((warp >> 1) & 3) + (lane >> 3);
-    const float ux = (float)(lx - 8), uy = (float)(ly - 8);
-    const int half = (warp >> 2) & 1;         // which M=128 MMA (TMEM column block) holds this pixel
-    const int urow = 32 * (warp & 3) + lane;  // TMEM lane == U row within the half
+    // pixels owned by a consumer thread.  NPIX = 1: warp w covers an 8x4 block, TMEM lanes 32(w%4).. of
+    // pixel half w/4.  NPIX = 2: warp w covers an 8x8 block as horizontal pixel pairs; pixel h of a thread
+    // is row 32w + lane of pixel half h, so one thread reads both halves of its TMEM lane.
+    constexpr int NPIX = K7_PIX;
+    int lx[NPIX], ly[NPIX], hf[NPIX];
+#pragma unroll
+    for (int h = 0; h < NPIX; h++) {
+        if (NPIX == 1) {
+            lx[h] = 8 * (warp & 1) + (lane & 7);
+            ly[h] = 4 * ((warp >> 1) & 3) + (lane >> 3);
+            hf[h] = (warp >> 2) & 1;
+        } else {
+            lx[h] = 8 * (warp & 1) + 2 * (lane & 3) + h;
+            ly[h] = 8 * ((warp >> 1) & 1) + (lane >> 2);
+            hf[h] = h;
+        }
+    }
+    const int urow = 32 * (warp & 3) + lane;  // TMEM lane == U row within a half
 
     if (warp < K7_CONSUMER_WARPS && TC) {
-        const float u[16] = {1.f, 1.f, 1.f, ux, uy, ux * ux, ux * uy, uy * uy, ux, uy, ux * ux, ux * uy, uy * uy, 1.f, 0.f, 0.f};
 #pragma unroll
-        for (int k = 0; k < 16; k++) sm.U[half][kmaj_off(urow, k)] = __float2half_rn(u[k]);
+        for (int h = 0; h < NPIX; h++) {
+            const float ux = (float)(lx[h] - 8), uy = (float)(ly[h] - 8);
+            const float u[16] = {1.f, 1.f, 1.f, ux, uy, ux * ux, ux * uy, uy * uy, ux, uy, ux * ux, ux * uy, uy * uy, 1.f, 0.f, 0.f};
+#pragma unroll
+            for (int k = 0; k < 16; k++) sm.U[hf[h]][kmaj_off(urow, k)] = __float2half_rn(u[k]);
+        }
         fence_async_smem();
     }
     if (tid == 0) {
@@ -510,32 +547,48 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
         producer<MODE>(sm, a, ids, tmem, warp - K7_CONSUMER_WARPS);
     } else {
         int cur_seq = -1, cur_tile = -1;
-        int px = 0, py = 0;
-        bool inside = false, done = true, term = false, warp_done = true;
-        float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
-        uint32_t cull = 0, n_total = 0;
-        float fcnt = 0.0f;  // blends of this pixel (exact in fp32; kept on the FMA pipe)
+        int px[NPIX], py[NPIX];
+        bool inside[NPIX], done[NPIX], term[NPIX];
+        float T[NPIX], c0[NPIX], c1[NPIX], c2[NPIX];
+        uint32_t cull[NPIX];
+        float fcnt[NPIX];  // blends of this pixel (exact in fp32; kept on the FMA pipe)
+        bool warp_done = true;
+        uint32_t n_total = 0;
+#pragma unroll
+        for (int h = 0; h < NPIX; h++) {
+            px[h] = py[h] = 0;
+            inside[h] = term[h] = false;
+            done[h] = true;
+            T[h] = 1.0f;
+            c0[h] = c1[h] = c2[h] = fcnt[h] = 0.0f;
+            cull[h] = 0;
+        }
 #ifdef TCGS_K7_PROFILE  // experiment builds only: per-warp work (stages entered, relevant columns) replaces T / n_contrib
         int prof_rel = 0, prof_st = 0;
 #endif
         auto flush = [&]() {
+#pragma unroll
+            for (int h = 0; h < NPIX; h++) {
 #ifdef TCGS_K7_PROFILE
-            T = (float)prof_st;
-            fcnt = (float)prof_rel;
+                T[h] = (float)prof_st;
+                fcnt[h] = (float)prof_rel;
+#endif
+                if (inside[h]) {
+                    const int64_t p = (int64_t)py[h] * a.width + px[h];
+                    a.rgb[3 * p] = c0[h];
+                    a.rgb[3 * p + 1] = c1[h];
+                    a.rgb[3 * p + 2] = c2[h];
+                    a.T[p] = T[h];
+                    a.n_contrib[p] = (int32_t)fcnt[h];
+                    s_pairs += n_total;
+                }
+                s_blend += (uint32_t)fcnt[h];
+                s_cull += cull[h];
+                s_term += term[h] ? 1u : 0u;
+            }
+#ifdef TCGS_K7_PROFILE
             prof_rel = prof_st = 0;
 #endif
-            if (inside) {
-                const int64_t p = (int64_t)py * a.width + px;
-                a.rgb[3 * p] = c0;
-                a.rgb[3 * p + 1] = c1;
-                a.rgb[3 * p + 2] = c2;
-                a.T[p] = T;
-                a.n_contrib[p] = (int32_t)fcnt;
-                s_pairs += n_total;
-            }
-            s_blend += (uint32_t)fcnt;
-            s_cull += cull;
-            s_term += term ? 1u : 0u;
         };
         for (int k = 0;; k++) {
             const int st = k % S, b = k % NB;
@@ -547,17 +600,22 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 cur_seq = m.seq;
                 cur_tile = m.tile;
                 const int tx = cur_tile % a.tiles_x, ty = a.band_y0 + cur_tile / a.tiles_x;
-                px = tx * TILE + lx;
-                py = ty * TILE + ly;
-                inside = px < a.width && py < a.height;
-                done = !inside;
-                term = false;
-                T = 1.0f;
-                c0 = c1 = c2 = 0.0f;
-                cull = 0;
-                fcnt = 0.0f;
+                bool all_done = true;
+#pragma unroll
+                for (int h = 0; h < NPIX; h++) {
+                    px[h] = tx * TILE + lx[h];
+                    py[h] = ty * TILE + ly[h];
+                    inside[h] = px[h] < a.width && py[h] < a.height;
+                    done[h] = !inside[h];
+                    all_done = all_done && done[h];
+                    term[h] = false;
+                    T[h] = 1.0f;
+                    c0[h] = c1[h] = c2[h] = 0.0f;
+                    cull[h] = 0;
+                    fcnt[h] = 0.0f;
+                }
                 n_total = m.n_total;
-                warp_done = __all_sync(FULL, done);
+                warp_done = __all_sync(FULL, all_done);
                 if (warp_done && lane == 0) atomicAdd(&sm.retire[cur_seq & 7], 1);
             }
             if (TC) {
@@ -570,82 +628,123 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 prof_st++;
 #endif
                 const int nl = m.n_live;
-                const bool live0 = !done;
-                const uint32_t tb = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (2 * K7_BATCH) + half * K7_BATCH;
-                int jt = K7_BATCH;
-                // pass threshold of beta: the EarlyCull cut while the pixel is live, +inf once it has
-                // terminated (a float, so the test stays one FSETP and the update a predicated move)
-                const float cut0 = CUT_LOG2;
-                float thr = done ? __int_as_float(0x7f800000) : cut0;
-                const float fcnt0 = fcnt;
-                // one column of the stage: this pixel passes EarlyCull iff beta >= thr (thr = the cut while live,
+                bool live0[NPIX];
+                int jt[NPIX];
+                float thr[NPIX], fcnt0[NPIX];
+                uint32_t tb[NPIX];
+#pragma unroll
+                for (int h = 0; h < NPIX; h++) {
+                    live0[h] = !done[h];
+                    jt[h] = K7_BATCH;
+                    // pass threshold of beta: the EarlyCull cut while the pixel is live, +inf once it has
+                    // terminated (a float, so the test stays one FSETP and the update a predicated move)
+                    thr[h] = done[h] ? __int_as_float(0x7f800000) : CUT_LOG2;
+                    fcnt0[h] = fcnt[h];
+                    tb[h] = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (2 * K7_BATCH) + hf[h] * K7_BATCH;
+                }
+                // one column of the stage: a pixel passes EarlyCull iff beta >= thr (thr = the cut while live,
                 // +inf once done); a warp vote skips the column when no pixel of the warp passes (uniform branch)
-                auto column = [&](uint32_t rb, int col) {
-                    const float bb = __uint_as_float(rb);
-                    const bool p = bb >= thr;  // (columns >= n_live hold beta = -65504: never pass)
-                    if (__any_sync(FULL, p)) {
+                auto column = [&](const uint32_t (&rb)[NPIX], int col) {
+                    bool p[NPIX], any = false;
+#pragma unroll
+                    for (int h = 0; h < NPIX; h++) {
+                        p[h] = __uint_as_float(rb[h]) >= thr[h];  // (columns >= n_live hold beta = -65504: never pass)
+                        any = any || p[h];
+                    }
+                    if (__any_sync(FULL, any)) {
 #ifdef TCGS_K7_PROFILE
                         prof_rel++;
 #endif
-                        // alpha = 2^beta' (no min(alpha, 1): alpha > 1 only by rounding, and then
-                        // T - alpha T < 1e-4 terminates exactly as alpha = 1 would)
-                        const float al = ex2_approx(bb);
-                        const float tn = fmaf(-al, T, T);
-                        if (p && tn < TERM_T) {  // termination precedes compositing
-                            jt = col;
-                            thr = __int_as_float(0x7f800000);
-                        }
-                        if (p && tn >= TERM_T) {
-                            const float4 cc = sm.col[st][col];
-                            const float w = al * T;
-                            c0 = fmaf(w, cc.x, c0);
-                            c1 = fmaf(w, cc.y, c1);
-                            c2 = fmaf(w, cc.z, c2);
-                            T = tn;
-                            fcnt += 1.0f;
+                        const float4 cc = sm.col[st][col];
+#pragma unroll
+                        for (int h = 0; h < NPIX; h++) {
+                            // alpha = 2^beta' (no min(alpha, 1): alpha > 1 only by rounding, and then
+                            // T - alpha T < 1e-4 terminates exactly as alpha = 1 would)
+                            const float al = ex2_approx(__uint_as_float(rb[h]));
+                            const float tn = fmaf(-al, T[h], T[h]);
+                            if (p[h] && tn < TERM_T) {  // termination precedes compositing
+                                jt[h] = col;
+                                thr[h] = __int_as_float(0x7f800000);
+                            }
+                            if (p[h] && tn >= TERM_T) {
+                                const float w = al * T[h];
+                                c0[h] = fmaf(w, cc.x, c0[h]);
+                                c1[h] = fmaf(w, cc.y, c1[h]);
+                                c2[h] = fmaf(w, cc.z, c2[h]);
+                                T[h] = tn;
+                                fcnt[h] += 1.0f;
+                            }
                         }
                     }
                 };
-                {
+                constexpr int G = NPIX == 1 ? 16 : 8;  // columns per TMEM load group (registers: G x NPIX betas)
 #pragma unroll
-                    for (int hc = 0; hc < K7_BATCH / 16; hc++) {  // 16-column groups: 16 betas live in registers
-                        uint32_t r[16];
-                        if (TC) {
-                            tmem_ld16(tb + 16 * hc, r);
-                            tmem_wait_ld();
+                for (int hc = 0; hc < K7_BATCH / G; hc++) {
+                    uint32_t r[NPIX][G];
+                    if (TC) {
 #pragma unroll
-                            for (int j = 0; j < 16; j++) asm volatile("" : "+r"(r[j]));
-                            if (NB == 1 && hc == K7_BATCH / 16 - 1) {  // single accumulator: free it for the next MMA
-                                tc_fence_before();
-                                __syncwarp();
-                                if (lane == 0) mbar_arrive(&sm.tmem_empty[b]);
-                                tmem_released = true;
-                            }
-                        } else {
+                        for (int h = 0; h < NPIX; h++) tmem_ld<G>(tb[h] + G * hc, r[h]);
+                        tmem_wait_ld();
 #pragma unroll
-                            for (int j = 0; j < 16; j++) {
-                                const float4 p0 = sm.vf[st][16 * hc + j][0], p1 = sm.vf[st][16 * hc + j][1];
-                                r[j] = __float_as_uint(p0.x + p0.y * ux + p0.z * uy + p0.w * ux * ux + p1.x * ux * uy +
-                                                       p1.y * uy * uy);
+                        for (int h = 0; h < NPIX; h++)
+#pragma unroll
+                            for (int j = 0; j < G; j++) asm volatile("" : "+r"(r[h][j]));
+                        if (NB == 1 && hc == K7_BATCH / G - 1) {  // single accumulator: free it for the next MMA
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&sm.tmem_empty[b]);
+                            tmem_released = true;
+                        }
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < NPIX; h++) {
+                            const float ux = (float)(lx[h] - 8), uy = (float)(ly[h] - 8);
+#pragma unroll
+                            for (int j = 0; j < G; j++) {
+                                const float4 p0 = sm.vf[st][G * hc + j][0], p1 = sm.vf[st][G * hc + j][1];
+                                r[h][j] = __float_as_uint(p0.x + p0.y * ux + p0.z * uy + p0.w * ux * ux + p1.x * ux * uy +
+                                                          p1.y * uy * uy);
                             }
                         }
+                    }
 #pragma unroll
-                        for (int j = 0; j < 16; j++) column(r[j], 16 * hc + j);
+                    for (int j = 0; j < G; j++) {
+                        uint32_t rj[NPIX];
+#pragma unroll
+                        for (int h = 0; h < NPIX; h++) rj[h] = r[h][j];
+                        column(rj, G * hc + j);
                     }
                 }
-                const bool tstage = jt < K7_BATCH;
-                term = term || tstage;
-                done = done || tstage;
-                // EarlyCull counts: valid columns before the termination that did not blend, plus the dead
-                // Gaussians of the list before the terminating one
-                if (live0) cull += (uint32_t)(tstage ? jt : nl) - (uint32_t)(fcnt - fcnt0);
-                if (tstage) cull += sm.dead_before[st][jt];
-                if (__all_sync(FULL, done)) {
+#ifdef TCGS_K7_SLOWCONS  // sensitivity experiment: extra dependent work per consumer warp-stage
+                {
+                    float z = (float)lane;
+#pragma unroll
+                    for (int q = 0; q < TCGS_K7_SLOWCONS; q++) asm volatile("fma.rn.f32 %0, %0, %0, %0;" : "+f"(z));
+                    if (z == 12345.0f) cull[0] += 1;
+                }
+#endif
+                bool all_done = true;
+#pragma unroll
+                for (int h = 0; h < NPIX; h++) {
+                    const bool tstage = jt[h] < K7_BATCH;
+                    term[h] = term[h] || tstage;
+                    done[h] = done[h] || tstage;
+                    all_done = all_done && done[h];
+                    // EarlyCull counts: valid columns before the termination that did not blend, plus the dead
+                    // Gaussians of the list before the terminating one
+                    if (live0[h]) cull[h] += (uint32_t)(tstage ? jt[h] : nl) - (uint32_t)(fcnt[h] - fcnt0[h]);
+                    if (tstage) cull[h] += sm.dead_before[st][jt[h]];
+                }
+                if (__all_sync(FULL, all_done)) {
                     warp_done = true;
                     if (lane == 0) atomicAdd(&sm.retire[cur_seq & 7], 1);
                 }
             }
-            if (m.last && !done) cull += m.dead_total;  // list exhausted: every dead Gaussian was a cull
+            if (m.last) {
+#pragma unroll
+                for (int h = 0; h < NPIX; h++)
+                    if (!done[h]) cull[h] += m.dead_total;  // list exhausted: every dead Gaussian was a cull
+            }
             if (TC && !tmem_released) tc_fence_before();
             __syncwarp();
             if (lane == 0) {

@@ -21,7 +21,11 @@ constexpr int TILE_MAX_PASSES = 4;    // tile key: <= 32 bits
 constexpr int DUP_ITEMS = 1024;       // Gaussians per duplicate-with-keys CTA
 constexpr int DUP_THREADS = 256;
 
-constexpr int K7_CONSUMER_WARPS = 8;  // one pixel per thread, 16x16 tile
+#ifndef TCGS_K7_PIX
+#define TCGS_K7_PIX 1
+#endif
+constexpr int K7_PIX = TCGS_K7_PIX;              // pixels per consumer thread (1 or 2)
+constexpr int K7_CONSUMER_WARPS = 8 / K7_PIX;  // 256 pixels of a 16x16 tile
 constexpr int K7_PRODUCERS = 2;       // producer warps (alternate 32-entry chunks, token-ordered compaction)
 constexpr int K7_THREADS = 32 * (K7_CONSUMER_WARPS + K7_PRODUCERS);
 #ifndef TCGS_K7_BATCH
@@ -38,7 +42,7 @@ constexpr int K7_STAGES = TCGS_K7_STAGES;  // shared-memory B-operand stages
 constexpr int K7_TMEM_BUFS = TCGS_K7_TMEM_BUFS;  // TMEM accumulator buffers (1: released after the last load)
 constexpr int K7_TMEM_COLS = K7_TMEM_BUFS * 2 * K7_BATCH;  // buffers x pixel halves x N
 #ifndef TCGS_K7_CTAS
-#define TCGS_K7_CTAS 3
+#define TCGS_K7_CTAS (TCGS_K7_PIX == 2 ? 4 : 3)
 #endif
 constexpr int K7_CTAS_PER_SM = TCGS_K7_CTAS;
 
@@ -142,6 +146,8 @@ inline Band make_band(const tcgs_camera &cam, const tcgs_opts *o) {
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug,
                               void *ws, const Layout &L, cudaStream_t st);
+cudaError_t launch_preprocess_views(const tcgs_scene &scene, const tcgs_camera *cams, const Band *bands, int n_views,
+                                    int debug, void *const *ws, const Layout *L, cudaStream_t st);
 cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st);
 cudaError_t launch_render(int alpha_mode, const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
                           void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st);
@@ -173,6 +179,11 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -16,6 +16,7 @@ blend kernel.  Nothing here computes pixels on the CPU.
 
 from __future__ import annotations
 
+import ctypes
 import time
 from dataclasses import dataclass, field
 
@@ -462,6 +463,46 @@ class ViewRenderer:
         s.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(s):
             return self.renderers[i].launch(cloud, cam, timers=timers)
+
+    def launch_group(self, cloud: GaussianCloud, cams, timers=None):
+        """Enqueue ``len(cams)`` views (at most the stream count and ``_abi.MAX_VIEWS_PER_PASS``) with ONE
+        fused K1 pass (``tcgs_preprocess_views``: each Gaussian's inputs are read once for every camera),
+        then each view's K2-K7 on its own stream.  Returns the views' (rgb, T, n_contrib) outputs.
+        ``timers`` (4 events) bracket the fused K1 and the last view's binning / blending."""
+        n = len(cams)
+        if not 1 <= n <= min(len(self.streams), _abi.MAX_VIEWS_PER_PASS):
+            raise ValueError(f"a view group holds 1..{min(len(self.streams), _abi.MAX_VIEWS_PER_PASS)} cameras")
+        idx = [(self.k + j) % len(self.streams) for j in range(n)]
+        self.k += n
+        rs = [self.renderers[i] for i in idx]
+        ss = [self.streams[i] for i in idx]
+        cs = [camera_struct(c) for c in cams]
+        cap = max(r.capacity(cloud.P) for r in rs)  # one workspace layout for the whole pass
+        wss = []
+        for r, c in zip(rs, cs):
+            r.max_splats = cap
+            wss.append(r.workspace(cloud.P, c.width, c.height, cap))
+        ps = ss[0]  # the fused K1 runs on the first view's stream, after every view's previous frame
+        ps.wait_stream(torch.cuda.current_stream(self.device))
+        for s in ss[1:]:
+            ps.wait_stream(s)
+        cam_arr = (_abi.Camera * n)(*cs)
+        ws_arr = (ctypes.c_void_p * n)(*[w.data_ptr() for w in wss])
+        ev = timers
+        with torch.cuda.stream(ps):
+            if ev:
+                ev[0].record()
+            _abi.check(self.lib.tcgs_preprocess_views(cloud._c(), cam_arr, n, rs[0]._opts(), ws_arr,
+                                                      min(w.numel() for w in wss), cap, ps.cuda_stream),
+                       "tcgs_preprocess_views")
+            if ev:
+                ev[1].record()
+        outs = []
+        for j, (r, s, cam) in enumerate(zip(rs, ss, cams)):
+            s.wait_stream(ps)
+            with torch.cuda.stream(s):
+                outs.append(r.bin_blend(cloud, cam, timers=ev if (ev and j == n - 1) else None))
+        return outs
 
     def join(self):
         cur = torch.cuda.current_stream(self.device)

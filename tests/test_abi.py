@@ -73,6 +73,29 @@ def test_invalid_arguments_are_rejected_before_any_launch(lib):
     assert lib.tcgs_launch_count() == n0
 
 
+def test_preprocess_views_rejects_bad_view_groups(lib):
+    scene = _abi.Scene()
+    scene.P, scene.sh_degree, scene.dtype = 0, 0, 0
+    cams = (_abi.Camera * 2)()
+    for c in cams:
+        c.width, c.height, c.fx, c.fy, c.near_plane = 64, 64, 50.0, 50.0, 0.2
+    need = lib.tcgs_workspace_size(0, 64, 64, 1024)
+    bufs = [ctypes.create_string_buffer(need) for _ in range(2)]
+    ws = (ctypes.c_void_p * 2)(*[ctypes.cast(b, ctypes.c_void_p).value for b in bufs])
+    n0 = lib.tcgs_launch_count()
+    for n in (0, _abi.MAX_VIEWS_PER_PASS + 1):
+        assert lib.tcgs_preprocess_views(ctypes.byref(scene), cams, n, None, ws, need, 1024, None) == \
+            _abi.TCGS_ERR_INVALID_ARG
+    same = (ctypes.c_void_p * 2)(ws[0], ws[0])
+    assert lib.tcgs_preprocess_views(ctypes.byref(scene), cams, 2, None, same, need, 1024, None) == \
+        _abi.TCGS_ERR_INVALID_ARG
+    assert b"distinct" in lib.tcgs_last_error()
+    cams[1].width = 0
+    assert lib.tcgs_preprocess_views(ctypes.byref(scene), cams, 2, None, ws, need, 1024, None) == \
+        _abi.TCGS_ERR_INVALID_ARG
+    assert lib.tcgs_launch_count() == n0
+
+
 def test_product_package_never_touches_the_oracle():
     """Only tests/, smoke() and bench.py may use oracle/: the shipped package must not import it."""
     for dirpath, _, files in os.walk(PKG):

@@ -431,6 +431,44 @@ def test_view_renderer_streams_match_sequential(renderers):
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("scale,group", [(0.02, 4), (0.005, 1), (0.005, 3)])
+def test_view_group_fused_preprocess_matches_frames(scale, group):
+    """One fused K1 pass for a group of cameras (tcgs_preprocess_views) gives every view exactly the frame
+    and FragmentStats of its own single-camera render."""
+    scene, cams = synthetic.config_scene("c4", scale)
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    views = [cams[i] for i in range(0, 256, 256 // (2 * group))][: 2 * group]
+    r = tcgs.Renderer("cuda", "tcgs")
+    ref = []
+    for c in views:  # (a Renderer reuses its output buffers: copy each frame before the next)
+        f = r.render_frame(cloud, c, timed=False)
+        ref.append((f.rgb.clone(), f.T.clone(), f.n_contrib.clone(), f.stats))
+    vr = tcgs.ViewRenderer("cuda", "tcgs", n_streams=group)
+    vr.warm(cloud, views[0])
+    for g0 in range(0, len(views), group):
+        outs = vr.launch_group(cloud, views[g0:g0 + group])
+        vr.join()
+        torch.cuda.synchronize()
+        for j, (rgb, T, cnt) in enumerate(outs):
+            a = ref[g0 + j]
+            rr = vr.renderers[(g0 + j) % group]
+            diag = (g0 + j, float((rgb - a[0]).abs().max()), int((cnt != a[2]).sum()), rr.read_stats(cloud.P)[1],
+                    a[3])
+            assert torch.equal(rgb, a[0]) and torch.equal(T, a[1]) and torch.equal(cnt, a[2]), diag
+            rc, fs = rr.read_stats(cloud.P)
+            assert rc == 0
+            assert (fs.f_blend, fs.f_cull, fs.n_splats, fs.dropped, fs.n_visible, fs.pixels_terminated) == (
+                a[3].f_blend, a[3].f_cull, a[3].n_splats, a[3].dropped, a[3].n_visible, a[3].pixels_terminated)
+
+
+def test_view_group_rejects_oversized_groups():
+    scene, cams = synthetic.config_scene("c4", 0.002)
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    vr = tcgs.ViewRenderer("cuda", "tcgs", n_streams=2)
+    with pytest.raises(ValueError):
+        vr.launch_group(cloud, cams[:3])
+
+
 def test_rasterize_batched_views_match_frames():
     scene, cams = synthetic.config_scene("c4", 0.02)
     views = [cams[i] for i in (3, 70, 150, 220, 250)]

@@ -541,11 +541,12 @@ def render(scene, cam, backend="tcgs", device=None) -> tuple[ImageBuffer, Fragme
 
 
 def rasterize(means, scales, rotations, opacities, features, sh_degree: int, cameras, backend="tcgs",
-              band=None, renderer: Renderer | None = None, n_streams: int = 3) -> dict:
+              band=None, renderer: Renderer | None = None, n_streams: int = 8) -> dict:
     """Batched entry: render every camera of ``cameras`` from device tensors.
 
     Views are independent, so they run ``n_streams`` at a time on their own workspaces and CUDA
-    streams (``ViewRenderer``); every view's outputs are copied out on its own stream and its
+    streams (``ViewRenderer``), in groups of up to ``n_streams // 2`` (<= 8) that share one fused K1
+    pass (``tcgs_preprocess_views``); every view's outputs are copied out on its own stream and its
     FragmentStats snapshotted without a host sync.  Returns ``rgb [V,H,W,3] f32``, ``T [V,H,W] f32``,
     ``n_contrib [V,H,W] i32`` (device tensors) and per-view FragmentStats.
     """
@@ -569,14 +570,19 @@ def rasterize(means, scales, rotations, opacities, features, sh_degree: int, cam
         nb = int(vr.lib.tcgs_counters_bytes())
         snaps = torch.empty((len(cams), nb), dtype=torch.uint8).pin_memory()
         outs = []
-        for v, cam in enumerate(cams):
-            i = vr.k % len(vr.streams)
-            rgb, T, cnt = vr.launch(cloud, cam)
-            with torch.cuda.stream(vr.streams[i]):
-                outs.append((rgb.clone(), T.clone(), cnt.clone()))
-                _abi.check(vr.lib.tcgs_snapshot_stats(ctypes.c_void_p(vr.renderers[i].ws.data_ptr()),
-                                                      ctypes.c_void_p(snaps[v].data_ptr()),
-                                                      ctypes.c_void_p(vr.streams[i].cuda_stream)), "snapshot")
+        # groups of views share one fused K1 pass; two groups in flight (the next group's K1 overlaps this
+        # group's binning and blending)
+        group = max(1, min(_abi.MAX_VIEWS_PER_PASS, len(vr.streams) // 2))
+        for v0 in range(0, len(cams), group):
+            n = len(vr.streams)
+            idx = [(vr.k + j) % n for j in range(min(group, len(cams) - v0))]
+            res = vr.launch_group(cloud, cams[v0:v0 + len(idx)])
+            for j, (i, (rgb, T, cnt)) in enumerate(zip(idx, res)):
+                with torch.cuda.stream(vr.streams[i]):
+                    outs.append((rgb.clone(), T.clone(), cnt.clone()))
+                    _abi.check(vr.lib.tcgs_snapshot_stats(ctypes.c_void_p(vr.renderers[i].ws.data_ptr()),
+                                                          ctypes.c_void_p(snaps[v0 + j].data_ptr()),
+                                                          ctypes.c_void_p(vr.streams[i].cuda_stream)), "snapshot")
         vr.join()
         torch.cuda.current_stream(means.device).synchronize()
         out = []

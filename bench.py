@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--streams", type=int, default=16, help="views in flight (one workspace + CUDA stream each)")
+    ap.add_argument("--coverage", choices=["square", "ellipse"], default="square",
+                    help="tiles per Gaussian: the reference's 3-sigma square (parity) or the opt-in alpha-ellipse "
+                         "box (same image, fewer splats; SURVEY.md 8(f) 4)")
     ap.add_argument("--view-group", type=int, default=8,
                     help="views per fused K1 pass (tcgs_preprocess_views; <= --streams, <= 8); 0 = one K1 per "
                          "view.  Two groups in flight: the next group's K1 overlaps this group's K2-K7")
@@ -364,7 +367,7 @@ def run_tcgs(args):
         first = br.render(cloud, base, with_stats=True)  # sizes the workspace
         st0 = first.stats
     else:
-        vr = tcgs.ViewRenderer(dev, args.backend, max(1, args.streams))
+        vr = tcgs.ViewRenderer(dev, args.backend, max(1, args.streams), coverage=args.coverage)
         r = vr.renderers[0]
         st0 = vr.warm(cloud, base)  # sizes the workspaces; stats of the base view
     stream = torch.cuda.current_stream(dev)
@@ -571,6 +574,7 @@ def run_tcgs(args):
         "backend": args.backend,
         "views_in_flight": 1 if bands_mode else max(1, args.streams),
         "view_group": group,
+        "coverage": args.coverage,
         "band_output": (args.band_output if world > 1 else "local") if bands_mode else None,
         "alpha_blend_ms": blend_avg,
         "stage_rooflines": stage_rooflines(scene, cloud.P, st_last, iso or stage, peaks, base, group),

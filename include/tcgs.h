@@ -80,7 +80,14 @@ typedef struct tcgs_opts {
     int32_t alpha_mode;     /* enum tcgs_alpha_mode */
     int32_t early_cull;     /* exp_calls accounting: 1 = EarlyCull (tensor_path.py:148-154), 0 = reference (raster.py:94) */
     int32_t debug;          /* 1: K1 also stores float64 conic/depth for tcgs_copy_projection */
+    int32_t coverage;       /* enum tcgs_coverage (K1's tile rectangle) */
 } tcgs_opts;
+
+/* Tiles a Gaussian is binned to.  SQUARE is the reference's covered_tiles (src/tilesplat/tiling.py:34-43:
+ * the 3-sigma square; parity).  ELLIPSE_BOX (opt-in) intersects that square with the
+ * bounding box of the alpha >= 1/255 ellipse, plus a margin: the splats it drops have no fragment that can
+ * pass EarlyCull, so the image is the same while N, f_cull and f_skip shrink. */
+enum tcgs_coverage { TCGS_COVER_SQUARE = 0, TCGS_COVER_ELLIPSE_BOX = 1 };
 
 /* FragmentStats (src/tilesplat/raster.py:19-49) plus extras. */
 typedef struct tcgs_stats {

@@ -41,7 +41,11 @@ class Camera(ctypes.Structure):
 
 class Opts(ctypes.Structure):
     _fields_ = [("tile_row_begin", ctypes.c_int32), ("tile_row_end", ctypes.c_int32),
-                ("alpha_mode", ctypes.c_int32), ("early_cull", ctypes.c_int32), ("debug", ctypes.c_int32)]
+                ("alpha_mode", ctypes.c_int32), ("early_cull", ctypes.c_int32), ("debug", ctypes.c_int32),
+                ("coverage", ctypes.c_int32)]
+
+
+COVERAGE = {"square": 0, "ellipse": 1}  # enum tcgs_coverage (include/tcgs.h)
 
 
 class Stats(ctypes.Structure):

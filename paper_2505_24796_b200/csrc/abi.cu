@@ -66,6 +66,8 @@ int check_common(const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t
     if (opts) {
         if (opts->alpha_mode < 0 || opts->alpha_mode > TCGS_ALPHA_FFMA)
             return fail(TCGS_ERR_INVALID_ARG, "unknown alpha mode");
+        if (opts->coverage < TCGS_COVER_SQUARE || opts->coverage > TCGS_COVER_ELLIPSE_BOX)
+            return fail(TCGS_ERR_INVALID_ARG, "unknown coverage mode");
         if (opts->tile_row_end > 0 && (opts->tile_row_begin < 0 || opts->tile_row_begin >= opts->tile_row_end ||
                                        opts->tile_row_end > ty))
             return fail(TCGS_ERR_INVALID_ARG, "invalid tile-row band");
@@ -124,7 +126,8 @@ int tcgs_preprocess(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_
     const Layout L = Layout::make(scene->P, cam->width, cam->height, max_splats);
     note_launch();
     init_counters<<<1, 1, 0, st>>>(at<DevCounters>(ws, L.counters));
-    cudaError_t e = launch_preprocess(*scene, *cam, make_band(*cam, opts), opts ? opts->debug : 0, ws, L, st);
+    cudaError_t e = launch_preprocess(*scene, *cam, make_band(*cam, opts), opts ? opts->debug : 0,
+                                      opts ? opts->coverage : 0, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "preprocess");
     return TCGS_OK;
 }
@@ -151,7 +154,8 @@ int tcgs_preprocess_views(const tcgs_scene *scene, const tcgs_camera *cams, int3
     cudaStream_t st = (cudaStream_t)stream;
     note_launch();
     init_counters_views<<<1, 32, 0, st>>>(cs, n_views);
-    cudaError_t e = launch_preprocess_views(*scene, cams, bands, n_views, opts ? opts->debug : 0, ws, L, st);
+    cudaError_t e = launch_preprocess_views(*scene, cams, bands, n_views, opts ? opts->debug : 0,
+                                            opts ? opts->coverage : 0, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "preprocess_views");
     return TCGS_OK;
 }

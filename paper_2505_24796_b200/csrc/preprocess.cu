@@ -185,6 +185,7 @@ struct PreArgs {
     int sh_degree;
     int tiles_x, tiles_y, band_y0, band_y1;
     int debug;
+    int coverage;  // enum tcgs_coverage
     Rec *rec;
     short4 *rect;
     uint32_t *touched;
@@ -400,6 +401,22 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
                     // band-agnostic (binning clips it to a tile-row band), so one K1 serves every band choice.
                     double fx0 = floor((mx - rad) / TILE), fx1 = floor((mx + rad) / TILE);
                     double fy0 = floor((my - rad) / TILE), fy1 = floor((my + rad) / TILE);
+                    if (a.coverage == TCGS_COVER_ELLIPSE_BOX) {
+                        // opt-in, not the reference's coverage: keep only tiles the
+                        // alpha >= 1/255 ellipse q <= 2 ln(255 o) can reach -- its bounding box, with a margin
+                        // above every rounding of K7's exponent -- inside the reference's square.  Splats it
+                        // drops have no live fragment, so the image is unchanged; N and f_cull shrink.
+                        const double Qc = 2.0 * (log(ld(opac, l)) + 5.541263545158426) + 0.02;
+                        if (Qc > 0.0) {
+                            const double ex = sqrt(Qc * sa) + 0.01, ey = sqrt(Qc * sc) + 0.01;
+                            fx0 = fmax(fx0, floor((mx - ex) / TILE));
+                            fx1 = fmin(fx1, floor((mx + ex) / TILE));
+                            fy0 = fmax(fy0, floor((my - ey) / TILE));
+                            fy1 = fmin(fy1, floor((my + ey) / TILE));
+                        } else {
+                            fx1 = fx0 - 1.0;  // opacity < 1/255: no fragment anywhere can pass EarlyCull
+                        }
+                    }
                     fx0 = fmax(fx0, 0.0);
                     fy0 = fmax(fy0, 0.0);
                     fx1 = fmin(fx1, (double)(a.tiles_x - 1));
@@ -486,8 +503,8 @@ cudaError_t launch_k1(const PreViews<NV> &pv, const tcgs_scene &scene, int F, in
     return cudaGetLastError();
 }
 
-PreArgs view_args(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug, void *ws,
-                  const Layout &L) {
+PreArgs view_args(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug, int coverage,
+                  void *ws, const Layout &L) {
     PreArgs a;
     a.cam = cam;
     const double *V = cam.view;
@@ -500,6 +517,7 @@ PreArgs view_args(const tcgs_scene &scene, const tcgs_camera &cam, const Band &b
     a.band_y0 = band.y0;
     a.band_y1 = band.y1;
     a.debug = debug;
+    a.coverage = coverage;
     a.rec = at<Rec>(ws, L.rec);
     a.rect = at<short4>(ws, L.rect);
     a.touched = at<uint32_t>(ws, L.touched);
@@ -523,17 +541,17 @@ cudaError_t launch_views(const PreViews<NV> &pv, const tcgs_scene &scene, cudaSt
 }  // namespace
 
 cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug,
-                              void *ws, const Layout &L, cudaStream_t st) {
+                              int coverage, void *ws, const Layout &L, cudaStream_t st) {
     PreViews<1> pv;
-    pv.v[0] = view_args(scene, cam, band, debug, ws, L);
+    pv.v[0] = view_args(scene, cam, band, debug, coverage, ws, L);
     pv.n = 1;
     return launch_views(pv, scene, st);
 }
 
 cudaError_t launch_preprocess_views(const tcgs_scene &scene, const tcgs_camera *cams, const Band *bands, int n_views,
-                                    int debug, void *const *ws, const Layout *L, cudaStream_t st) {
+                                    int debug, int coverage, void *const *ws, const Layout *L, cudaStream_t st) {
     PreViews<TCGS_MAX_VIEWS_PER_PASS> pv;
-    for (int v = 0; v < n_views; v++) pv.v[v] = view_args(scene, cams[v], bands[v], debug, ws[v], L[v]);
+    for (int v = 0; v < n_views; v++) pv.v[v] = view_args(scene, cams[v], bands[v], debug, coverage, ws[v], L[v]);
     pv.n = n_views;
     return launch_views(pv, scene, st);
 }

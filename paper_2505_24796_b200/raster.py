@@ -239,7 +239,10 @@ class Renderer:
     the splat capacity.
     """
 
-    def __init__(self, device=None, backend="tcgs", max_splats: int | None = None):
+    def __init__(self, device=None, backend="tcgs", max_splats: int | None = None, coverage: str = "square"):
+        if coverage not in _abi.COVERAGE:
+            raise ValueError(f"coverage must be one of {sorted(_abi.COVERAGE)}")
+        self.coverage = _abi.COVERAGE[coverage]  # "square": the reference's tiles; "ellipse": opt-in, fewer splats
         self.lib = _abi.load()
         self.device = torch.device(device or "cuda")
         if self.device.type != "cuda":
@@ -258,6 +261,7 @@ class Renderer:
         o.alpha_mode = self.backend.alpha_mode
         o.early_cull = 1 if self.backend.early_cull else 0
         o.debug = 1 if debug else 0
+        o.coverage = self.coverage
         return o
 
     def workspace(self, P: int, W: int, H: int, cap: int) -> torch.Tensor:
@@ -436,9 +440,9 @@ class ViewRenderer:
     changes no result.  ``join()`` makes the caller's current stream wait for every view.
     """
 
-    def __init__(self, device=None, backend="tcgs", n_streams: int = 2):
+    def __init__(self, device=None, backend="tcgs", n_streams: int = 2, coverage: str = "square"):
         self.device = torch.device(device or "cuda")
-        self.renderers = [Renderer(self.device, backend) for _ in range(n_streams)]
+        self.renderers = [Renderer(self.device, backend, coverage=coverage) for _ in range(n_streams)]
         self.streams = [torch.cuda.Stream(self.device) for _ in range(n_streams)]
         self.outputs = [None] * n_streams
         self.k = 0

@@ -70,6 +70,10 @@ def test_invalid_arguments_are_rejected_before_any_launch(lib):
     assert rc == _abi.TCGS_ERR_WORKSPACE  # 16 bytes is far below tcgs_workspace_size
     with pytest.raises(ValueError):
         _abi.check(rc, "tcgs_bin")
+    o = _abi.Opts()
+    o.coverage = 7
+    rc = lib.tcgs_bin(10, ctypes.byref(cam), ctypes.byref(o), ctypes.cast(ws, ctypes.c_void_p), 16, 100, None)
+    assert rc == _abi.TCGS_ERR_INVALID_ARG and b"coverage" in lib.tcgs_last_error()
     assert lib.tcgs_launch_count() == n0
 
 

@@ -461,6 +461,26 @@ def test_view_group_fused_preprocess_matches_frames(scale, group):
                 a[3].f_blend, a[3].f_cull, a[3].n_splats, a[3].dropped, a[3].n_visible, a[3].pixels_terminated)
 
 
+@pytest.mark.parametrize("cfg,scale", [("c2", 0.05), ("c5", 0.01), ("c4", 0.01)])
+def test_ellipse_coverage_keeps_the_image(cfg, scale):
+    """Opt-in ellipse-box coverage bins fewer splats but drops only splats with no live
+    fragment: image, transmittance, contributor counts, blends and terminations equal the reference coverage."""
+    scene, cams = synthetic.config_scene(cfg, scale)
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    sq = tcgs.Renderer("cuda", "tcgs").render_frame(cloud, cams[0], timed=False)
+    sq = (sq.rgb.clone(), sq.T.clone(), sq.n_contrib.clone(), sq.stats)
+    el = tcgs.Renderer("cuda", "tcgs", coverage="ellipse").render_frame(cloud, cams[0], timed=False)
+    assert torch.equal(el.rgb, sq[0]) and torch.equal(el.T, sq[1]) and torch.equal(el.n_contrib, sq[2])
+    assert el.stats.f_blend == sq[3].f_blend and el.stats.pixels_terminated == sq[3].pixels_terminated
+    assert el.stats.n_splats < sq[3].n_splats
+    assert el.stats.f_cull < sq[3].f_cull
+
+
+def test_unknown_coverage_is_rejected():
+    with pytest.raises(ValueError):
+        tcgs.Renderer("cuda", "tcgs", coverage="disc")
+
+
 def test_view_group_rejects_oversized_groups():
     scene, cams = synthetic.config_scene("c4", 0.002)
     cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")

@@ -48,9 +48,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--streams", type=int, default=16, help="views in flight (one workspace + CUDA stream each)")
-    ap.add_argument("--coverage", choices=["square", "ellipse"], default="square",
-                    help="tiles per Gaussian: the reference's 3-sigma square (parity) or the opt-in alpha-ellipse "
-                         "box (same image, fewer splats; SURVEY.md 8(f) 4)")
+    ap.add_argument("--coverage", choices=["square", "box", "ellipse"], default="square",
+                    help="tiles per Gaussian: the reference's 3-sigma square (parity), or opt-in (same image, fewer "
+                         "splats; SURVEY.md 8(f) 4): the alpha-ellipse's bounding box, or every tile it touches")
     ap.add_argument("--view-group", type=int, default=8,
                     help="views per fused K1 pass (tcgs_preprocess_views; <= --streams, <= 8); 0 = one K1 per "
                          "view.  Two groups in flight: the next group's K1 overlaps this group's K2-K7")

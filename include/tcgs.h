@@ -84,10 +84,12 @@ typedef struct tcgs_opts {
 } tcgs_opts;
 
 /* Tiles a Gaussian is binned to.  SQUARE is the reference's covered_tiles (src/tilesplat/tiling.py:34-43:
- * the 3-sigma square; parity).  ELLIPSE_BOX (opt-in) intersects that square with the
- * bounding box of the alpha >= 1/255 ellipse, plus a margin: the splats it drops have no fragment that can
- * pass EarlyCull, so the image is the same while N, f_cull and f_skip shrink. */
-enum tcgs_coverage { TCGS_COVER_SQUARE = 0, TCGS_COVER_ELLIPSE_BOX = 1 };
+ * the 3-sigma square; parity).  The opt-in modes keep only tiles of that square the
+ * alpha >= 1/255 ellipse (grown by a margin) can reach: ELLIPSE_BOX its bounding box, ELLIPSE every tile it
+ * intersects (FlashGS-style exact coverage, per tile row).  The splats they drop have no fragment that can
+ * pass EarlyCull, so the image is the same while N, f_cull and f_skip shrink.  Pass the same mode to
+ * tcgs_preprocess and tcgs_bin. */
+enum tcgs_coverage { TCGS_COVER_SQUARE = 0, TCGS_COVER_ELLIPSE_BOX = 1, TCGS_COVER_ELLIPSE = 2 };
 
 /* FragmentStats (src/tilesplat/raster.py:19-49) plus extras. */
 typedef struct tcgs_stats {

@@ -45,7 +45,7 @@ class Opts(ctypes.Structure):
                 ("coverage", ctypes.c_int32)]
 
 
-COVERAGE = {"square": 0, "ellipse": 1}  # enum tcgs_coverage (include/tcgs.h)
+COVERAGE = {"square": 0, "box": 1, "ellipse": 2}  # enum tcgs_coverage (include/tcgs.h)
 
 
 class Stats(ctypes.Structure):

@@ -66,7 +66,7 @@ int check_common(const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t
     if (opts) {
         if (opts->alpha_mode < 0 || opts->alpha_mode > TCGS_ALPHA_FFMA)
             return fail(TCGS_ERR_INVALID_ARG, "unknown alpha mode");
-        if (opts->coverage < TCGS_COVER_SQUARE || opts->coverage > TCGS_COVER_ELLIPSE_BOX)
+        if (opts->coverage < TCGS_COVER_SQUARE || opts->coverage > TCGS_COVER_ELLIPSE)
             return fail(TCGS_ERR_INVALID_ARG, "unknown coverage mode");
         if (opts->tile_row_end > 0 && (opts->tile_row_begin < 0 || opts->tile_row_begin >= opts->tile_row_end ||
                                        opts->tile_row_end > ty))

@@ -470,9 +470,28 @@ __device__ __forceinline__ uint32_t band_count(short4 q, int y0, int y1) {
     return q.y <= q.w ? (uint32_t)((q.z - q.x + 1) * (q.w - q.y + 1)) : 0u;
 }
 
+// Opt-in exact coverage (TCGS_COVER_ELLIPSE): the tiles of band-clipped rectangle q the ellipse touches.
+__device__ __forceinline__ uint32_t cover_count(const CoverRec &cs, short4 q) {
+    uint32_t n = 0;
+    for (int ty = q.y; ty <= q.w; ty++) {
+        int lo, hi;
+        if (cover_row(cs, ty, q.x, q.z, lo, hi)) n += (uint32_t)(hi - lo + 1);
+    }
+    return n;
+}
+
+template <bool EXACT>
+__device__ __forceinline__ uint32_t splat_count(const CoverRec *cover, uint32_t g, short4 q, int y0, int y1) {
+    if (!EXACT) return band_count(q, y0, y1);
+    q = band_rect(q, y0, y1);
+    return q.y <= q.w ? cover_count(cover[g], q) : 0u;
+}
+
+template <bool EXACT>  // EXACT: opt-in TCGS_COVER_ELLIPSE (separate instantiation: the default keeps its registers)
 __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx0, const uint32_t *idx1,
                                                              const DevCounters *ctr, const uint32_t *touched,
-                                                             const short4 *rect, int band_y0, int band_y1,
+                                                             const short4 *rect, const CoverRec *cover,
+                                                             int band_y0, int band_y1,
                                                              int64_t P, unsigned long long *blocksum) {
     const uint32_t *order = ctr->depth_cur ? idx1 : idx0;
     const int64_t beg = (int64_t)blockIdx.x * DUP_ITEMS;
@@ -482,7 +501,7 @@ __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx
         const int64_t i = beg + u * DUP_THREADS + threadIdx.x;
         if (i < P) {
             const uint32_t g = order[i];
-            if (touched[g]) s += band_count(rect[g], band_y0, band_y1);
+            if (touched[g]) s += splat_count<EXACT>(cover, g, rect[g], band_y0, band_y1);
         }
     }
 #pragma unroll
@@ -534,10 +553,11 @@ __global__ void __launch_bounds__(1024) count_scan(unsigned long long *blocksum,
 // K4: duplicate-with-keys.  Each CTA walks DUP_ITEMS depth-ordered Gaussians 256 at a time, scans their
 // tile counts, then expands (Gaussian, covered tile) pairs cooperatively: consecutive threads write
 // consecutive splats (binary search of the slot in the shared inclusive scan).
-template <typename KT>
+template <typename KT, bool EXACT>
 __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *idx0, const uint32_t *idx1,
                                                               const DevCounters *ctr, const uint32_t *touched,
-                                                              const short4 *rect, int64_t P,
+                                                              const short4 *rect, const CoverRec *cover,
+                                                              int64_t P,
                                                               const unsigned long long *blockoff, int tiles_x,
                                                               int band_y0, int band_y1, int64_t cap, KT *tkey,
                                                               uint32_t *tval) {
@@ -552,6 +572,7 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
     __shared__ uint32_t sval[DUP_STAGE];
     const uint32_t *order = ctr->depth_cur ? idx1 : idx0;
     const int tid = threadIdx.x;
+    constexpr bool exact = EXACT;
     const int64_t beg = (int64_t)blockIdx.x * DUP_ITEMS;
     unsigned long long base = blockoff[blockIdx.x];
     for (int r = 0; r < DUP_ITEMS / DUP_THREADS; r++) {
@@ -563,6 +584,7 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
             if (touched[g]) {
                 q = band_rect(rect[g], band_y0, band_y1);
                 c = q.x <= q.z && q.y <= q.w ? (uint32_t)((q.z - q.x + 1) * (q.w - q.y + 1)) : 0u;
+                if (c && exact) c = cover_count(cover[g], q);
                 if (!c) q = make_short4(0, 0, -1, -1);
             }
         }
@@ -572,9 +594,13 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
             constexpr uint32_t SMALL = 32;
             if (c <= SMALL) {
                 uint32_t o = ex;
+                CoverRec cs;
+                if (exact && c) cs = cover[g];
                 for (int ty = q.y; ty <= q.w; ty++) {
                     const uint32_t row = (uint32_t)((ty - band_y0) * tiles_x);
-                    for (int tx = q.x; tx <= q.z; tx++, o++) {
+                    int lo = q.x, hi = q.z;
+                    if (exact && !cover_row(cs, ty, q.x, q.z, lo, hi)) continue;
+                    for (int tx = lo; tx <= hi; tx++, o++) {
                         skey[o] = (KT)(row + tx);
                         sval[o] = g;
                     }
@@ -589,9 +615,25 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                 const uint32_t bex = __shfl_sync(0xffffffffu, ex, src);
                 const int bx0 = __shfl_sync(0xffffffffu, (int)q.x, src), by0 = __shfl_sync(0xffffffffu, (int)q.y, src);
                 const int bw = __shfl_sync(0xffffffffu, (int)(q.z - q.x + 1), src);
-                for (uint32_t kk = lane; kk < bc; kk += 32) {
-                    skey[bex + kk] = (KT)((by0 + (int)(kk / bw) - band_y0) * tiles_x + bx0 + (int)(kk % bw));
-                    sval[bex + kk] = bg;
+                if (exact) {  // row by row: every lane computes the (uniform) row span
+                    const int by1 = __shfl_sync(0xffffffffu, (int)q.w, src);
+                    const CoverRec cs = cover[bg];
+                    uint32_t o = bex;
+                    for (int ty = by0; ty <= by1; ty++) {
+                        int lo, hi;
+                        if (!cover_row(cs, ty, bx0, bx0 + bw - 1, lo, hi)) continue;
+                        const uint32_t row = (uint32_t)((ty - band_y0) * tiles_x);
+                        for (int tx = lo + lane; tx <= hi; tx += 32) {
+                            skey[o + (uint32_t)(tx - lo)] = (KT)(row + tx);
+                            sval[o + (uint32_t)(tx - lo)] = bg;
+                        }
+                        o += (uint32_t)(hi - lo + 1);
+                    }
+                } else {
+                    for (uint32_t kk = lane; kk < bc; kk += 32) {
+                        skey[bex + kk] = (KT)((by0 + (int)(kk / bw) - band_y0) * tiles_x + bx0 + (int)(kk % bw));
+                        sval[bex + kk] = bg;
+                    }
                 }
             }
             __syncthreads();
@@ -615,10 +657,23 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                     if (incl[mid] > s) hi = mid;
                     else lo = mid + 1;
                 }
-                const uint32_t kk = s - (lo ? incl[lo - 1] : 0u);
+                uint32_t kk = s - (lo ? incl[lo - 1] : 0u);
                 const short4 qq = rc[lo];
                 const int w = qq.z - qq.x + 1;
-                const int ty = qq.y + (int)(kk / w), tx = qq.x + (int)(kk % w);
+                int ty = qq.y + (int)(kk / w), tx = qq.x + (int)(kk % w);
+                if (exact) {  // walk the rows to the kk-th covered tile
+                    const CoverRec cs = cover[gid[lo]];
+                    for (ty = qq.y; ty <= qq.w; ty++) {
+                        int rlo, rhi;
+                        if (!cover_row(cs, ty, qq.x, qq.z, rlo, rhi)) continue;
+                        const uint32_t rw = (uint32_t)(rhi - rlo + 1);
+                        if (kk < rw) {
+                            tx = rlo + (int)kk;
+                            break;
+                        }
+                        kk -= rw;
+                    }
+                }
                 const uint32_t key = (uint32_t)((ty - band_y0) * tiles_x + tx);
                 const unsigned long long pos = base + s;
                 if (pos < (unsigned long long)cap) {
@@ -699,7 +754,8 @@ __global__ void pack_ranges(const int64_t *offsets, int band_tile0, int n_tiles,
 // Splats per tile row of the whole frame (sum over Gaussians of the covered tiles in that row), from K1's
 // frame-clipped rectangles: the replicated input of the tile-band partition (multi-GPU).
 __global__ void __launch_bounds__(256) row_counts_kernel(int64_t P, const uint32_t *touched, const short4 *rect,
-                                                         int tiles_y, unsigned long long *out) {
+                                                         const CoverRec *cover, int coverage, int tiles_y,
+                                                         unsigned long long *out) {
     constexpr int SMEM_ROWS = 4096;
     __shared__ unsigned long long h[SMEM_ROWS];
     const bool priv = tiles_y <= SMEM_ROWS;
@@ -709,6 +765,15 @@ __global__ void __launch_bounds__(256) row_counts_kernel(int64_t P, const uint32
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
         if (!touched[i]) continue;
         const short4 q = rect[i];
+        if (coverage == TCGS_COVER_ELLIPSE) {
+            const CoverRec cs = cover[i];
+            for (int y = q.y; y <= q.w; y++) {
+                int lo, hi;
+                if (cover_row(cs, y, q.x, q.z, lo, hi))
+                    atomicAdd(priv ? &h[y] : &out[y], (unsigned long long)(hi - lo + 1));
+            }
+            continue;
+        }
         const unsigned long long w = (unsigned long long)(q.z - q.x + 1);
         for (int y = q.y; y <= q.w; y++) atomicAdd(priv ? &h[y] : &out[y], w);
     }
@@ -732,16 +797,18 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     const int nblk = (int)div_up(P > 0 ? P : 1, DUP_ITEMS);
     // K3
     note_launch();
-    count_upsweep<<<nblk, DUP_THREADS, 0, st>>>(at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr,
-                                                 at<uint32_t>(ws, L.touched), at<short4>(ws, L.rect), band.y0,
-                                                 band.y1, P, blocksum);
+    const bool exact = band.coverage == TCGS_COVER_ELLIPSE;
+    (exact ? count_upsweep<true> : count_upsweep<false>)<<<nblk, DUP_THREADS, 0, st>>>(
+        at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr, at<uint32_t>(ws, L.touched),
+        at<short4>(ws, L.rect), at<CoverRec>(ws, L.cover), band.y0, band.y1, P, blocksum);
     note_launch();
     count_scan<<<1, 1024, 0, st>>>(blocksum, nblk, ctr, cap);
     // K4
     note_launch();
-    duplicate_keys<KT><<<nblk, DUP_THREADS, 0, st>>>(at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr,
-                                                      at<uint32_t>(ws, L.touched), at<short4>(ws, L.rect), P,
-                                                      blocksum, band.tiles_x, band.y0, band.y1, cap, tk0, tv0);
+    (exact ? duplicate_keys<KT, true> : duplicate_keys<KT, false>)<<<nblk, DUP_THREADS, 0, st>>>(
+        at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr, at<uint32_t>(ws, L.touched),
+        at<short4>(ws, L.rect), at<CoverRec>(ws, L.cover), P, blocksum, band.tiles_x, band.y0, band.y1, cap, tk0,
+        tv0);
     // K5
     note_launch();
     sort_plan<<<1, 256, 0, st>>>(ss_tile, npass, &ctr->n_splats, 0, cap, nullptr, 0, &ctr->tile_cur);
@@ -765,7 +832,8 @@ cudaError_t launch_row_counts(int64_t P, const Band &band, const void *ws, const
     const int64_t blocks = div_up(P, 256 * 8);
     note_launch();
     row_counts_kernel<<<(unsigned)(blocks < 4 * 148 ? blocks : 4 * 148), 256, 0, st>>>(
-        P, at<uint32_t>(ws, L.touched), at<short4>(ws, L.rect), band.tiles_y,
+        P, at<uint32_t>(ws, L.touched), at<short4>(ws, L.rect), at<CoverRec>(ws, L.cover), band.coverage,
+        band.tiles_y,
         reinterpret_cast<unsigned long long *>(out));
     return cudaGetLastError();
 }

@@ -187,6 +187,7 @@ struct PreArgs {
     int debug;
     int coverage;  // enum tcgs_coverage
     Rec *rec;
+    CoverRec *cover;
     short4 *rect;
     uint32_t *touched;
     unsigned long long *keys;
@@ -401,14 +402,15 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
                     // band-agnostic (binning clips it to a tile-row band), so one K1 serves every band choice.
                     double fx0 = floor((mx - rad) / TILE), fx1 = floor((mx + rad) / TILE);
                     double fy0 = floor((my - rad) / TILE), fy1 = floor((my + rad) / TILE);
-                    if (a.coverage == TCGS_COVER_ELLIPSE_BOX) {
+                    if (a.coverage != TCGS_COVER_SQUARE) {
                         // opt-in, not the reference's coverage: keep only tiles the
-                        // alpha >= 1/255 ellipse q <= 2 ln(255 o) can reach -- its bounding box, with a margin
-                        // above every rounding of K7's exponent -- inside the reference's square.  Splats it
-                        // drops have no live fragment, so the image is unchanged; N and f_cull shrink.
-                        const double Qc = 2.0 * (log(ld(opac, l)) + 5.541263545158426) + 0.02;
+                        // alpha >= 1/255 ellipse q <= 2 ln(255 o) can reach -- its bounding box, with margins
+                        // above every rounding of K7's exponent -- inside the reference's square (the exact
+                        // mode then trims each row in binning).  Splats it drops have no live fragment, so
+                        // the image is unchanged; N and f_cull shrink.
+                        const double Qc = 2.0 * (log(ld(opac, l)) + 5.541263545158426) + COVER_Q_MARGIN;
                         if (Qc > 0.0) {
-                            const double ex = sqrt(Qc * sa) + 0.01, ey = sqrt(Qc * sc) + 0.01;
+                            const double ex = sqrt(Qc * sa) + COVER_PX_MARGIN, ey = sqrt(Qc * sc) + COVER_PX_MARGIN;
                             fx0 = fmax(fx0, floor((mx - ex) / TILE));
                             fx1 = fmin(fx1, floor((mx + ex) / TILE));
                             fy0 = fmax(fy0, floor((my - ey) / TILE));
@@ -453,6 +455,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
                         rc.g = col[1];
                         rc.b = col[2];
                         a.rec[i] = rc;
+                        if (a.coverage == TCGS_COVER_ELLIPSE) a.cover[i] = make_cover(rc);  // binning's row spans
                     }
                 }
             }
@@ -519,6 +522,7 @@ PreArgs view_args(const tcgs_scene &scene, const tcgs_camera &cam, const Band &b
     a.debug = debug;
     a.coverage = coverage;
     a.rec = at<Rec>(ws, L.rec);
+    a.cover = at<CoverRec>(ws, L.cover);
     a.rect = at<short4>(ws, L.rect);
     a.touched = at<uint32_t>(ws, L.touched);
     a.keys = at<unsigned long long>(ws, L.key_src);

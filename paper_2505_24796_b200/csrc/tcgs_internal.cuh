@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_fp16.h>
+#include <math.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -53,6 +54,69 @@ struct __align__(16) Rec {
     float r, g, b, opacity;    // colour (SH evaluated) and opacity
 };
 
+// ---- opt-in tile coverage.  A fragment can pass EarlyCull only inside the ellipse
+// q(d) = s11 dx^2 + 2 s12 dx dy + s22 dy^2 <= Q = 2 ln(255 o) (d = pixel - mean).  The tests below keep every
+// tile that ellipse, grown by margins far above K7's exponent rounding, touches -- so only splats with no
+// live fragment are dropped and the image is unchanged.  K1 derives each Gaussian's row-span parameters in
+// float64 from the render record's fp32 conic and log-opacity (what K7 evaluates), so needle-thin ellipses
+// keep their exact extent; binning evaluates them per tile row in fp32 without cancellation.
+constexpr double COVER_Q_MARGIN = 0.2;   // in q (0.1 in beta = ln alpha)
+constexpr float COVER_PX_MARGIN = 0.5f;  // pixels, on every side
+
+struct __align__(16) CoverRec {
+    float mx, my;  // mean (pixels)
+    float b_a;     // s12 / s11: the centre of a row's x-interval is -b_a * dy
+    float det_a;   // det / s11^2: the half-width is sqrt(det_a (ry^2 - dy^2))
+    float ry;      // |dy| extent of the ellipse: sqrt(Q s11 / det)
+    float dys;     // dy of the rightmost point (the leftmost one is at -dys)
+    float pad;
+    int mode;      // 0: ellipse; 1: degenerate record, keep the reference's square; 2: no live fragment
+};
+
+__host__ __device__ inline CoverRec make_cover(const Rec &r) {
+    CoverRec c;
+    c.mx = (float)((double)r.mx + (double)r.mx_lo);
+    c.my = (float)((double)r.my + (double)r.my_lo);
+    c.b_a = c.det_a = c.ry = c.dys = c.pad = 0.0f;
+    const double a = r.s11, b = r.s12, cc = r.s22;
+    const double Q = 2.0 * ((double)r.ln_o + 5.541263545158426) + COVER_Q_MARGIN;
+    const double det = a * cc - b * b;
+    if (!(Q > 0.0)) {
+        c.mode = 2;
+    } else if (!(a > 0.0 && cc > 0.0 && det > 0.0) || !isfinite(det)) {
+        c.mode = 1;
+    } else {
+        c.mode = 0;
+        c.b_a = (float)(b / a);
+        c.det_a = (float)(det / (a * a));
+        c.ry = (float)sqrt(Q * a / det);
+        c.dys = (float)(-b * sqrt(Q / (cc * det)));
+    }
+    return c;
+}
+
+// Tiles [lo, hi] of tile row ty (within [x0, x1]) that the ellipse touches; false if none.  The x-interval of
+// the ellipse over the row's pixel strip is [min of the left boundary, max of the right boundary]: the right
+// boundary -b_a dy + hw(dy) is concave in dy, so its maximum over the strip is at the rightmost point's dy
+// clamped into the strip (and symmetrically on the left).  hw = sqrt(det_a (ry - |dy|)(ry + |dy|)).
+__device__ __forceinline__ bool cover_row(const CoverRec &c, int ty, int x0, int x1, int &lo, int &hi) {
+    lo = x0;
+    hi = x1;
+    if (c.mode) return c.mode == 1;
+    const float ylo = fmaxf(16.0f * ty - c.my - COVER_PX_MARGIN, -c.ry);
+    const float yhi = fminf(16.0f * ty + 15.0f - c.my + COVER_PX_MARGIN, c.ry);
+    if (ylo > yhi) return false;
+    const float yr = fminf(fmaxf(c.dys, ylo), yhi), yl = fminf(fmaxf(-c.dys, ylo), yhi);
+    const float ar = fabsf(yr), al = fabsf(yl);
+    const float xr = -c.b_a * yr + sqrtf(fmaxf(c.det_a * (c.ry - ar) * (c.ry + ar), 0.0f));
+    const float xl = -c.b_a * yl - sqrtf(fmaxf(c.det_a * (c.ry - al) * (c.ry + al), 0.0f));
+    const float fl = floorf((c.mx + xl - COVER_PX_MARGIN) * (1.0f / 16.0f));
+    const float fh = floorf((c.mx + xr + COVER_PX_MARGIN) * (1.0f / 16.0f));
+    lo = fl > (float)x0 ? (int)fl : x0;
+    hi = fh < (float)x1 ? (int)fh : x1;
+    return lo <= hi;
+}
+
 // Device-side counters and sort bookkeeping (zeroed at the start of each frame).
 struct DevCounters {
     unsigned long long dropped, n_visible, n_splats, overflow;
@@ -78,7 +142,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 struct Layout {
-    size_t counters, sort_state[2], rec, rect, touched, key_src, key64[2], long_runs, fix_scratch, idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
+    size_t counters, sort_state[2], rec, cover, rect, touched, key_src, key64[2], long_runs, fix_scratch, idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
     size_t blocksum, lb_depth, lb_tile, tkey[2], tval[2], ranges, total;
     size_t zero_begin, zero_bytes;  // sort state, cleared at the start of every binning
     static Layout make(int64_t P, int W, int H, int64_t cap) {
@@ -96,6 +160,7 @@ struct Layout {
         L.lb_depth = take(sizeof(uint32_t) * RADIX * MAX_PASSES * (size_t)div_up((int64_t)Pn, OS_THREADS * DEPTH_IPT));
         L.lb_tile = take(sizeof(uint32_t) * RADIX * TILE_MAX_PASSES * (size_t)div_up((int64_t)cn, OS_THREADS * TILEKEY_IPT));
         L.rec = take(sizeof(Rec) * Pn);
+        L.cover = take(sizeof(CoverRec) * Pn);
         L.rect = take(sizeof(short4) * Pn);
         L.touched = take(sizeof(uint32_t) * Pn);
         L.key_src = take(sizeof(uint64_t) * Pn);
@@ -127,6 +192,7 @@ inline const T *at(const void *ws, size_t off) { return reinterpret_cast<const T
 
 struct Band {
     int tiles_x, tiles_y, y0, y1;  // tile rows [y0, y1)
+    int coverage;                  // enum tcgs_coverage
     int n_tiles() const { return tiles_x * (y1 - y0); }
 };
 
@@ -136,6 +202,7 @@ inline Band make_band(const tcgs_camera &cam, const tcgs_opts *o) {
     b.tiles_y = (cam.height + TILE - 1) / TILE;
     b.y0 = 0;
     b.y1 = b.tiles_y;
+    b.coverage = o ? o->coverage : TCGS_COVER_SQUARE;
     if (o && o->tile_row_end > 0) {
         b.y0 = o->tile_row_begin < 0 ? 0 : o->tile_row_begin;
         b.y1 = o->tile_row_end > b.tiles_y ? b.tiles_y : o->tile_row_end;

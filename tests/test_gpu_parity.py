@@ -461,19 +461,39 @@ def test_view_group_fused_preprocess_matches_frames(scale, group):
                 a[3].f_blend, a[3].f_cull, a[3].n_splats, a[3].dropped, a[3].n_visible, a[3].pixels_terminated)
 
 
-@pytest.mark.parametrize("cfg,scale", [("c2", 0.05), ("c5", 0.01), ("c4", 0.01)])
+@pytest.mark.parametrize("cfg,scale", [("c2", 0.05), ("c5", 0.01), ("c4", 0.01), ("c3", 0.01)])
 def test_ellipse_coverage_keeps_the_image(cfg, scale):
-    """Opt-in ellipse-box coverage bins fewer splats but drops only splats with no live
-    fragment: image, transmittance, contributor counts, blends and terminations equal the reference coverage."""
+    """Opt-in coverage modes bin fewer splats but drop only splats with no live fragment:
+    image, transmittance, contributor counts, blends and terminations equal the reference coverage's, and the
+    exact per-tile mode keeps a subset of the bounding-box mode's splats."""
     scene, cams = synthetic.config_scene(cfg, scale)
     cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
     sq = tcgs.Renderer("cuda", "tcgs").render_frame(cloud, cams[0], timed=False)
     sq = (sq.rgb.clone(), sq.T.clone(), sq.n_contrib.clone(), sq.stats)
-    el = tcgs.Renderer("cuda", "tcgs", coverage="ellipse").render_frame(cloud, cams[0], timed=False)
-    assert torch.equal(el.rgb, sq[0]) and torch.equal(el.T, sq[1]) and torch.equal(el.n_contrib, sq[2])
-    assert el.stats.f_blend == sq[3].f_blend and el.stats.pixels_terminated == sq[3].pixels_terminated
-    assert el.stats.n_splats < sq[3].n_splats
-    assert el.stats.f_cull < sq[3].f_cull
+    n = {}
+    for mode in ("box", "ellipse"):
+        el = tcgs.Renderer("cuda", "tcgs", coverage=mode).render_frame(cloud, cams[0], timed=False)
+        assert torch.equal(el.rgb, sq[0]) and torch.equal(el.T, sq[1]) and torch.equal(el.n_contrib, sq[2]), mode
+        assert el.stats.f_blend == sq[3].f_blend and el.stats.pixels_terminated == sq[3].pixels_terminated
+        assert el.stats.n_splats < sq[3].n_splats and el.stats.f_cull < sq[3].f_cull
+        n[mode] = el.stats.n_splats
+    assert n["ellipse"] < n["box"]
+
+
+def test_exact_coverage_tile_lists_are_a_filtered_reference():
+    """Exact coverage's tile lists are the reference lists with some entries removed (same depth order)."""
+    scene, cams = synthetic.config_scene("c5", 0.005)
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    lists = {}
+    for mode in ("square", "ellipse"):
+        r = tcgs.Renderer("cuda", "tcgs", coverage=mode)
+        r.render_frame(cloud, cams[0], timed=False)
+        lists[mode] = r.tile_lists(cloud.P, cams[0])
+    (o_sq, i_sq), (o_el, i_el) = lists["square"], lists["ellipse"]
+    for t in range(len(o_sq) - 1):
+        ref, got = i_sq[o_sq[t]:o_sq[t + 1]], i_el[o_el[t]:o_el[t + 1]]
+        keep = np.isin(ref, got)
+        assert np.array_equal(ref[keep], got), t
 
 
 def test_unknown_coverage_is_rejected():

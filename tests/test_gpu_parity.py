@@ -501,6 +501,31 @@ def test_unknown_coverage_is_rejected():
         tcgs.Renderer("cuda", "tcgs", coverage="disc")
 
 
+@pytest.mark.parametrize("dtype,sh", [(torch.float64, True), (torch.float32, False), (torch.float64, False)])
+def test_view_group_dtypes_and_colour_modes(dtype, sh):
+    """The fused K1 pass in float64 scenes and for plain RGB colours (no SH), with a P that leaves a ragged tail
+    CTA, equals the per-view frames; and a group of views with the exact coverage keeps every image."""
+    scene, cams = synthetic.config_scene("c4", 0.0031)
+    if not sh:
+        scene = {k: v for k, v in scene.items() if k not in ("features", "sh_degree")}
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda", dtype=dtype)
+    views = [cams[i] for i in (5, 77, 140)]
+    for coverage in ("square", "ellipse"):
+        r = tcgs.Renderer("cuda", "tcgs", coverage=coverage)
+        ref = []
+        for c in views:
+            f = r.render_frame(cloud, c, timed=False)
+            ref.append((f.rgb.clone(), f.n_contrib.clone(), f.stats.n_splats))
+        vr = tcgs.ViewRenderer("cuda", "tcgs", n_streams=3, coverage=coverage)
+        vr.warm(cloud, views[0])
+        outs = vr.launch_group(cloud, views)
+        vr.join()
+        torch.cuda.synchronize()
+        for j, (rgb, T, cnt) in enumerate(outs):
+            assert torch.equal(rgb, ref[j][0]) and torch.equal(cnt, ref[j][1]), (coverage, j)
+            assert vr.renderers[j].read_stats(cloud.P)[1].n_splats == ref[j][2]
+
+
 def test_view_group_rejects_oversized_groups():
     scene, cams = synthetic.config_scene("c4", 0.002)
     cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")

@@ -480,17 +480,33 @@ __device__ __forceinline__ uint32_t cover_count(const CoverRec &cs, short4 q) {
     return n;
 }
 
+// Exact coverage of Gaussian g clipped to the band: its count, and -- for rectangles of at most
+// COVER_MASK_TILES tiles -- its K1 mask re-based to the clipped rectangle q (mask 0 with a count: walk rows).
+__device__ __forceinline__ uint32_t exact_cover(const CoverRec *cover, const unsigned long long *tmask, uint32_t g,
+                                                short4 r, short4 q, unsigned long long &m) {
+    m = 0ull;
+    if (q.y > q.w) return 0u;
+    const int w = r.z - r.x + 1;
+    if (w * (r.w - r.y + 1) <= COVER_MASK_TILES) {
+        m = mask_rows(tmask[g], w, q.y - r.y, q.w - r.y);
+        return (uint32_t)__popcll(m);
+    }
+    return cover_count(cover[g], q);
+}
+
 template <bool EXACT>
-__device__ __forceinline__ uint32_t splat_count(const CoverRec *cover, uint32_t g, short4 q, int y0, int y1) {
-    if (!EXACT) return band_count(q, y0, y1);
-    q = band_rect(q, y0, y1);
-    return q.y <= q.w ? cover_count(cover[g], q) : 0u;
+__device__ __forceinline__ uint32_t splat_count(const CoverRec *cover, const unsigned long long *tmask, uint32_t g,
+                                                short4 r, int y0, int y1) {
+    if (!EXACT) return band_count(r, y0, y1);
+    unsigned long long m;
+    return exact_cover(cover, tmask, g, r, band_rect(r, y0, y1), m);
 }
 
 template <bool EXACT>  // EXACT: opt-in TCGS_COVER_ELLIPSE (separate instantiation: the default keeps its registers)
 __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx0, const uint32_t *idx1,
                                                              const DevCounters *ctr, const uint32_t *touched,
                                                              const short4 *rect, const CoverRec *cover,
+                                                             const unsigned long long *tmask,
                                                              int band_y0, int band_y1,
                                                              int64_t P, unsigned long long *blocksum) {
     const uint32_t *order = ctr->depth_cur ? idx1 : idx0;
@@ -501,7 +517,7 @@ __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx
         const int64_t i = beg + u * DUP_THREADS + threadIdx.x;
         if (i < P) {
             const uint32_t g = order[i];
-            if (touched[g]) s += splat_count<EXACT>(cover, g, rect[g], band_y0, band_y1);
+            if (touched[g]) s += splat_count<EXACT>(cover, tmask, g, rect[g], band_y0, band_y1);
         }
     }
 #pragma unroll
@@ -557,13 +573,14 @@ template <typename KT, bool EXACT>
 __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *idx0, const uint32_t *idx1,
                                                               const DevCounters *ctr, const uint32_t *touched,
                                                               const short4 *rect, const CoverRec *cover,
-                                                              int64_t P,
+                                                              const unsigned long long *tmask, int64_t P,
                                                               const unsigned long long *blockoff, int tiles_x,
                                                               int band_y0, int band_y1, int64_t cap, KT *tkey,
                                                               uint32_t *tval) {
     __shared__ uint32_t incl[DUP_THREADS];
     __shared__ uint32_t gid[DUP_THREADS];
     __shared__ short4 rc[DUP_THREADS];
+    __shared__ unsigned long long msk[EXACT ? DUP_THREADS : 1];
     __shared__ uint32_t wt[8];
     // staging of one round's output: every thread writes its own rectangle (no search, no division), then
     // the CTA copies the round out with coalesced stores
@@ -578,13 +595,15 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
     for (int r = 0; r < DUP_ITEMS / DUP_THREADS; r++) {
         const int64_t i = beg + r * DUP_THREADS + tid;
         uint32_t c = 0, g = 0;
+        unsigned long long m = 0ull;  // exact coverage: the tile mask over q (0: walk rows)
         short4 q = make_short4(0, 0, -1, -1);
         if (i < P) {
             g = order[i];
             if (touched[g]) {
-                q = band_rect(rect[g], band_y0, band_y1);
+                const short4 r = rect[g];
+                q = band_rect(r, band_y0, band_y1);
                 c = q.x <= q.z && q.y <= q.w ? (uint32_t)((q.z - q.x + 1) * (q.w - q.y + 1)) : 0u;
-                if (c && exact) c = cover_count(cover[g], q);
+                if (c && exact) c = exact_cover(cover, tmask, g, r, q, m);
                 if (!c) q = make_short4(0, 0, -1, -1);
             }
         }
@@ -594,15 +613,24 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
             constexpr uint32_t SMALL = 32;
             if (c <= SMALL) {
                 uint32_t o = ex;
-                CoverRec cs;
-                if (exact && c) cs = cover[g];
-                for (int ty = q.y; ty <= q.w; ty++) {
-                    const uint32_t row = (uint32_t)((ty - band_y0) * tiles_x);
-                    int lo = q.x, hi = q.z;
-                    if (exact && !cover_row(cs, ty, q.x, q.z, lo, hi)) continue;
-                    for (int tx = lo; tx <= hi; tx++, o++) {
-                        skey[o] = (KT)(row + tx);
+                if (exact && m) {  // set bits of the mask, row-major
+                    const int w = q.z - q.x + 1;
+                    for (unsigned long long mm = m; mm; mm &= mm - 1ull, o++) {
+                        const int b = __ffsll((long long)mm) - 1, ty = q.y + b / w, tx = q.x + b % w;
+                        skey[o] = (KT)((ty - band_y0) * tiles_x + tx);
                         sval[o] = g;
+                    }
+                } else {
+                    CoverRec cs;
+                    if (exact && c) cs = cover[g];
+                    for (int ty = q.y; ty <= q.w; ty++) {
+                        const uint32_t row = (uint32_t)((ty - band_y0) * tiles_x);
+                        int lo = q.x, hi = q.z;
+                        if (exact && !cover_row(cs, ty, q.x, q.z, lo, hi)) continue;
+                        for (int tx = lo; tx <= hi; tx++, o++) {
+                            skey[o] = (KT)(row + tx);
+                            sval[o] = g;
+                        }
                     }
                 }
             }
@@ -615,7 +643,15 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                 const uint32_t bex = __shfl_sync(0xffffffffu, ex, src);
                 const int bx0 = __shfl_sync(0xffffffffu, (int)q.x, src), by0 = __shfl_sync(0xffffffffu, (int)q.y, src);
                 const int bw = __shfl_sync(0xffffffffu, (int)(q.z - q.x + 1), src);
-                if (exact) {  // row by row: every lane computes the (uniform) row span
+                const unsigned long long bm = exact ? __shfl_sync(0xffffffffu, m, src) : 0ull;
+                if (exact && bm) {  // mask: lane b takes bit b, its slot is the popcount below it
+                    for (int b = lane; b < COVER_MASK_TILES; b += 32) {
+                        if (!((bm >> b) & 1ull)) continue;
+                        const uint32_t o = bex + (uint32_t)__popcll(bm & ((1ull << b) - 1ull));
+                        skey[o] = (KT)((by0 + b / bw - band_y0) * tiles_x + bx0 + b % bw);
+                        sval[o] = bg;
+                    }
+                } else if (exact) {  // row by row: every lane computes the (uniform) row span
                     const int by1 = __shfl_sync(0xffffffffu, (int)q.w, src);
                     const CoverRec cs = cover[bg];
                     uint32_t o = bex;
@@ -648,6 +684,7 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
             incl[tid] = ex + c;
             gid[tid] = g;
             rc[tid] = q;
+            if (exact) msk[tid] = m;
             __syncthreads();
             for (uint32_t s = tid; s < total; s += DUP_THREADS) {
                 int lo = 0, hi = DUP_THREADS - 1;  // first item whose inclusive count exceeds s
@@ -661,7 +698,13 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                 const short4 qq = rc[lo];
                 const int w = qq.z - qq.x + 1;
                 int ty = qq.y + (int)(kk / w), tx = qq.x + (int)(kk % w);
-                if (exact) {  // walk the rows to the kk-th covered tile
+                if (exact && msk[lo]) {  // the kk-th set bit of the mask
+                    unsigned long long mm = msk[lo];
+                    for (uint32_t j = 0; j < kk; j++) mm &= mm - 1ull;
+                    const int b = __ffsll((long long)mm) - 1;
+                    ty = qq.y + b / w;
+                    tx = qq.x + b % w;
+                } else if (exact) {  // walk the rows to the kk-th covered tile
                     const CoverRec cs = cover[gid[lo]];
                     for (ty = qq.y; ty <= qq.w; ty++) {
                         int rlo, rhi;
@@ -800,15 +843,16 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     const bool exact = band.coverage == TCGS_COVER_ELLIPSE;
     (exact ? count_upsweep<true> : count_upsweep<false>)<<<nblk, DUP_THREADS, 0, st>>>(
         at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr, at<uint32_t>(ws, L.touched),
-        at<short4>(ws, L.rect), at<CoverRec>(ws, L.cover), band.y0, band.y1, P, blocksum);
+        at<short4>(ws, L.rect), at<CoverRec>(ws, L.cover), at<unsigned long long>(ws, L.tmask), band.y0, band.y1, P,
+        blocksum);
     note_launch();
     count_scan<<<1, 1024, 0, st>>>(blocksum, nblk, ctr, cap);
     // K4
     note_launch();
     (exact ? duplicate_keys<KT, true> : duplicate_keys<KT, false>)<<<nblk, DUP_THREADS, 0, st>>>(
         at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr, at<uint32_t>(ws, L.touched),
-        at<short4>(ws, L.rect), at<CoverRec>(ws, L.cover), P, blocksum, band.tiles_x, band.y0, band.y1, cap, tk0,
-        tv0);
+        at<short4>(ws, L.rect), at<CoverRec>(ws, L.cover), at<unsigned long long>(ws, L.tmask), P, blocksum,
+        band.tiles_x, band.y0, band.y1, cap, tk0, tv0);
     // K5
     note_launch();
     sort_plan<<<1, 256, 0, st>>>(ss_tile, npass, &ctr->n_splats, 0, cap, nullptr, 0, &ctr->tile_cur);

@@ -178,6 +178,28 @@ __device__ void sh_color(const T *sh, int deg, double dx, double dy, double dz, 
     out[2] = fminf(fmaxf(r2 + 0.5f, 0.0f), 1.0f);
 }
 
+// Exact coverage records of one Gaussian (opt-in TCGS_COVER_ELLIPSE), out of line so that the default path's
+// register allocation does not pay for it.  Returns the touched count: the mask's popcount for rectangles of
+// at most COVER_MASK_TILES tiles, otherwise the rectangle's area (binning walks its rows).
+__device__ __noinline__ uint32_t exact_cover_record(float mx, float mx_lo, float my, float my_lo, float s11, float s12,
+                                                    float s22, float ln_o, int x0, int y0, int x1, int y1,
+                                                    CoverRec *cover, unsigned long long *tmask, uint32_t area) {
+    Rec rc;
+    rc.mx = mx;
+    rc.mx_lo = mx_lo;
+    rc.my = my;
+    rc.my_lo = my_lo;
+    rc.s11 = s11;
+    rc.s12 = s12;
+    rc.s22 = s22;
+    rc.ln_o = ln_o;
+    const CoverRec cr = make_cover(rc);
+    *cover = cr;
+    const unsigned long long m = cover_mask(cr, x0, y0, x1, y1);
+    *tmask = m;
+    return (x1 - x0 + 1) * (y1 - y0 + 1) <= COVER_MASK_TILES ? (uint32_t)__popcll(m) : area;
+}
+
 struct PreArgs {
     tcgs_camera cam;
     double campos[3];
@@ -188,6 +210,7 @@ struct PreArgs {
     int coverage;  // enum tcgs_coverage
     Rec *rec;
     CoverRec *cover;
+    unsigned long long *tmask;
     short4 *rect;
     uint32_t *touched;
     unsigned long long *keys;
@@ -455,7 +478,11 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
                         rc.g = col[1];
                         rc.b = col[2];
                         a.rec[i] = rc;
-                        if (a.coverage == TCGS_COVER_ELLIPSE) a.cover[i] = make_cover(rc);  // binning's row spans
+                        if (a.coverage == TCGS_COVER_ELLIPSE) {  // binning's row spans; small rectangles as masks
+                            touched = exact_cover_record(rc.mx, rc.mx_lo, rc.my, rc.my_lo, rc.s11, rc.s12, rc.s22,
+                                                         rc.ln_o, x0, y0, x1, y1, a.cover + i, a.tmask + i, touched);
+                            if (!touched) key = ~0ull;  // the ellipse reaches none of its tiles
+                        }
                     }
                 }
             }
@@ -523,6 +550,7 @@ PreArgs view_args(const tcgs_scene &scene, const tcgs_camera &cam, const Band &b
     a.coverage = coverage;
     a.rec = at<Rec>(ws, L.rec);
     a.cover = at<CoverRec>(ws, L.cover);
+    a.tmask = at<unsigned long long>(ws, L.tmask);
     a.rect = at<short4>(ws, L.rect);
     a.touched = at<uint32_t>(ws, L.touched);
     a.keys = at<unsigned long long>(ws, L.key_src);

@@ -78,19 +78,22 @@ __host__ __device__ inline CoverRec make_cover(const Rec &r) {
     c.mx = (float)((double)r.mx + (double)r.mx_lo);
     c.my = (float)((double)r.my + (double)r.my_lo);
     c.b_a = c.det_a = c.ry = c.dys = c.pad = 0.0f;
-    const double a = r.s11, b = r.s12, cc = r.s22;
-    const double Q = 2.0 * ((double)r.ln_o + 5.541263545158426) + COVER_Q_MARGIN;
-    const double det = a * cc - b * b;
-    if (!(Q > 0.0)) {
+    const float a = r.s11, b = r.s12, cc = r.s22;
+    const float Q = 2.0f * (r.ln_o + 5.541263545158426f) + (float)COVER_Q_MARGIN;
+    // the determinant in float64 (exact products of the fp32 entries): it is the one cancellation-prone
+    // quantity; everything derived from it below keeps fp32 relative precision
+    const float det = (float)((double)a * (double)cc - (double)b * (double)b);
+    if (!(Q > 0.0f)) {
         c.mode = 2;
-    } else if (!(a > 0.0 && cc > 0.0 && det > 0.0) || !isfinite(det)) {
+    } else if (!(a > 0.0f && cc > 0.0f && det > 0.0f) || !isfinite(det)) {
         c.mode = 1;
     } else {
         c.mode = 0;
-        c.b_a = (float)(b / a);
-        c.det_a = (float)(det / (a * a));
-        c.ry = (float)sqrt(Q * a / det);
-        c.dys = (float)(-b * sqrt(Q / (cc * det)));
+        const float inv_a = 1.0f / a;
+        c.b_a = b * inv_a;
+        c.det_a = det * inv_a * inv_a;
+        c.ry = sqrtf(Q * a / det);
+        c.dys = -b * sqrtf(Q / (cc * det));
     }
     return c;
 }
@@ -99,19 +102,30 @@ __host__ __device__ inline CoverRec make_cover(const Rec &r) {
 // the ellipse over the row's pixel strip is [min of the left boundary, max of the right boundary]: the right
 // boundary -b_a dy + hw(dy) is concave in dy, so its maximum over the strip is at the rightmost point's dy
 // clamped into the strip (and symmetrically on the left).  hw = sqrt(det_a (ry - |dy|)(ry + |dy|)).
+// one MUFU instruction, identical in every translation unit (relative error ~2^-22, far inside the margins)
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// (explicitly rounded operations: K1 and binning are compiled with different FMA contraction, and both must
+// see the same spans)
 __device__ __forceinline__ bool cover_row(const CoverRec &c, int ty, int x0, int x1, int &lo, int &hi) {
     lo = x0;
     hi = x1;
     if (c.mode) return c.mode == 1;
-    const float ylo = fmaxf(16.0f * ty - c.my - COVER_PX_MARGIN, -c.ry);
-    const float yhi = fminf(16.0f * ty + 15.0f - c.my + COVER_PX_MARGIN, c.ry);
+    const float ylo = fmaxf(__fsub_rn(__fsub_rn(16.0f * ty, c.my), COVER_PX_MARGIN), -c.ry);
+    const float yhi = fminf(__fadd_rn(__fsub_rn(__fadd_rn(16.0f * ty, 15.0f), c.my), COVER_PX_MARGIN), c.ry);
     if (ylo > yhi) return false;
     const float yr = fminf(fmaxf(c.dys, ylo), yhi), yl = fminf(fmaxf(-c.dys, ylo), yhi);
     const float ar = fabsf(yr), al = fabsf(yl);
-    const float xr = -c.b_a * yr + sqrtf(fmaxf(c.det_a * (c.ry - ar) * (c.ry + ar), 0.0f));
-    const float xl = -c.b_a * yl - sqrtf(fmaxf(c.det_a * (c.ry - al) * (c.ry + al), 0.0f));
-    const float fl = floorf((c.mx + xl - COVER_PX_MARGIN) * (1.0f / 16.0f));
-    const float fh = floorf((c.mx + xr + COVER_PX_MARGIN) * (1.0f / 16.0f));
+    const float hr = sqrt_approx(fmaxf(__fmul_rn(__fmul_rn(c.det_a, __fsub_rn(c.ry, ar)), __fadd_rn(c.ry, ar)), 0.0f));
+    const float hl = sqrt_approx(fmaxf(__fmul_rn(__fmul_rn(c.det_a, __fsub_rn(c.ry, al)), __fadd_rn(c.ry, al)), 0.0f));
+    const float xr = __fadd_rn(__fmul_rn(-c.b_a, yr), hr);
+    const float xl = __fsub_rn(__fmul_rn(-c.b_a, yl), hl);
+    const float fl = floorf(__fmul_rn(__fsub_rn(__fadd_rn(c.mx, xl), COVER_PX_MARGIN), 1.0f / 16.0f));
+    const float fh = floorf(__fmul_rn(__fadd_rn(__fadd_rn(c.mx, xr), COVER_PX_MARGIN), 1.0f / 16.0f));
     lo = fl > (float)x0 ? (int)fl : x0;
     hi = fh < (float)x1 ? (int)fh : x1;
     return lo <= hi;
@@ -142,7 +156,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 struct Layout {
-    size_t counters, sort_state[2], rec, cover, rect, touched, key_src, key64[2], long_runs, fix_scratch, idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
+    size_t counters, sort_state[2], rec, cover, tmask, rect, touched, key_src, key64[2], long_runs, fix_scratch, idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
     size_t blocksum, lb_depth, lb_tile, tkey[2], tval[2], ranges, total;
     size_t zero_begin, zero_bytes;  // sort state, cleared at the start of every binning
     static Layout make(int64_t P, int W, int H, int64_t cap) {
@@ -161,6 +175,7 @@ struct Layout {
         L.lb_tile = take(sizeof(uint32_t) * RADIX * TILE_MAX_PASSES * (size_t)div_up((int64_t)cn, OS_THREADS * TILEKEY_IPT));
         L.rec = take(sizeof(Rec) * Pn);
         L.cover = take(sizeof(CoverRec) * Pn);
+        L.tmask = take(sizeof(uint64_t) * Pn);
         L.rect = take(sizeof(short4) * Pn);
         L.touched = take(sizeof(uint32_t) * Pn);
         L.key_src = take(sizeof(uint64_t) * Pn);
@@ -244,6 +259,30 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
+}
+
+// Exact coverage of a rectangle of at most 64 tiles as a row-major bit mask (bit (ty - y0) w + (tx - x0)):
+// K1 builds it once so that binning counts and expands with popcounts, no float work.  Larger rectangles
+// return 0 and binning walks their rows with cover_row.
+constexpr int COVER_MASK_TILES = 64;
+__device__ __forceinline__ unsigned long long cover_mask(const CoverRec &c, int x0, int y0, int x1, int y1) {
+    const int w = x1 - x0 + 1;
+    if (w * (y1 - y0 + 1) > COVER_MASK_TILES) return 0ull;
+    unsigned long long m = 0ull;
+    for (int ty = y0; ty <= y1; ty++) {
+        int lo, hi;
+        if (cover_row(c, ty, x0, x1, lo, hi)) {
+            const int b0 = (ty - y0) * w + (lo - x0), n = hi - lo + 1;
+            m |= (n >= 64 ? ~0ull : ((1ull << n) - 1ull)) << b0;
+        }
+    }
+    return m;
+}
+// Rows [r0, r1] of a w-wide mask, shifted down so that row r0 becomes row 0.
+__device__ __forceinline__ unsigned long long mask_rows(unsigned long long m, int w, int r0, int r1) {
+    const int b0 = r0 * w, n = (r1 - r0 + 1) * w;
+    m >>= b0;
+    return n >= 64 ? m : (m & ((1ull << n) - 1ull));
 }
 
 __device__ __forceinline__ float rcp_approx(float x) {

@@ -480,33 +480,27 @@ __device__ __forceinline__ uint32_t cover_count(const CoverRec &cs, short4 q) {
     return n;
 }
 
-// Exact coverage of Gaussian g clipped to the band: its count, and -- for rectangles of at most
-// COVER_MASK_TILES tiles -- its K1 mask re-based to the clipped rectangle q (mask 0 with a count: walk rows).
-__device__ __forceinline__ uint32_t exact_cover(const CoverRec *cover, const unsigned long long *tmask, uint32_t g,
-                                                short4 r, short4 q, unsigned long long &m) {
+// Exact coverage of Gaussian g clipped to the band (q = band_rect(r)): its count, and -- for rectangles of at
+// most COVER_MASK_TILES tiles -- its tile mask re-based to q (mask 0 with a count: walk the rows).
+__device__ __forceinline__ uint32_t exact_cover(const Rec *rec, uint32_t g, short4 r, short4 q, unsigned long long &m) {
     m = 0ull;
     if (q.y > q.w) return 0u;
+    const CoverRec cs = make_cover(rec[g]);
     const int w = r.z - r.x + 1;
     if (w * (r.w - r.y + 1) <= COVER_MASK_TILES) {
-        m = mask_rows(tmask[g], w, q.y - r.y, q.w - r.y);
+        m = mask_rows(cover_mask(cs, r.x, r.y, r.z, r.w), w, q.y - r.y, q.w - r.y);
         return (uint32_t)__popcll(m);
     }
-    return cover_count(cover[g], q);
+    return cover_count(cs, q);
 }
 
+// EXACT: opt-in TCGS_COVER_ELLIPSE (separate instantiation, so the default keeps its registers): also stores
+// each Gaussian's band-clipped tile mask in depth order for K4.
 template <bool EXACT>
-__device__ __forceinline__ uint32_t splat_count(const CoverRec *cover, const unsigned long long *tmask, uint32_t g,
-                                                short4 r, int y0, int y1) {
-    if (!EXACT) return band_count(r, y0, y1);
-    unsigned long long m;
-    return exact_cover(cover, tmask, g, r, band_rect(r, y0, y1), m);
-}
-
-template <bool EXACT>  // EXACT: opt-in TCGS_COVER_ELLIPSE (separate instantiation: the default keeps its registers)
 __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx0, const uint32_t *idx1,
                                                              const DevCounters *ctr, const uint32_t *touched,
-                                                             const short4 *rect, const CoverRec *cover,
-                                                             const unsigned long long *tmask,
+                                                             const short4 *rect, const Rec *rec,
+                                                             unsigned long long *tmask,
                                                              int band_y0, int band_y1,
                                                              int64_t P, unsigned long long *blocksum) {
     const uint32_t *order = ctr->depth_cur ? idx1 : idx0;
@@ -517,7 +511,16 @@ __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx
         const int64_t i = beg + u * DUP_THREADS + threadIdx.x;
         if (i < P) {
             const uint32_t g = order[i];
-            if (touched[g]) s += splat_count<EXACT>(cover, tmask, g, rect[g], band_y0, band_y1);
+            if (!EXACT) {
+                if (touched[g]) s += band_count(rect[g], band_y0, band_y1);
+            } else {
+                unsigned long long m = 0ull;
+                if (touched[g]) {
+                    const short4 r = rect[g];
+                    s += exact_cover(rec, g, r, band_rect(r, band_y0, band_y1), m);
+                }
+                tmask[i] = m;
+            }
         }
     }
 #pragma unroll
@@ -572,7 +575,7 @@ __global__ void __launch_bounds__(1024) count_scan(unsigned long long *blocksum,
 template <typename KT, bool EXACT>
 __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *idx0, const uint32_t *idx1,
                                                               const DevCounters *ctr, const uint32_t *touched,
-                                                              const short4 *rect, const CoverRec *cover,
+                                                              const short4 *rect, const Rec *rec,
                                                               const unsigned long long *tmask, int64_t P,
                                                               const unsigned long long *blockoff, int tiles_x,
                                                               int band_y0, int band_y1, int64_t cap, KT *tkey,
@@ -603,7 +606,10 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                 const short4 r = rect[g];
                 q = band_rect(r, band_y0, band_y1);
                 c = q.x <= q.z && q.y <= q.w ? (uint32_t)((q.z - q.x + 1) * (q.w - q.y + 1)) : 0u;
-                if (c && exact) c = exact_cover(cover, tmask, g, r, q, m);
+                if (c && exact) {  // K3's mask (depth order, coalesced); rows for large rectangles
+                    m = tmask[i];
+                    c = m ? (uint32_t)__popcll(m) : cover_count(make_cover(rec[g]), q);
+                }
                 if (!c) q = make_short4(0, 0, -1, -1);
             }
         }
@@ -622,7 +628,7 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                     }
                 } else {
                     CoverRec cs;
-                    if (exact && c) cs = cover[g];
+                    if (exact && c) cs = make_cover(rec[g]);
                     for (int ty = q.y; ty <= q.w; ty++) {
                         const uint32_t row = (uint32_t)((ty - band_y0) * tiles_x);
                         int lo = q.x, hi = q.z;
@@ -653,7 +659,7 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                     }
                 } else if (exact) {  // row by row: every lane computes the (uniform) row span
                     const int by1 = __shfl_sync(0xffffffffu, (int)q.w, src);
-                    const CoverRec cs = cover[bg];
+                    const CoverRec cs = make_cover(rec[bg]);
                     uint32_t o = bex;
                     for (int ty = by0; ty <= by1; ty++) {
                         int lo, hi;
@@ -705,7 +711,7 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                     ty = qq.y + b / w;
                     tx = qq.x + b % w;
                 } else if (exact) {  // walk the rows to the kk-th covered tile
-                    const CoverRec cs = cover[gid[lo]];
+                    const CoverRec cs = make_cover(rec[gid[lo]]);
                     for (ty = qq.y; ty <= qq.w; ty++) {
                         int rlo, rhi;
                         if (!cover_row(cs, ty, qq.x, qq.z, rlo, rhi)) continue;
@@ -797,7 +803,7 @@ __global__ void pack_ranges(const int64_t *offsets, int band_tile0, int n_tiles,
 // Splats per tile row of the whole frame (sum over Gaussians of the covered tiles in that row), from K1's
 // frame-clipped rectangles: the replicated input of the tile-band partition (multi-GPU).
 __global__ void __launch_bounds__(256) row_counts_kernel(int64_t P, const uint32_t *touched, const short4 *rect,
-                                                         const CoverRec *cover, int coverage, int tiles_y,
+                                                         const Rec *rec, int coverage, int tiles_y,
                                                          unsigned long long *out) {
     constexpr int SMEM_ROWS = 4096;
     __shared__ unsigned long long h[SMEM_ROWS];
@@ -809,7 +815,7 @@ __global__ void __launch_bounds__(256) row_counts_kernel(int64_t P, const uint32
         if (!touched[i]) continue;
         const short4 q = rect[i];
         if (coverage == TCGS_COVER_ELLIPSE) {
-            const CoverRec cs = cover[i];
+            const CoverRec cs = make_cover(rec[i]);
             for (int y = q.y; y <= q.w; y++) {
                 int lo, hi;
                 if (cover_row(cs, y, q.x, q.z, lo, hi))
@@ -843,7 +849,7 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     const bool exact = band.coverage == TCGS_COVER_ELLIPSE;
     (exact ? count_upsweep<true> : count_upsweep<false>)<<<nblk, DUP_THREADS, 0, st>>>(
         at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr, at<uint32_t>(ws, L.touched),
-        at<short4>(ws, L.rect), at<CoverRec>(ws, L.cover), at<unsigned long long>(ws, L.tmask), band.y0, band.y1, P,
+        at<short4>(ws, L.rect), at<Rec>(ws, L.rec), at<unsigned long long>(ws, L.tmask), band.y0, band.y1, P,
         blocksum);
     note_launch();
     count_scan<<<1, 1024, 0, st>>>(blocksum, nblk, ctr, cap);
@@ -851,7 +857,7 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     note_launch();
     (exact ? duplicate_keys<KT, true> : duplicate_keys<KT, false>)<<<nblk, DUP_THREADS, 0, st>>>(
         at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr, at<uint32_t>(ws, L.touched),
-        at<short4>(ws, L.rect), at<CoverRec>(ws, L.cover), at<unsigned long long>(ws, L.tmask), P, blocksum,
+        at<short4>(ws, L.rect), at<Rec>(ws, L.rec), at<unsigned long long>(ws, L.tmask), P, blocksum,
         band.tiles_x, band.y0, band.y1, cap, tk0, tv0);
     // K5
     note_launch();
@@ -876,7 +882,7 @@ cudaError_t launch_row_counts(int64_t P, const Band &band, const void *ws, const
     const int64_t blocks = div_up(P, 256 * 8);
     note_launch();
     row_counts_kernel<<<(unsigned)(blocks < 4 * 148 ? blocks : 4 * 148), 256, 0, st>>>(
-        P, at<uint32_t>(ws, L.touched), at<short4>(ws, L.rect), at<CoverRec>(ws, L.cover), band.coverage,
+        P, at<uint32_t>(ws, L.touched), at<short4>(ws, L.rect), at<Rec>(ws, L.rec), band.coverage,
         band.tiles_y,
         reinterpret_cast<unsigned long long *>(out));
     return cudaGetLastError();

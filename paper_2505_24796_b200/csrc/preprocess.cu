@@ -178,28 +178,6 @@ __device__ void sh_color(const T *sh, int deg, double dx, double dy, double dz, 
     out[2] = fminf(fmaxf(r2 + 0.5f, 0.0f), 1.0f);
 }
 
-// Exact coverage records of one Gaussian (opt-in TCGS_COVER_ELLIPSE), out of line so that the default path's
-// register allocation does not pay for it.  Returns the touched count: the mask's popcount for rectangles of
-// at most COVER_MASK_TILES tiles, otherwise the rectangle's area (binning walks its rows).
-__device__ __noinline__ uint32_t exact_cover_record(float mx, float mx_lo, float my, float my_lo, float s11, float s12,
-                                                    float s22, float ln_o, int x0, int y0, int x1, int y1,
-                                                    CoverRec *cover, unsigned long long *tmask, uint32_t area) {
-    Rec rc;
-    rc.mx = mx;
-    rc.mx_lo = mx_lo;
-    rc.my = my;
-    rc.my_lo = my_lo;
-    rc.s11 = s11;
-    rc.s12 = s12;
-    rc.s22 = s22;
-    rc.ln_o = ln_o;
-    const CoverRec cr = make_cover(rc);
-    *cover = cr;
-    const unsigned long long m = cover_mask(cr, x0, y0, x1, y1);
-    *tmask = m;
-    return (x1 - x0 + 1) * (y1 - y0 + 1) <= COVER_MASK_TILES ? (uint32_t)__popcll(m) : area;
-}
-
 struct PreArgs {
     tcgs_camera cam;
     double campos[3];
@@ -209,8 +187,6 @@ struct PreArgs {
     int debug;
     int coverage;  // enum tcgs_coverage
     Rec *rec;
-    CoverRec *cover;
-    unsigned long long *tmask;
     short4 *rect;
     uint32_t *touched;
     unsigned long long *keys;
@@ -429,7 +405,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
                         // opt-in, not the reference's coverage: keep only tiles the
                         // alpha >= 1/255 ellipse q <= 2 ln(255 o) can reach -- its bounding box, with margins
                         // above every rounding of K7's exponent -- inside the reference's square (the exact
-                        // mode then trims each row in binning).  Splats it drops have no live fragment, so
+                        // mode then keeps only the tiles the ellipse touches, in binning).  Splats it drops have no live fragment, so
                         // the image is unchanged; N and f_cull shrink.
                         const double Qc = 2.0 * (log(ld(opac, l)) + 5.541263545158426) + COVER_Q_MARGIN;
                         if (Qc > 0.0) {
@@ -478,11 +454,6 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
                         rc.g = col[1];
                         rc.b = col[2];
                         a.rec[i] = rc;
-                        if (a.coverage == TCGS_COVER_ELLIPSE) {  // binning's row spans; small rectangles as masks
-                            touched = exact_cover_record(rc.mx, rc.mx_lo, rc.my, rc.my_lo, rc.s11, rc.s12, rc.s22,
-                                                         rc.ln_o, x0, y0, x1, y1, a.cover + i, a.tmask + i, touched);
-                            if (!touched) key = ~0ull;  // the ellipse reaches none of its tiles
-                        }
                     }
                 }
             }
@@ -549,8 +520,6 @@ PreArgs view_args(const tcgs_scene &scene, const tcgs_camera &cam, const Band &b
     a.debug = debug;
     a.coverage = coverage;
     a.rec = at<Rec>(ws, L.rec);
-    a.cover = at<CoverRec>(ws, L.cover);
-    a.tmask = at<unsigned long long>(ws, L.tmask);
     a.rect = at<short4>(ws, L.rect);
     a.touched = at<uint32_t>(ws, L.touched);
     a.keys = at<unsigned long long>(ws, L.key_src);

@@ -57,9 +57,10 @@ struct __align__(16) Rec {
 // ---- opt-in tile coverage.  A fragment can pass EarlyCull only inside the ellipse
 // q(d) = s11 dx^2 + 2 s12 dx dy + s22 dy^2 <= Q = 2 ln(255 o) (d = pixel - mean).  The tests below keep every
 // tile that ellipse, grown by margins far above K7's exponent rounding, touches -- so only splats with no
-// live fragment are dropped and the image is unchanged.  K1 derives each Gaussian's row-span parameters in
-// float64 from the render record's fp32 conic and log-opacity (what K7 evaluates), so needle-thin ellipses
-// keep their exact extent; binning evaluates them per tile row in fp32 without cancellation.
+// live fragment are dropped and the image is unchanged.  The row-span parameters come from the render
+// record's fp32 conic and log-opacity (what K7 evaluates), with the one cancellation-prone quantity (the
+// determinant) in float64, so needle-thin ellipses keep their exact extent; rows are evaluated in fp32
+// without cancellation.
 constexpr double COVER_Q_MARGIN = 0.2;   // in q (0.1 in beta = ln alpha)
 constexpr float COVER_PX_MARGIN = 0.5f;  // pixels, on every side
 
@@ -156,7 +157,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 struct Layout {
-    size_t counters, sort_state[2], rec, cover, tmask, rect, touched, key_src, key64[2], long_runs, fix_scratch, idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
+    size_t counters, sort_state[2], rec, tmask, rect, touched, key_src, key64[2], long_runs, fix_scratch, idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
     size_t blocksum, lb_depth, lb_tile, tkey[2], tval[2], ranges, total;
     size_t zero_begin, zero_bytes;  // sort state, cleared at the start of every binning
     static Layout make(int64_t P, int W, int H, int64_t cap) {
@@ -174,8 +175,7 @@ struct Layout {
         L.lb_depth = take(sizeof(uint32_t) * RADIX * MAX_PASSES * (size_t)div_up((int64_t)Pn, OS_THREADS * DEPTH_IPT));
         L.lb_tile = take(sizeof(uint32_t) * RADIX * TILE_MAX_PASSES * (size_t)div_up((int64_t)cn, OS_THREADS * TILEKEY_IPT));
         L.rec = take(sizeof(Rec) * Pn);
-        L.cover = take(sizeof(CoverRec) * Pn);
-        L.tmask = take(sizeof(uint64_t) * Pn);
+        L.tmask = take(sizeof(uint64_t) * Pn);  // exact coverage: tile masks in depth order (K3 -> K4)
         L.rect = take(sizeof(short4) * Pn);
         L.touched = take(sizeof(uint32_t) * Pn);
         L.key_src = take(sizeof(uint64_t) * Pn);
@@ -262,8 +262,8 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 // Exact coverage of a rectangle of at most 64 tiles as a row-major bit mask (bit (ty - y0) w + (tx - x0)):
-// K1 builds it once so that binning counts and expands with popcounts, no float work.  Larger rectangles
-// return 0 and binning walks their rows with cover_row.
+// K3 builds it once (in depth order) so that K4 expands with popcounts, no float work.  Larger rectangles
+// return 0 and K3/K4 walk their rows with cover_row.
 constexpr int COVER_MASK_TILES = 64;
 __device__ __forceinline__ unsigned long long cover_mask(const CoverRec &c, int x0, int y0, int x1, int y1) {
     const int w = x1 - x0 + 1;

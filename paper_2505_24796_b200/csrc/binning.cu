@@ -30,6 +30,10 @@
 // host synchronisation (graph-capturable).
 #include <algorithm>
 
+#ifndef TCGS_TILE_DIGITS_EVEN
+#define TCGS_TILE_DIGITS_EVEN 0  // tile-key radix: 1 = equal digit widths per pass (measured: no gain over 8-bit)
+#endif
+
 #include "tcgs_internal.cuh"
 
 namespace tcgs {
@@ -67,11 +71,12 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t *war
 
 // Lanes of the warp holding the same 8-bit digit (invalid items: digit >= RADIX match only each other).
 // Nine ballots instead of MATCH.ANY, whose throughput is far lower.
+template <int DB = RADIX_BITS>  // digit bits (<= RADIX_BITS); invalid items carry d = RADIX
 __device__ __forceinline__ unsigned warp_peers(int d) {
     unsigned peers = __ballot_sync(0xffffffffu, d < RADIX);
     if (d >= RADIX) peers = ~peers;
 #pragma unroll
-    for (int b = 0; b < RADIX_BITS; b++) {
+    for (int b = 0; b < DB; b++) {
         const bool bit = (d >> b) & 1;
         const unsigned m = __ballot_sync(0xffffffffu, bit);
         peers &= bit ? m : ~m;
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(256) sort_plan(SortState *ss, int npass, const
 //                   digit base (scan of the totals) + row prefix + local rank, scatter staged
 //                   through shared memory
 //                   so the stores are coalesced runs.
-template <typename KT, int IPT>
+template <typename KT, int IPT, int DB>
 __global__ void __launch_bounds__(OS_THREADS) radix_upsweep(const KT *k0, const KT *k1, const unsigned long long *n_dev,
                                                             int64_t n_host, int64_t cap, int pass, int shift,
                                                             const SortState *ss, uint32_t *table, int64_t T) {
@@ -300,7 +305,7 @@ __global__ void __launch_bounds__(OS_THREADS) radix_upsweep(const KT *k0, const 
 #pragma unroll
     for (int it = 0; it < IPT; it++) {
         const int64_t idx = seg + it * 32 + lane;
-        if (idx < n) atomicAdd(&wh[warp][(unsigned)(k[it] >> shift) & (RADIX - 1)], 1u);
+        if (idx < n) atomicAdd(&wh[warp][(unsigned)(k[it] >> shift) & ((1u << DB) - 1u)], 1u);
     }
     __syncthreads();
     const int d = tid;
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(256) radix_rowscan(const unsigned long long *n
     if (threadIdx.x == 0) ss->ghist[pass][blockIdx.x] = carry;  // digit total
 }
 
-template <typename KT, int IPT>
+template <typename KT, int IPT, int DB>  // DB digit bits: digits >= 1 << DB stay empty
 __global__ void __launch_bounds__(OS_THREADS, 3) radix_downsweep(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1,
                                                               const unsigned long long *n_dev, int64_t n_host,
                                                               int64_t cap, int pass, int shift, const SortState *ss,
@@ -383,8 +388,8 @@ __global__ void __launch_bounds__(OS_THREADS, 3) radix_downsweep(KT *k0, KT *k1,
 #pragma unroll
     for (int it = 0; it < IPT; it++) {
         const bool valid = seg + it * 32 + lane < n;
-        const int d = valid ? (int)((k[it] >> shift) & (RADIX - 1)) : RADIX;
-        const unsigned peers = warp_peers(d);
+        const int d = valid ? (int)((k[it] >> shift) & ((1u << DB) - 1u)) : RADIX;
+        const unsigned peers = warp_peers<DB>(d);
         uint32_t b = 0;
         if (d < RADIX) b = wh[warp][d];
         __syncwarp();
@@ -418,7 +423,7 @@ __global__ void __launch_bounds__(OS_THREADS, 3) radix_downsweep(KT *k0, KT *k1,
     __syncthreads();
     for (int i = tid; i < tile_n; i += OS_THREADS) {
         const KT key = skey[i];
-        const uint32_t pos = gofs[(unsigned)(key >> shift) & (RADIX - 1)] + (uint32_t)i;
+        const uint32_t pos = gofs[(unsigned)(key >> shift) & ((1u << DB) - 1u)] + (uint32_t)i;
         kout[pos] = key;
         vout[pos] = sval[i];
     }
@@ -429,17 +434,18 @@ constexpr int downsweep_smem() {
     return (int)((sizeof(KT) + sizeof(uint32_t)) * OS_THREADS * IPT);
 }
 
-template <typename KT, int IPT>
-cudaError_t launch_radix_pass(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const unsigned long long *n_dev,
-                              int64_t n_host, int64_t cap, int pass, SortState *ss, uint32_t *table_all,
-                              cudaStream_t st) {
+template <typename KT, int IPT, int DB>
+cudaError_t launch_radix_pass_db(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const unsigned long long *n_dev,
+                                 int64_t n_host, int64_t cap, int pass, int shift, SortState *ss, uint32_t *table_all,
+                                 cudaStream_t st) {
     static bool configured_dev[TCGS_MAX_DEVICES] = {};
     bool &configured = configured_dev[current_device()];
     constexpr int smem = downsweep_smem<KT, IPT>();
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(radix_downsweep<KT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(radix_downsweep<KT, IPT, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(radix_downsweep<KT, IPT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+            e = cudaFuncSetAttribute(radix_downsweep<KT, IPT, DB>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      (int)cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
         configured = true;
@@ -447,15 +453,27 @@ cudaError_t launch_radix_pass(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const 
     const int64_t tiles = div_up(n_dev ? cap : n_host, OS_THREADS * IPT);
     const unsigned grid = (unsigned)(tiles > 0 ? tiles : 1);
     uint32_t *table = table_all + (int64_t)pass * RADIX * tiles;
-    const int shift = RADIX_BITS * pass;
     note_launch();
-    radix_upsweep<KT, IPT><<<grid, OS_THREADS, 0, st>>>(k0, k1, n_dev, n_host, cap, pass, shift, ss, table, tiles);
+    radix_upsweep<KT, IPT, DB><<<grid, OS_THREADS, 0, st>>>(k0, k1, n_dev, n_host, cap, pass, shift, ss, table, tiles);
     note_launch();
     radix_rowscan<IPT><<<RADIX, 256, 0, st>>>(n_dev, n_host, cap, pass, ss, table, tiles);
     note_launch();
-    radix_downsweep<KT, IPT><<<grid, OS_THREADS, smem, st>>>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table,
-                                                             tiles);
+    radix_downsweep<KT, IPT, DB><<<grid, OS_THREADS, smem, st>>>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss,
+                                                                 table, tiles);
     return cudaGetLastError();
+}
+
+// One pass on digit bits [shift, shift + db) (db <= RADIX_BITS): fewer digit bits, fewer warp ballots.
+template <typename KT, int IPT>
+cudaError_t launch_radix_pass(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const unsigned long long *n_dev,
+                              int64_t n_host, int64_t cap, int pass, int shift, int db, SortState *ss,
+                              uint32_t *table_all, cudaStream_t st) {
+    switch (db) {
+        case 5: return launch_radix_pass_db<KT, IPT, 5>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st);
+        case 6: return launch_radix_pass_db<KT, IPT, 6>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st);
+        case 7: return launch_radix_pass_db<KT, IPT, 7>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st);
+        default: return launch_radix_pass_db<KT, IPT, 8>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st);
+    }
 }
 
 // ---------------------------------------------------------------- K3 / K4
@@ -862,9 +880,13 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     // K5
     note_launch();
     sort_plan<<<1, 256, 0, st>>>(ss_tile, npass, &ctr->n_splats, 0, cap, nullptr, 0, &ctr->tile_cur);
-    for (int p = 0; p < npass; p++) {
-        cudaError_t e = launch_radix_pass<KT, TILEKEY_IPT>(tk0, tk1, tv0, tv1, &ctr->n_splats, 0, cap, p, ss_tile,
-                                                          at<uint32_t>(ws, L.lb_tile), st);
+    // the key's bits split as evenly as possible over the passes (13 bits: 7 + 6, not 8 + 5)
+    const int db0 = TCGS_TILE_DIGITS_EVEN ? (bits + npass - 1) / npass : RADIX_BITS;
+    for (int p = 0, shift = 0; p < npass; p++) {
+        const int db = std::min(db0, bits - shift);
+        cudaError_t e = launch_radix_pass<KT, TILEKEY_IPT>(tk0, tk1, tv0, tv1, &ctr->n_splats, 0, cap, p, shift, db,
+                                                          ss_tile, at<uint32_t>(ws, L.lb_tile), st);
+        shift += db;
         if (e != cudaSuccess) return e;
     }
     // K6
@@ -922,7 +944,8 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
         note_launch();
         sort_plan<<<1, 256, 0, st>>>(ss_depth, DEPTH_PASSES, nullptr, P, P, &ctr->key_range, 1, &ctr->depth_cur);
         for (int p = 0; p < DEPTH_PASSES; p++) {
-            e = launch_radix_pass<uint32_t, DEPTH_IPT>(k0, k1, i0, i1, nullptr, P, P, p, ss_depth,
+            e = launch_radix_pass<uint32_t, DEPTH_IPT>(k0, k1, i0, i1, nullptr, P, P, p, RADIX_BITS * p, RADIX_BITS,
+                                                       ss_depth,
                                                       at<uint32_t>(ws, L.lb_depth), st);
             if (e != cudaSuccess) return e;
         }

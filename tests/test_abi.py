@@ -109,3 +109,17 @@ def test_product_package_never_touches_the_oracle():
                 assert not re.search(r"^\s*(from|import)\s+oracle", text, flags=re.M), f
                 assert not re.search(r"#include\s*[<\"].*oracle", text), f
                 assert not re.search(r"CDLL\(.*oracle|libtcgs_oracle", text), f
+
+
+def test_c_example_compiles_and_links(lib):
+    """examples/render_c.c uses only include/tcgs.h and links libtcgs.so from plain C (gcc, C11)."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None or shutil.which("make") is None:
+        pytest.skip("no gcc/make")
+    ex = os.path.join(ROOT, "examples")
+    r = subprocess.run(["make", "-B", "-C", ex], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "warning" not in r.stderr.lower(), r.stderr
+    assert os.access(os.path.join(ex, "render_c"), os.X_OK)

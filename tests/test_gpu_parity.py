@@ -614,3 +614,60 @@ def test_full_size_lists_and_band_pixels(renderers, cfg, scale, rows):
     n_mis, unexplained = explain_count_mismatches(g_cnt, cnt, o_off, o_ids, proj.mean2d, proj.inv_cov,
                                                   np.asarray(scene["opacities"], np.float64), cam.width, "hilo")
     assert not unexplained, (cfg, n_mis, unexplained[:5])
+
+
+def _c_example_scene(P):
+    """numpy mirror of examples/render_c.c's LCG scene (float32 arithmetic in the same order)."""
+    state = np.uint32(12345)
+    f32 = np.float32
+
+    def uni():
+        nonlocal state
+        state = np.uint32((int(state) * 1664525 + 1013904223) & 0xFFFFFFFF)
+        return f32(int(state) >> 8) * f32(1.0 / 16777216.0)
+
+    means = np.zeros((P, 3), f32)
+    scales = np.zeros((P, 3), f32)
+    rots = np.zeros((P, 4), f32)
+    opac = np.zeros(P, f32)
+    rgb = np.zeros((P, 3), f32)
+    for i in range(P):
+        z = f32(3) + f32(6) * uni()
+        means[i, 0] = (f32(2) * uni() - f32(1)) * z * f32(0.5)
+        means[i, 1] = (f32(2) * uni() - f32(1)) * z * f32(0.4)
+        means[i, 2] = z
+        for k in range(3):
+            scales[i, k] = f32(0.01) + f32(0.08) * uni()
+        q = [uni() - f32(0.5) for _ in range(4)]
+        n = f32(0)
+        for v in q:
+            n = n + v * v
+        n = np.sqrt(n, dtype=f32)
+        rots[i] = [v / n for v in q]
+        opac[i] = f32(0.1) + f32(0.8) * uni()
+        rgb[i] = [uni() for _ in range(3)]
+    return {"means": means, "scales": scales, "rotations": rots, "opacities": opac, "colors": rgb}
+
+
+def test_c_example_matches_python(tmp_path):
+    """The C caller (examples/render_c.c, include/tcgs.h only) renders the same frame and FragmentStats as the
+    Python API on the same scene, bit for bit."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "render_c")
+    if not os.access(exe, os.X_OK):
+        subprocess.run(["make", "-C", os.path.join(root, "examples")], check=True, capture_output=True)
+    P = 3000
+    out = tmp_path / "c.f32"
+    r = subprocess.run([exe, str(P), str(out)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    st_c = dict(kv.split("=") for kv in r.stdout.split())
+    img_c = np.fromfile(out, dtype=np.float32).reshape(192, 256, 3)
+    cam = synthetic.CameraSpec(np.eye(4), 1.2 * 256, 1.2 * 256, 128.0, 96.0, 256, 192, 0.2)
+    f = tcgs.Renderer("cuda", "tcgs").render_frame(tcgs.GaussianCloud.from_arrays(_c_example_scene(P), "cuda"), cam,
+                                                   timed=False)
+    assert np.array_equal(img_c, f.rgb.cpu().numpy())
+    assert int(st_c["N"]) == f.stats.n_splats and int(st_c["f_blend"]) == f.stats.f_blend
+    assert int(st_c["f_cull"]) == f.stats.f_cull and int(st_c["pixels_terminated"]) == f.stats.pixels_terminated

@@ -671,3 +671,23 @@ def test_c_example_matches_python(tmp_path):
     assert np.array_equal(img_c, f.rgb.cpu().numpy())
     assert int(st_c["N"]) == f.stats.n_splats and int(st_c["f_blend"]) == f.stats.f_blend
     assert int(st_c["f_cull"]) == f.stats.f_cull and int(st_c["pixels_terminated"]) == f.stats.pixels_terminated
+
+
+def test_frame_is_cuda_graph_capturable():
+    """A whole frame (K1..K7: ~25 launches, all counts on the device) captures into one CUDA graph; replays
+    give the frame and FragmentStats of an eager render."""
+    scene, cams = synthetic.config_scene("c2", 0.01)
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    r = tcgs.Renderer("cuda", "tcgs")
+    f = r.render_frame(cloud, cams[0], timed=False)  # sizes the workspace, configures the kernels
+    ref = (f.rgb.clone(), f.T.clone(), f.n_contrib.clone(), f.stats)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        rgb, T, cnt = r.launch(cloud, cams[0])
+    for _ in range(2):
+        rgb.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(rgb, ref[0]) and torch.equal(T, ref[1]) and torch.equal(cnt, ref[2])
+        rc, fs = r.read_stats(cloud.P)
+        assert rc == 0 and (fs.n_splats, fs.f_blend, fs.f_cull) == (ref[3].n_splats, ref[3].f_blend, ref[3].f_cull)

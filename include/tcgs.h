@@ -79,7 +79,7 @@ typedef struct tcgs_opts {
     int32_t tile_row_end;
     int32_t alpha_mode;     /* enum tcgs_alpha_mode */
     int32_t early_cull;     /* exp_calls accounting: 1 = EarlyCull (tensor_path.py:148-154), 0 = reference (raster.py:94) */
-    int32_t debug;          /* 1: K1 also stores float64 conic/depth for tcgs_copy_projection */
+    int32_t debug;          /* 1: K1 also stores the radius and float64 conic/depth for tcgs_copy_projection */
     int32_t coverage;       /* enum tcgs_coverage (K1's tile rectangle) */
 } tcgs_opts;
 

@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
 #pragma unroll
             for (int k = 0; k < 3; k++) t[k] = dot3_gemv(V[4 * k + 0], V[4 * k + 1], V[4 * k + 2], m0, m1, m2) + V[4 * k + 3];
             const double tz = t[2];
-            a.radius[i] = -1;
+            if (a.debug) a.radius[i] = -1;  // the radius only feeds tcgs_copy_projection (debug)
             if (!(tz > a.cam.near_plane)) {  // src/tilesplat/projection.py:76-78 (tz <= near culls)
                 dropped = true;
             } else {
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
                     dropped = true;
                 } else {
                     const double s11 = sc / det, s12 = -sb / det, s22 = sa / det;
-                    a.radius[i] = rad;
+                    if (a.debug) a.radius[i] = rad;
                     if (a.debug) {
                         a.dbg_conic[3 * i] = s11;
                         a.dbg_conic[3 * i + 1] = s12;

@@ -516,8 +516,7 @@ __device__ __forceinline__ uint32_t exact_cover(const Rec *rec, uint32_t g, shor
 // each Gaussian's band-clipped tile mask in depth order for K4.
 template <bool EXACT>
 __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx0, const uint32_t *idx1,
-                                                             const DevCounters *ctr, const uint32_t *touched,
-                                                             const short4 *rect, const Rec *rec,
+                                                             const DevCounters *ctr, const short4 *rect, const Rec *rec,
                                                              unsigned long long *tmask,
                                                              int band_y0, int band_y1,
                                                              int64_t P, unsigned long long *blocksum) {
@@ -530,13 +529,11 @@ __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx
         if (i < P) {
             const uint32_t g = order[i];
             if (!EXACT) {
-                if (touched[g]) s += band_count(rect[g], band_y0, band_y1);
+                s += band_count(rect[g], band_y0, band_y1);  // (an empty rectangle: 0)
             } else {
                 unsigned long long m = 0ull;
-                if (touched[g]) {
-                    const short4 r = rect[g];
-                    s += exact_cover(rec, g, r, band_rect(r, band_y0, band_y1), m);
-                }
+                const short4 r = rect[g];
+                if (r.x <= r.z) s += exact_cover(rec, g, r, band_rect(r, band_y0, band_y1), m);
                 tmask[i] = m;
             }
         }
@@ -592,8 +589,7 @@ __global__ void __launch_bounds__(1024) count_scan(unsigned long long *blocksum,
 // consecutive splats (binary search of the slot in the shared inclusive scan).
 template <typename KT, bool EXACT>
 __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *idx0, const uint32_t *idx1,
-                                                              const DevCounters *ctr, const uint32_t *touched,
-                                                              const short4 *rect, const Rec *rec,
+                                                              const DevCounters *ctr, const short4 *rect, const Rec *rec,
                                                               const unsigned long long *tmask, int64_t P,
                                                               const unsigned long long *blockoff, int tiles_x,
                                                               int band_y0, int band_y1, int64_t cap, KT *tkey,
@@ -620,16 +616,14 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
         short4 q = make_short4(0, 0, -1, -1);
         if (i < P) {
             g = order[i];
-            if (touched[g]) {
-                const short4 r = rect[g];
-                q = band_rect(r, band_y0, band_y1);
-                c = q.x <= q.z && q.y <= q.w ? (uint32_t)((q.z - q.x + 1) * (q.w - q.y + 1)) : 0u;
-                if (c && exact) {  // K3's mask (depth order, coalesced); rows for large rectangles
-                    m = tmask[i];
-                    c = m ? (uint32_t)__popcll(m) : cover_count(make_cover(rec[g]), q);
-                }
-                if (!c) q = make_short4(0, 0, -1, -1);
+            const short4 r = rect[g];  // (an empty rectangle for Gaussians that touch no tile)
+            q = band_rect(r, band_y0, band_y1);
+            c = q.x <= q.z && q.y <= q.w ? (uint32_t)((q.z - q.x + 1) * (q.w - q.y + 1)) : 0u;
+            if (c && exact) {  // K3's mask (depth order, coalesced); rows for large rectangles
+                m = tmask[i];
+                c = m ? (uint32_t)__popcll(m) : cover_count(make_cover(rec[g]), q);
             }
+            if (!c) q = make_short4(0, 0, -1, -1);
         }
         uint32_t total;
         const uint32_t ex = block_excl_scan256(c, wt, &total);
@@ -820,7 +814,7 @@ __global__ void pack_ranges(const int64_t *offsets, int band_tile0, int n_tiles,
 
 // Splats per tile row of the whole frame (sum over Gaussians of the covered tiles in that row), from K1's
 // frame-clipped rectangles: the replicated input of the tile-band partition (multi-GPU).
-__global__ void __launch_bounds__(256) row_counts_kernel(int64_t P, const uint32_t *touched, const short4 *rect,
+__global__ void __launch_bounds__(256) row_counts_kernel(int64_t P, const short4 *rect,
                                                          const Rec *rec, int coverage, int tiles_y,
                                                          unsigned long long *out) {
     constexpr int SMEM_ROWS = 4096;
@@ -830,8 +824,8 @@ __global__ void __launch_bounds__(256) row_counts_kernel(int64_t P, const uint32
         for (int r = threadIdx.x; r < tiles_y; r += blockDim.x) h[r] = 0ull;
     __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-        if (!touched[i]) continue;
         const short4 q = rect[i];
+        if (q.x > q.z) continue;  // touches no tile
         if (coverage == TCGS_COVER_ELLIPSE) {
             const CoverRec cs = make_cover(rec[i]);
             for (int y = q.y; y <= q.w; y++) {
@@ -866,7 +860,7 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     note_launch();
     const bool exact = band.coverage == TCGS_COVER_ELLIPSE;
     (exact ? count_upsweep<true> : count_upsweep<false>)<<<nblk, DUP_THREADS, 0, st>>>(
-        at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr, at<uint32_t>(ws, L.touched),
+        at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr,
         at<short4>(ws, L.rect), at<Rec>(ws, L.rec), at<unsigned long long>(ws, L.tmask), band.y0, band.y1, P,
         blocksum);
     note_launch();
@@ -874,7 +868,7 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     // K4
     note_launch();
     (exact ? duplicate_keys<KT, true> : duplicate_keys<KT, false>)<<<nblk, DUP_THREADS, 0, st>>>(
-        at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr, at<uint32_t>(ws, L.touched),
+        at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr,
         at<short4>(ws, L.rect), at<Rec>(ws, L.rec), at<unsigned long long>(ws, L.tmask), P, blocksum,
         band.tiles_x, band.y0, band.y1, cap, tk0, tv0);
     // K5
@@ -904,7 +898,7 @@ cudaError_t launch_row_counts(int64_t P, const Band &band, const void *ws, const
     const int64_t blocks = div_up(P, 256 * 8);
     note_launch();
     row_counts_kernel<<<(unsigned)(blocks < 4 * 148 ? blocks : 4 * 148), 256, 0, st>>>(
-        P, at<uint32_t>(ws, L.touched), at<short4>(ws, L.rect), at<Rec>(ws, L.rec), band.coverage,
+        P, at<short4>(ws, L.rect), at<Rec>(ws, L.rec), band.coverage,
         band.tiles_y,
         reinterpret_cast<unsigned long long *>(out));
     return cudaGetLastError();

@@ -188,7 +188,6 @@ struct PreArgs {
     int coverage;  // enum tcgs_coverage
     Rec *rec;
     short4 *rect;
-    uint32_t *touched;
     unsigned long long *keys;
     uint32_t *idx;
     int32_t *radius;
@@ -313,6 +312,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
         const bool in_range = i < a.P;
         unsigned long long key = ~0ull;  // "touches nothing": rewritten by depth_key_fix
         uint32_t touched = 0;
+        short4 rect = make_short4(0, 0, -1, -1);  // empty: touches no tile (binning reads the rectangle only)
         bool dropped = false;
         if (in_range) {
             const double *V = a.cam.view;
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
                     if (fx0 <= fx1 && fy0 <= fy1) {
                         const int x0 = (int)fx0, x1 = (int)fx1, y0 = (int)fy0, y1 = (int)fy1;
                         touched = (uint32_t)((x1 - x0 + 1) * (y1 - y0 + 1));
-                        a.rect[i] = make_short4((short)x0, (short)y0, (short)x1, (short)y1);
+                        rect = make_short4((short)x0, (short)y0, (short)x1, (short)y1);
                         key = (unsigned long long)__double_as_longlong(tz);  // tz > 0: bit order == value order
                         Rec rc;
                         rc.mx = (float)mx;
@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
                     }
                 }
             }
-            a.touched[i] = touched;
+            a.rect[i] = rect;
             a.keys[i] = key;
         }
         // warp-aggregated counters
@@ -521,7 +521,6 @@ PreArgs view_args(const tcgs_scene &scene, const tcgs_camera &cam, const Band &b
     a.coverage = coverage;
     a.rec = at<Rec>(ws, L.rec);
     a.rect = at<short4>(ws, L.rect);
-    a.touched = at<uint32_t>(ws, L.touched);
     a.keys = at<unsigned long long>(ws, L.key_src);
     a.radius = at<int32_t>(ws, L.radius);
     a.dbg_conic = at<double>(ws, L.dbg_conic);

@@ -157,7 +157,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 struct Layout {
-    size_t counters, sort_state[2], rec, tmask, rect, touched, key_src, key64[2], long_runs, fix_scratch, idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
+    size_t counters, sort_state[2], rec, tmask, rect, key_src, key64[2], long_runs, fix_scratch, idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
     size_t blocksum, lb_depth, lb_tile, tkey[2], tval[2], ranges, total;
     size_t zero_begin, zero_bytes;  // sort state, cleared at the start of every binning
     static Layout make(int64_t P, int W, int H, int64_t cap) {
@@ -177,7 +177,6 @@ struct Layout {
         L.rec = take(sizeof(Rec) * Pn);
         L.tmask = take(sizeof(uint64_t) * Pn);  // exact coverage: tile masks in depth order (K3 -> K4)
         L.rect = take(sizeof(short4) * Pn);
-        L.touched = take(sizeof(uint32_t) * Pn);
         L.key_src = take(sizeof(uint64_t) * Pn);
         L.key64[0] = take(sizeof(uint64_t) * Pn);
         L.key64[1] = take(sizeof(uint64_t) * Pn);

@@ -30,6 +30,9 @@
 // host synchronisation (graph-capturable).
 #include <algorithm>
 
+#ifndef TCGS_DUP_SMALL
+#define TCGS_DUP_SMALL 32  // K4: rectangles of more tiles than this are expanded by the whole warp
+#endif
 #ifndef TCGS_TILE_DIGITS_EVEN
 #define TCGS_TILE_DIGITS_EVEN 0  // tile-key radix: 1 = equal digit widths per pass (measured: no gain over 8-bit)
 #endif
@@ -628,7 +631,7 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
         uint32_t total;
         const uint32_t ex = block_excl_scan256(c, wt, &total);
         if (total <= (uint32_t)DUP_STAGE) {
-            constexpr uint32_t SMALL = 32;
+            constexpr uint32_t SMALL = TCGS_DUP_SMALL;  // larger rectangles: the whole warp writes one
             if (c <= SMALL) {
                 uint32_t o = ex;
                 if (exact && m) {  // set bits of the mask, row-major

@@ -553,9 +553,22 @@ __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx
     }
 }
 
+__global__ void __launch_bounds__(256) bin_init(uint4 *zero, int64_t n16, uint2 *ranges, int64_t n_ranges,
+                                                DevCounters *ctr) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = t; i < n16; i += step) zero[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int64_t i = t; i < n_ranges; i += step) ranges[i] = make_uint2(0u, 0u);
+    if (t == 0) {
+        ctr->n_splats = 0ull;
+        ctr->overflow = 0ull;
+        ctr->n_long_runs = 0u;
+    }
+}
+
 // Exclusive scan of the per-block counts (one CTA of 1024 threads) -> write offsets and N.
+// Also plans the tile-key sort (what sort_plan does for it): every pass runs unless there are no splats.
 __global__ void __launch_bounds__(1024) count_scan(unsigned long long *blocksum, int nblocks, DevCounters *ctr,
-                                                   int64_t cap) {
+                                                   int64_t cap, SortState *ss_tile, int npass) {
     __shared__ unsigned long long wt[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int per = (nblocks + 1023) / 1024;
@@ -584,6 +597,15 @@ __global__ void __launch_bounds__(1024) count_scan(unsigned long long *blocksum,
     if (tid == 0) {
         ctr->n_splats = tot;
         ctr->overflow = tot > (unsigned long long)cap ? 1ull : 0ull;
+        const bool any = tot > 0ull;
+        int cur = 0;
+        for (int p = 0; p < npass; p++) {
+            ss_tile->pass_in[p] = cur;
+            ss_tile->pass_do[p] = any ? 1 : 0;
+            if (any) cur ^= 1;
+        }
+        ss_tile->final_buf = cur;
+        ctr->tile_cur = cur;
     }
 }
 
@@ -867,7 +889,7 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
         at<short4>(ws, L.rect), at<Rec>(ws, L.rec), at<unsigned long long>(ws, L.tmask), band.y0, band.y1, P,
         blocksum);
     note_launch();
-    count_scan<<<1, 1024, 0, st>>>(blocksum, nblk, ctr, cap);
+    count_scan<<<1, 1024, 0, st>>>(blocksum, nblk, ctr, cap, ss_tile, npass);
     // K4
     note_launch();
     (exact ? duplicate_keys<KT, true> : duplicate_keys<KT, false>)<<<nblk, DUP_THREADS, 0, st>>>(
@@ -875,8 +897,6 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
         at<short4>(ws, L.rect), at<Rec>(ws, L.rec), at<unsigned long long>(ws, L.tmask), P, blocksum,
         band.tiles_x, band.y0, band.y1, cap, tk0, tv0);
     // K5
-    note_launch();
-    sort_plan<<<1, 256, 0, st>>>(ss_tile, npass, &ctr->n_splats, 0, cap, nullptr, 0, &ctr->tile_cur);
     // the key's bits split as evenly as possible over the passes (13 bits: 7 + 6, not 8 + 5)
     const int db0 = TCGS_TILE_DIGITS_EVEN ? (bits + npass - 1) / npass : RADIX_BITS;
     for (int p = 0, shift = 0; p < npass; p++) {
@@ -914,20 +934,16 @@ int tile_key_bits(const Band &band) {
     return bits;
 }
 
-int bin_launch_count(int64_t P, const Band &band) {
-    const int npass = (tile_key_bits(band) + RADIX_BITS - 1) / RADIX_BITS;
-    return (P > 0 ? 2 + 3 * MAX_PASSES : 0) + 3 + 1 + 3 * npass + 1;
-}
-
 cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st) {
     DevCounters *ctr = at<DevCounters>(ws, L.counters);
     SortState *ss_depth = at<SortState>(ws, L.sort_state[0]);
-    cudaError_t e = cudaMemsetAsync(static_cast<char *>(ws) + L.zero_begin, 0, L.zero_bytes, st);
-    // per-binning counters (K1's dropped / n_visible / key_min / key_max stay)
-    if (e == cudaSuccess) e = cudaMemsetAsync(&ctr->n_splats, 0, 2 * sizeof(unsigned long long), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(&ctr->n_long_runs, 0, sizeof(unsigned int), st);
-    if (e == cudaSuccess)
-        e = cudaMemsetAsync(at<uint2>(ws, L.ranges), 0, sizeof(uint2) * (size_t)(band.n_tiles() ? band.n_tiles() : 1), st);
+    // one kernel clears the sort state, the tile ranges and the per-binning counters (K1's dropped /
+    // n_visible / key_min / key_max stay)
+    note_launch();
+    bin_init<<<64, 256, 0, st>>>(reinterpret_cast<uint4 *>(static_cast<char *>(ws) + L.zero_begin),
+                                 (int64_t)(L.zero_bytes / sizeof(uint4)), at<uint2>(ws, L.ranges),
+                                 (int64_t)(band.n_tiles() ? band.n_tiles() : 1), ctr);
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     uint32_t *k0 = at<uint32_t>(ws, L.key64[0]);
     uint32_t *k1 = at<uint32_t>(ws, L.key64[1]);

@@ -127,6 +127,33 @@ __global__ void __launch_bounds__(256) depth_fix_hist(const unsigned long long *
         const uint32_t c = (&h[0][0])[e];
         if (c) atomicAdd(&(&ss->ghist[0][0])[e], c);
     }
+    // the last CTA to finish plans the passes (no separate planning launch): a pass whose digit is
+    // the same for every key is the identity and is skipped
+    __shared__ int last, trivial;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&ss->done_ctas, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    int cur = 0;
+    for (int p = 0; p < DEPTH_PASSES; p++) {
+        if (threadIdx.x == 0) trivial = P == 0 ? 1 : 0;
+        __syncthreads();
+        if ((int64_t)__ldcg(&ss->ghist[p][threadIdx.x]) == P) trivial = 1;
+        __syncthreads();
+        const int triv = trivial;
+        if (threadIdx.x == 0) {
+            ss->pass_in[p] = cur;
+            ss->pass_do[p] = triv ? 0 : 1;
+        }
+        if (!triv) cur ^= 1;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        ss->final_buf = cur;
+        ctr->depth_cur = cur;
+    }
 }
 
 // ---------------------------------------------------------------- K2 fix-up
@@ -245,35 +272,6 @@ __global__ void __launch_bounds__(256) depth_fixup_long(const uint32_t *k0, cons
             if (s >= 0) break;
             i = e;
         }
-    }
-}
-
-// Mark identity passes (from the digit histograms when count_hist) and assign ping-pong buffers.
-__global__ void __launch_bounds__(256) sort_plan(SortState *ss, int npass, const unsigned long long *n_dev,
-                                                 int64_t n_host, int64_t cap, const unsigned long long *range,
-                                                 int count_hist, int *final_out) {
-    __shared__ int trivial;
-    const int d = threadIdx.x;
-    const int64_t n = dev_count(n_dev, n_host, cap);
-    int cur = 0;
-    for (int p = 0; p < npass; p++) {
-        const bool active = range ? (((*range) >> (RADIX_BITS * p)) != 0ull) : true;
-        if (d == 0) trivial = (!active || n == 0) ? 1 : 0;
-        __syncthreads();
-        const uint32_t c = (active && count_hist) ? ss->ghist[p][d] : 0u;
-        if (count_hist && (int64_t)c == n) trivial = 1;
-        __syncthreads();
-        const int triv = trivial;
-        if (d == 0) {
-            ss->pass_in[p] = cur;
-            ss->pass_do[p] = triv ? 0 : 1;
-        }
-        if (!triv) cur ^= 1;
-        __syncthreads();
-    }
-    if (d == 0) {
-        ss->final_buf = cur;
-        *final_out = cur;
     }
 }
 
@@ -566,7 +564,7 @@ __global__ void __launch_bounds__(256) bin_init(uint4 *zero, int64_t n16, uint2 
 }
 
 // Exclusive scan of the per-block counts (one CTA of 1024 threads) -> write offsets and N.
-// Also plans the tile-key sort (what sort_plan does for it): every pass runs unless there are no splats.
+// Also plans the tile-key sort: every pass runs unless there are no splats.
 __global__ void __launch_bounds__(1024) count_scan(unsigned long long *blocksum, int nblocks, DevCounters *ctr,
                                                    int64_t cap, SortState *ss_tile, int npass) {
     __shared__ unsigned long long wt[32];
@@ -954,8 +952,6 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
         const unsigned long long *src = at<unsigned long long>(ws, L.key_src);
         note_launch();
         depth_fix_hist<<<2 * 148, 256, 0, st>>>(src, k0, i0, P, ctr, ss_depth);
-        note_launch();
-        sort_plan<<<1, 256, 0, st>>>(ss_depth, DEPTH_PASSES, nullptr, P, P, &ctr->key_range, 1, &ctr->depth_cur);
         for (int p = 0; p < DEPTH_PASSES; p++) {
             e = launch_radix_pass<uint32_t, DEPTH_IPT>(k0, k1, i0, i1, nullptr, P, P, p, RADIX_BITS * p, RADIX_BITS,
                                                        ss_depth,

@@ -149,7 +149,8 @@ struct SortState {
     int pass_do[MAX_PASSES];                // 0: the pass is the identity (one digit value or above the key range)
     int pass_in[MAX_PASSES];                // ping-pong buffer the pass reads
     int final_buf;
-    int pad[3];
+    int done_ctas;  // depth_fix_hist: CTAs finished (the last one plans the passes)
+    int pad[2];
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

@@ -513,14 +513,59 @@ __device__ __forceinline__ uint32_t exact_cover(const Rec *rec, uint32_t g, shor
     return cover_count(cs, q);
 }
 
+// Exclusive scan of the per-block counts -> write offsets and N; also plans the tile-key sort (every pass
+// runs unless there are no splats).  Run by the last CTA of count_upsweep (blockDim.x threads).
+__device__ void count_scan(unsigned long long *blocksum, int nblocks, DevCounters *ctr, int64_t cap,
+                           SortState *ss_tile, int npass) {
+    __shared__ unsigned long long wt[32];
+    const int nt = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (nblocks + nt - 1) / nt;
+    const int b0 = tid * per;
+    unsigned long long s = 0;
+    for (int b = b0; b < b0 + per && b < nblocks; b++) s += __ldcg(&blocksum[b]);
+    unsigned long long x = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wt[warp] = x;
+    __syncthreads();
+    unsigned long long pre = 0, tot = 0;
+    for (int w = 0; w < nt / 32; w++) {
+        pre += w < warp ? wt[w] : 0ull;
+        tot += wt[w];
+    }
+    unsigned long long run = pre + x - s;
+    for (int b = b0; b < b0 + per && b < nblocks; b++) {
+        const unsigned long long v = __ldcg(&blocksum[b]);
+        blocksum[b] = run;
+        run += v;
+    }
+    if (tid == 0) {
+        ctr->n_splats = tot;
+        ctr->overflow = tot > (unsigned long long)cap ? 1ull : 0ull;
+        const bool any = tot > 0ull;
+        int cur = 0;
+        for (int p = 0; p < npass; p++) {
+            ss_tile->pass_in[p] = cur;
+            ss_tile->pass_do[p] = any ? 1 : 0;
+            if (any) cur ^= 1;
+        }
+        ss_tile->final_buf = cur;
+        ctr->tile_cur = cur;
+    }
+}
+
 // EXACT: opt-in TCGS_COVER_ELLIPSE (separate instantiation, so the default keeps its registers): also stores
 // each Gaussian's band-clipped tile mask in depth order for K4.
 template <bool EXACT>
 __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx0, const uint32_t *idx1,
-                                                             const DevCounters *ctr, const short4 *rect, const Rec *rec,
+                                                             DevCounters *ctr, const short4 *rect, const Rec *rec,
                                                              unsigned long long *tmask,
                                                              int band_y0, int band_y1,
-                                                             int64_t P, unsigned long long *blocksum) {
+                                                             int64_t P, unsigned long long *blocksum, int64_t cap,
+                                                             SortState *ss_tile, int npass) {
     const uint32_t *order = ctr->depth_cur ? idx1 : idx0;
     const int64_t beg = (int64_t)blockIdx.x * DUP_ITEMS;
     unsigned long long s = 0;
@@ -544,10 +589,18 @@ __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx
     __shared__ unsigned long long ws[DUP_THREADS / 32];
     if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
     __syncthreads();
+    __shared__ int last;
     if (threadIdx.x == 0) {
         unsigned long long t = 0;
         for (int w = 0; w < DUP_THREADS / 32; w++) t += ws[w];
         blocksum[blockIdx.x] = t;
+        __threadfence();
+        last = atomicAdd(&ss_tile->done_ctas, 1) == (int)gridDim.x - 1;  // the last CTA scans (K3b)
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        count_scan(blocksum, (int)gridDim.x, ctr, cap, ss_tile, npass);
     }
 }
 
@@ -564,48 +617,6 @@ __global__ void __launch_bounds__(256) bin_init(uint4 *zero, int64_t n16, uint2 
 }
 
 // Exclusive scan of the per-block counts (one CTA of 1024 threads) -> write offsets and N.
-// Also plans the tile-key sort: every pass runs unless there are no splats.
-__global__ void __launch_bounds__(1024) count_scan(unsigned long long *blocksum, int nblocks, DevCounters *ctr,
-                                                   int64_t cap, SortState *ss_tile, int npass) {
-    __shared__ unsigned long long wt[32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int per = (nblocks + 1023) / 1024;
-    const int b0 = tid * per;
-    unsigned long long s = 0;
-    for (int b = b0; b < b0 + per && b < nblocks; b++) s += blocksum[b];
-    unsigned long long x = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) wt[warp] = x;
-    __syncthreads();
-    unsigned long long pre = 0, tot = 0;
-    for (int w = 0; w < 32; w++) {
-        pre += w < warp ? wt[w] : 0ull;
-        tot += wt[w];
-    }
-    unsigned long long run = pre + x - s;
-    for (int b = b0; b < b0 + per && b < nblocks; b++) {
-        const unsigned long long v = blocksum[b];
-        blocksum[b] = run;
-        run += v;
-    }
-    if (tid == 0) {
-        ctr->n_splats = tot;
-        ctr->overflow = tot > (unsigned long long)cap ? 1ull : 0ull;
-        const bool any = tot > 0ull;
-        int cur = 0;
-        for (int p = 0; p < npass; p++) {
-            ss_tile->pass_in[p] = cur;
-            ss_tile->pass_do[p] = any ? 1 : 0;
-            if (any) cur ^= 1;
-        }
-        ss_tile->final_buf = cur;
-        ctr->tile_cur = cur;
-    }
-}
 
 // K4: duplicate-with-keys.  Each CTA walks DUP_ITEMS depth-ordered Gaussians 256 at a time, scans their
 // tile counts, then expands (Gaussian, covered tile) pairs cooperatively: consecutive threads write
@@ -885,9 +896,7 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     (exact ? count_upsweep<true> : count_upsweep<false>)<<<nblk, DUP_THREADS, 0, st>>>(
         at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr,
         at<short4>(ws, L.rect), at<Rec>(ws, L.rec), at<unsigned long long>(ws, L.tmask), band.y0, band.y1, P,
-        blocksum);
-    note_launch();
-    count_scan<<<1, 1024, 0, st>>>(blocksum, nblk, ctr, cap, ss_tile, npass);
+        blocksum, cap, ss_tile, npass);
     // K4
     note_launch();
     (exact ? duplicate_keys<KT, true> : duplicate_keys<KT, false>)<<<nblk, DUP_THREADS, 0, st>>>(

@@ -7,6 +7,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -45,3 +47,23 @@ def test_gpu_arm_options():
     for opt in ("--gpus", "--steps", "--warmup", "--impl", "--config", "--streams", "--view-group", "--coverage",
                 "--band-output"):
         assert opt in r.stdout, opt
+
+
+@pytest.mark.gpu
+def test_gpu_arm_line_has_the_contract_keys():
+    """bench.py's own arm on the GPU (small config): value, e2e with byte counts, roofline, clocks, launches."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = _bench(["--config", "c1", "--steps", "4", "--warmup", "3", "--no-cpu-baseline"], timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "e2e", "roofline", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["value"] > 0 and d["steps"] == 4 and d["warmup"] == 3 and d["gpu_launches"] > 0
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    rf = d["roofline"]
+    assert rf["bound"] in ("hbm", "tensor") and rf["peak"] > 0 and 0 < rf["frac"] < 1
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+    assert d["clocks"]["sm_mhz"] > 0

@@ -691,3 +691,32 @@ def test_frame_is_cuda_graph_capturable():
         assert torch.equal(rgb, ref[0]) and torch.equal(T, ref[1]) and torch.equal(cnt, ref[2])
         rc, fs = r.read_stats(cloud.P)
         assert rc == 0 and (fs.n_splats, fs.f_blend, fs.f_cull) == (ref[3].n_splats, ref[3].f_blend, ref[3].f_cull)
+
+
+def test_view_group_mixed_resolutions_and_empty_scene():
+    """A fused K1 group may mix frame sizes (each view has its own workspace layout); an empty scene renders
+    black frames with zero splats."""
+    scene, _ = synthetic.config_scene("c4", 0.002)
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    cams = [synthetic.make_camera(320, 240), synthetic.make_camera(200, 120), synthetic.make_camera(64, 48)]
+    r = tcgs.Renderer("cuda", "tcgs")
+    ref = []
+    for c in cams:
+        f = r.render_frame(cloud, c, timed=False)
+        ref.append((f.rgb.clone(), f.stats.n_splats))
+    vr = tcgs.ViewRenderer("cuda", "tcgs", n_streams=3)
+    vr.warm(cloud, cams[0])
+    outs = vr.launch_group(cloud, cams)
+    vr.join()
+    torch.cuda.synchronize()
+    for j, (rgb, T, cnt) in enumerate(outs):
+        assert rgb.shape == ref[j][0].shape and torch.equal(rgb, ref[j][0]), j
+        assert vr.renderers[j].read_stats(cloud.P)[1].n_splats == ref[j][1]
+    empty = tcgs.GaussianCloud.from_arrays({k: np.asarray(v)[:0] for k, v in scene.items() if k != "sh_degree"}
+                                           | {"sh_degree": scene["sh_degree"]}, "cuda")
+    outs = vr.launch_group(empty, cams[:2])
+    vr.join()
+    torch.cuda.synchronize()
+    for j, (rgb, T, cnt) in enumerate(outs):
+        assert float(rgb.abs().sum()) == 0.0 and int(cnt.sum()) == 0
+        assert vr.renderers[(3 + j) % 3].read_stats(0)[1].n_splats == 0

@@ -155,6 +155,25 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def pinned_h2d_GBps(host, dev, reps=3):
+    """Measured pinned host -> device copy bandwidth of this GPU's link (the scene's own buffers, CUDA events)."""
+    import torch
+
+    bufs = [(v, torch.empty_like(v, device=dev)) for v in host.values()]
+    nbytes = sum(v.numel() * v.element_size() for v in host.values())
+    for h, d in bufs:  # warm
+        d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(reps):
+        for h, d in bufs:
+            d.copy_(h, non_blocking=True)
+    t1.record()
+    torch.cuda.synchronize(dev)
+    return reps * nbytes / (t0.elapsed_time(t1) * 1e-3) / 1e9
+
+
 def e2e_resident(vr, cloud, views, base, dev, world, dist):
     """Context for `e2e`: the same host-facing loop with the scene kept resident in HBM (a renderer's usual
     case): per frame only the camera goes host -> device (as kernel parameters) and the RGB image plus the
@@ -518,6 +537,10 @@ def run_tcgs(args):
                "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                "path": ("pinned host scene -> H2D -> tcgs render -> D2H RGB + FragmentStats, every step"
                         + ("" if bands_mode else "; FramePipeline overlaps H2D(k+1) / render(k) / D2H(k-1)"))}
+        # what bounds it: the step's H2D bytes against this link's measured pinned-copy bandwidth
+        per_rank_fps = e2e["value"] / (1 if bands_mode else world)
+        e2e["h2d_achieved_GBps"] = h2d * per_rank_fps / 1e9
+        e2e["h2d_link_GBps"] = pinned_h2d_GBps(host, dev)
         if not bands_mode:
             e2e["resident_scene"] = e2e_resident(vr, cloud, my_views, base, dev, world, dist)
 

@@ -81,6 +81,7 @@ typedef struct tcgs_opts {
     int32_t early_cull;     /* exp_calls accounting: 1 = EarlyCull (tensor_path.py:148-154), 0 = reference (raster.py:94) */
     int32_t debug;          /* 1: K1 also stores the radius and float64 conic/depth for tcgs_copy_projection */
     int32_t coverage;       /* enum tcgs_coverage (K1's tile rectangle) */
+    int32_t defer_colour;   /* 1: tcgs_preprocess computes geometry only; tcgs_colour adds the colours later */
 } tcgs_opts;
 
 /* Tiles a Gaussian is binned to.  SQUARE is the reference's covered_tiles (src/tilesplat/tiling.py:34-43:
@@ -107,6 +108,13 @@ size_t tcgs_workspace_size(int64_t P, int32_t width, int32_t height, int64_t max
  * (replaces project/project_scene, src/tilesplat/projection.py:68-134). */
 int tcgs_preprocess(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts *opts, void *ws,
                     size_t ws_bytes, int64_t max_splats, void *stream);
+
+/* Deferred colour for tile bands: after tcgs_preprocess with opts->defer_colour = 1 (geometry
+ * only: no SH read) and the band partition, evaluates the SH colour of every Gaussian whose tile rectangle meets
+ * opts' tile-row band -- reading SH coefficients only for those -- with K1's arithmetic, so the frame is the
+ * same as with tcgs_preprocess's own colours. */
+int tcgs_colour(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes,
+                int64_t max_splats, void *stream);
 
 /* K1 for up to TCGS_MAX_VIEWS_PER_PASS cameras of one scene in one pass: each Gaussian's inputs (236 B at
  * SH3) are read once for all of them.  View v's outputs go to workspace ws[v] (each of

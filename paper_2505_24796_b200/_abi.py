@@ -42,7 +42,7 @@ class Camera(ctypes.Structure):
 class Opts(ctypes.Structure):
     _fields_ = [("tile_row_begin", ctypes.c_int32), ("tile_row_end", ctypes.c_int32),
                 ("alpha_mode", ctypes.c_int32), ("early_cull", ctypes.c_int32), ("debug", ctypes.c_int32),
-                ("coverage", ctypes.c_int32)]
+                ("coverage", ctypes.c_int32), ("defer_colour", ctypes.c_int32)]
 
 
 COVERAGE = {"square": 0, "box": 1, "ellipse": 2}  # enum tcgs_coverage (include/tcgs.h)
@@ -64,6 +64,8 @@ SIGNATURES = {
     "tcgs_workspace_size": (ctypes.c_size_t, [_I64, ctypes.c_int32, ctypes.c_int32, _I64]),
     "tcgs_preprocess": (ctypes.c_int, [ctypes.POINTER(Scene), ctypes.POINTER(Camera), ctypes.POINTER(Opts), _P,
                                        ctypes.c_size_t, _I64, _P]),
+    "tcgs_colour": (ctypes.c_int, [ctypes.POINTER(Scene), ctypes.POINTER(Camera), ctypes.POINTER(Opts), _P,
+                                   ctypes.c_size_t, _I64, _P]),
     "tcgs_preprocess_views": (ctypes.c_int, [ctypes.POINTER(Scene), ctypes.POINTER(Camera), ctypes.c_int32,
                                              ctypes.POINTER(Opts), ctypes.POINTER(_P), ctypes.c_size_t, _I64, _P]),
     "tcgs_bin": (ctypes.c_int, [_I64, ctypes.POINTER(Camera), ctypes.POINTER(Opts), _P, ctypes.c_size_t, _I64, _P]),

@@ -127,8 +127,20 @@ int tcgs_preprocess(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_
     note_launch();
     init_counters<<<1, 1, 0, st>>>(at<DevCounters>(ws, L.counters));
     cudaError_t e = launch_preprocess(*scene, *cam, make_band(*cam, opts), opts ? opts->debug : 0,
-                                      opts ? opts->coverage : 0, ws, L, st);
+                                      opts ? opts->coverage : 0, opts ? opts->defer_colour : 0, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "preprocess");
+    return TCGS_OK;
+}
+
+int tcgs_colour(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes,
+                int64_t max_splats, void *stream) {
+    int rc = check_scene(scene);
+    if (rc) return rc;
+    rc = check_common(cam, opts, ws, ws_bytes, scene->P, max_splats);
+    if (rc) return rc;
+    const Layout L = Layout::make(scene->P, cam->width, cam->height, max_splats);
+    cudaError_t e = launch_colour(*scene, *cam, make_band(*cam, opts), ws, L, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "colour");
     return TCGS_OK;
 }
 

@@ -185,7 +185,8 @@ struct PreArgs {
     int sh_degree;
     int tiles_x, tiles_y, band_y0, band_y1;
     int debug;
-    int coverage;  // enum tcgs_coverage
+    int coverage;      // enum tcgs_coverage
+    int defer_colour;  // 1: geometry only (no feature staging, no colour); tcgs_colour fills rgb later
     Rec *rec;
     short4 *rect;
     unsigned long long *keys;
@@ -222,7 +223,8 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
     const int NT = blockDim.x;
     const int64_t base = (int64_t)blockIdx.x * NT;
     const int n = (int)(a0.P - base < NT ? a0.P - base : NT);
-    const int F = a0.sh_degree < 0 ? 3 : 3 * (a0.sh_degree + 1) * (a0.sh_degree + 1);  // features per Gaussian
+    // features per Gaussian (none staged when the colour is deferred)
+    const int F = a0.defer_colour ? 0 : (a0.sh_degree < 0 ? 3 : 3 * (a0.sh_degree + 1) * (a0.sh_degree + 1));
     // staged SoA segments, each 16-B aligned: means 3, scales 3, rotations 4, opacity 1, features F per Gaussian
     const int per[5] = {3, 3, 4, 1, F};
     const T *src[5] = {g_means, g_scales, g_rots, g_opac, g_feats};
@@ -438,9 +440,11 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
                         const double o = ld(opac, l);
                         rc.ln_o = logf((float)o);
                         rc.opacity = (float)o;
-                        float col[3];
+                        float col[3] = {0.0f, 0.0f, 0.0f};
                         wait_bar(1);  // features staged (usually long done: they streamed in during the projection)
-                        if (a.sh_degree < 0) {
+                        if (a.defer_colour) {
+                            // colour_kernel fills it after the band partition
+                        } else if (a.sh_degree < 0) {
                             col[0] = (float)ld(feats, 3 * l);
                             col[1] = (float)ld(feats, 3 * l + 1);
                             col[2] = (float)ld(feats, 3 * l + 2);
@@ -519,6 +523,7 @@ PreArgs view_args(const tcgs_scene &scene, const tcgs_camera &cam, const Band &b
     a.band_y1 = band.y1;
     a.debug = debug;
     a.coverage = coverage;
+    a.defer_colour = 0;
     a.rec = at<Rec>(ws, L.rec);
     a.rect = at<short4>(ws, L.rect);
     a.keys = at<unsigned long long>(ws, L.key_src);
@@ -533,17 +538,75 @@ PreArgs view_args(const tcgs_scene &scene, const tcgs_camera &cam, const Band &b
 template <int NV>
 cudaError_t launch_views(const PreViews<NV> &pv, const tcgs_scene &scene, cudaStream_t st) {
     if (scene.P <= 0) return cudaSuccess;
-    const int F = scene.sh_degree < 0 ? 3 : 3 * (scene.sh_degree + 1) * (scene.sh_degree + 1);
+    const int F = pv.v[0].defer_colour ? 0 : (scene.sh_degree < 0 ? 3 : 3 * (scene.sh_degree + 1) * (scene.sh_degree + 1));
     if (scene.dtype == TCGS_F64) return launch_k1<double, NV>(pv, scene, F, 128, st);
     return launch_k1<float, NV>(pv, scene, F, TCGS_K1_THREADS, st);
 }
 
+// Deferred colour (tile bands): the SH colour of every Gaussian whose tile rectangle meets the rank's tile rows
+// [band_y0, band_y1), straight from global memory -- one 192-B SH3 read per such Gaussian instead of the
+// CTA-wide staging of all of them -- with exactly K1's arithmetic (same function, same translation unit).
+struct ColourArgs {
+    double campos[3];
+    int64_t P;
+    int sh_degree, band_y0, band_y1;
+    const short4 *rect;
+    Rec *rec;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) colour_kernel(ColourArgs c, const T *__restrict__ g_means,
+                                                     const T *__restrict__ g_feats) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= c.P) return;
+    const short4 r = c.rect[i];
+    if (r.x > r.z || r.w < c.band_y0 || r.y >= c.band_y1) return;  // no tile, or none in the band
+    float col[3];
+    if (c.sh_degree < 0) {
+        col[0] = (float)g_feats[3 * i];
+        col[1] = (float)g_feats[3 * i + 1];
+        col[2] = (float)g_feats[3 * i + 2];
+    } else {
+        const int K = (c.sh_degree + 1) * (c.sh_degree + 1);
+        const double m0 = g_means[3 * i], m1 = g_means[3 * i + 1], m2 = g_means[3 * i + 2];
+        const double dx = m0 - c.campos[0], dy = m1 - c.campos[1], dz = m2 - c.campos[2];
+        const double nn = sqrt(dx * dx + dy * dy + dz * dz);
+        sh_color(g_feats + (size_t)i * K * 3, c.sh_degree, dx / nn, dy / nn, dz / nn, col);
+    }
+    Rec &rr = c.rec[i];
+    rr.r = col[0];
+    rr.g = col[1];
+    rr.b = col[2];
+}
+
 }  // namespace
 
+cudaError_t launch_colour(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, void *ws,
+                          const Layout &L, cudaStream_t st) {
+    if (scene.P <= 0) return cudaSuccess;
+    const PreArgs a = view_args(scene, cam, band, 0, 0, ws, L);
+    ColourArgs c;
+    for (int k = 0; k < 3; k++) c.campos[k] = a.campos[k];
+    c.P = scene.P;
+    c.sh_degree = scene.sh_degree;
+    c.band_y0 = band.y0;
+    c.band_y1 = band.y1;
+    c.rect = a.rect;
+    c.rec = a.rec;
+    const unsigned blocks = (unsigned)((scene.P + 255) / 256);
+    note_launch();
+    if (scene.dtype == TCGS_F64)
+        colour_kernel<double><<<blocks, 256, 0, st>>>(c, (const double *)scene.means, (const double *)scene.features);
+    else
+        colour_kernel<float><<<blocks, 256, 0, st>>>(c, (const float *)scene.means, (const float *)scene.features);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug,
-                              int coverage, void *ws, const Layout &L, cudaStream_t st) {
+                              int coverage, int defer_colour, void *ws, const Layout &L, cudaStream_t st) {
     PreViews<1> pv;
     pv.v[0] = view_args(scene, cam, band, debug, coverage, ws, L);
+    pv.v[0].defer_colour = defer_colour;
     pv.n = 1;
     return launch_views(pv, scene, st);
 }

@@ -227,7 +227,9 @@ inline Band make_band(const tcgs_camera &cam, const tcgs_opts *o) {
 
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug,
-                              int coverage, void *ws, const Layout &L, cudaStream_t st);
+                              int coverage, int defer_colour, void *ws, const Layout &L, cudaStream_t st);
+cudaError_t launch_colour(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, void *ws,
+                          const Layout &L, cudaStream_t st);
 cudaError_t launch_preprocess_views(const tcgs_scene &scene, const tcgs_camera *cams, const Band *bands, int n_views,
                                     int debug, int coverage, void *const *ws, const Layout *L, cudaStream_t st);
 cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st);

@@ -255,8 +255,9 @@ class Renderer:
         self.ws_key = None
         self._out = {}
 
-    def _opts(self, band=None, debug=False) -> _abi.Opts:
+    def _opts(self, band=None, debug=False, defer_colour=False) -> _abi.Opts:
         o = _abi.Opts()
+        o.defer_colour = 1 if defer_colour else 0
         o.tile_row_begin, o.tile_row_end = (band if band is not None else (0, 0))
         o.alpha_mode = self.backend.alpha_mode
         o.early_cull = 1 if self.backend.early_cull else 0
@@ -294,14 +295,22 @@ class Renderer:
             ev[1].record()
         return self.bin_blend(cloud, cam, band, outputs, ev)
 
-    def preprocess(self, cloud: GaussianCloud, cam, band=None, debug=False) -> None:
-        """K1 (band-agnostic: its tile rectangles serve any band binned afterwards)."""
+    def preprocess(self, cloud: GaussianCloud, cam, band=None, debug=False, defer_colour=False) -> None:
+        """K1 (band-agnostic: its tile rectangles serve any band binned afterwards).  ``defer_colour``: geometry
+        only -- call ``colour`` for the band before binning it."""
         c = camera_struct(cam)
         cap = self.capacity(cloud.P)
         ws = self.workspace(cloud.P, c.width, c.height, cap)
         st = torch.cuda.current_stream(self.device).cuda_stream
-        _abi.check(self.lib.tcgs_preprocess(cloud._c(), c, self._opts(band, debug), ws.data_ptr(), ws.numel(), cap,
-                                            st), "tcgs_preprocess")
+        _abi.check(self.lib.tcgs_preprocess(cloud._c(), c, self._opts(band, debug, defer_colour), ws.data_ptr(),
+                                            ws.numel(), cap, st), "tcgs_preprocess")
+
+    def colour(self, cloud: GaussianCloud, cam, band=None) -> None:
+        """The deferred colours of the Gaussians whose tile rectangle meets ``band`` (tile rows [y0, y1))."""
+        c = camera_struct(cam)
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        _abi.check(self.lib.tcgs_colour(cloud._c(), c, self._opts(band), self.ws.data_ptr(), self.ws.numel(),
+                                        self.capacity(cloud.P), st), "tcgs_colour")
 
     def bin_blend(self, cloud: GaussianCloud, cam, band=None, outputs=None, timers=None):
         """K2-K6 and K7 for ``band`` (tile rows [y0, y1); None = the whole frame) after ``preprocess``."""

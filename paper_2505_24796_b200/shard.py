@@ -10,11 +10,14 @@ below exploit:
   views; there is no collective on the data path (weak scaling).
 * **tile bands** -- one huge frame (config 3, 3840x2160) is split into
   contiguous tile-row bands.  Every rank runs the replicated, band-agnostic
-  K1 preprocess, reads the per-tile-row splat counts (``tcgs_tile_row_counts``)
-  and computes the SAME prefix-balanced partition locally (no communication),
-  then bins and blends only its band.  One grouped NCCL send/recv assembles
-  the frame on rank 0 (``gather_bands``); the fragment counters are summed
-  with one tiny all-reduce.
+  K1 preprocess in geometry-only mode (no SH read), reads the per-tile-row
+  splat counts (``tcgs_tile_row_counts``) and computes the SAME
+  prefix-balanced partition locally (no communication), evaluates the SH
+  colour of only the Gaussians that reach its band (``tcgs_colour``), then
+  bins and blends its band.  The frame reaches rank 0 through NVLink peer
+  memory (K7 writes into rank 0's frame) or one grouped NCCL send/recv
+  (``gather_bands``); the fragment counters are summed with one tiny
+  all-reduce.
 
 The partition/gather helpers are plain torch.distributed code, so they are
 covered on CPU with the gloo backend (tests/test_shard.py); the render itself
@@ -277,11 +280,12 @@ class BandRenderer:
         with torch.cuda.device(self.device):
             if ev:
                 ev[0].record()
-            self.r.preprocess(cloud, cam)
+            self.r.preprocess(cloud, cam, defer_colour=True)  # geometry for every Gaussian, no SH read
             if ev:
                 ev[1].record()
             bands = self.partition(cloud, cam)
             band = bands[rank]
+            self.r.colour(cloud, cam, band)  # SH only for the Gaussians that reach this rank's band
             c = camera_struct(cam)
             outs = None
             if self.output == "peer":

@@ -73,7 +73,8 @@ int main(int argc, char **argv) {
                         to_device(rgb, sizeof(float) * 3 * P)};
     if (!scene.means || !scene.scales || !scene.rotations || !scene.opacities || !scene.features) return 2;
     tcgs_camera cam = {{1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1}, 1.2 * W, 1.2 * W, W / 2.0, H / 2.0, 0.2, W, H};
-    tcgs_opts opts = {0, 0, TCGS_ALPHA_TC_HILO, /*early_cull*/ 1, /*debug*/ 0, TCGS_COVER_SQUARE};
+    /* designated initialisers: fields added to tcgs_opts later default to 0 (the reference's behaviour) */
+    tcgs_opts opts = {.alpha_mode = TCGS_ALPHA_TC_HILO, .early_cull = 1, .coverage = TCGS_COVER_SQUARE};
 
     const int64_t max_splats = 64 * P;
     const size_t ws_bytes = tcgs_workspace_size(P, W, H, max_splats);

@@ -280,12 +280,16 @@ class BandRenderer:
         with torch.cuda.device(self.device):
             if ev:
                 ev[0].record()
-            self.r.preprocess(cloud, cam, defer_colour=True)  # geometry for every Gaussian, no SH read
+            # several ranks: geometry for every Gaussian (no SH read), then SH only for the Gaussians that reach
+            # this rank's band; one rank: K1's own staged colour (its band is the whole frame)
+            defer = dist.get_world_size(self.group) > 1
+            self.r.preprocess(cloud, cam, defer_colour=defer)
             if ev:
                 ev[1].record()
             bands = self.partition(cloud, cam)
             band = bands[rank]
-            self.r.colour(cloud, cam, band)  # SH only for the Gaussians that reach this rank's band
+            if defer:
+                self.r.colour(cloud, cam, band)
             c = camera_struct(cam)
             outs = None
             if self.output == "peer":

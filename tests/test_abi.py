@@ -100,6 +100,23 @@ def test_preprocess_views_rejects_bad_view_groups(lib):
     assert lib.tcgs_launch_count() == n0
 
 
+def test_colour_pass_rejects_bad_arguments(lib):
+    cam = _abi.Camera()
+    cam.width, cam.height, cam.fx, cam.fy, cam.near_plane = 64, 64, 50.0, 50.0, 0.2
+    ws = ctypes.create_string_buffer(16)
+    n0 = lib.tcgs_launch_count()
+    assert lib.tcgs_colour(None, ctypes.byref(cam), None, ctypes.cast(ws, ctypes.c_void_p), 16, 100, None) == \
+        _abi.TCGS_ERR_INVALID_ARG
+    scene = _abi.Scene()
+    scene.P, scene.sh_degree, scene.dtype = 0, 0, 0
+    assert lib.tcgs_colour(ctypes.byref(scene), ctypes.byref(cam), None, ctypes.cast(ws, ctypes.c_void_p), 16, 100,
+                           None) == _abi.TCGS_ERR_WORKSPACE
+    scene.sh_degree = 7
+    assert lib.tcgs_colour(ctypes.byref(scene), ctypes.byref(cam), None, ctypes.cast(ws, ctypes.c_void_p), 16, 100,
+                           None) == _abi.TCGS_ERR_INVALID_ARG
+    assert lib.tcgs_launch_count() == n0
+
+
 def test_product_package_never_touches_the_oracle():
     """Only tests/, smoke() and bench.py may use oracle/: the shipped package must not import it."""
     for dirpath, _, files in os.walk(PKG):

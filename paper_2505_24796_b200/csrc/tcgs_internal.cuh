@@ -19,7 +19,10 @@ constexpr int DEPTH_IPT = 8;          // items per thread: depth sort (u64 keys)
 constexpr int TILEKEY_IPT = 16;       // items per thread: tile-key sort, 4096-item tiles
 constexpr int MAX_PASSES = 8;         // depth key: <= 64 bits
 constexpr int TILE_MAX_PASSES = 4;    // tile key: <= 32 bits
-constexpr int DUP_ITEMS = 1024;       // Gaussians per duplicate-with-keys CTA
+#ifndef TCGS_DUP_ITEMS
+#define TCGS_DUP_ITEMS 1024
+#endif
+constexpr int DUP_ITEMS = TCGS_DUP_ITEMS;  // Gaussians per duplicate-with-keys CTA
 constexpr int DUP_THREADS = 256;
 
 #ifndef TCGS_K7_PIX

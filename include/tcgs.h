@@ -82,7 +82,13 @@ typedef struct tcgs_opts {
     int32_t debug;          /* 1: K1 also stores the radius and float64 conic/depth for tcgs_copy_projection */
     int32_t coverage;       /* enum tcgs_coverage (K1's tile rectangle) */
     int32_t defer_colour;   /* 1: tcgs_preprocess computes geometry only; tcgs_colour adds the colours later */
+    int32_t schedule;       /* enum tcgs_schedule (how tcgs_blend hands tiles to CTAs) */
 } tcgs_opts;
+
+/* K7 tile assignment.  DYNAMIC (default): after its first tile a CTA takes the next from a global queue --
+ * the best latency for a frame that has the GPU to itself.  STATIC: CTA b takes tiles b, b + grid, ... -- its
+ * staggered tail lets other streams' kernels in, the better choice with several frames in flight. */
+enum tcgs_schedule { TCGS_SCHEDULE_DYNAMIC = 0, TCGS_SCHEDULE_STATIC = 1 };
 
 /* Tiles a Gaussian is binned to.  SQUARE is the reference's covered_tiles (src/tilesplat/tiling.py:34-43:
  * the 3-sigma square; parity).  The opt-in modes keep only tiles of that square the

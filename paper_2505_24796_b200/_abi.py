@@ -42,7 +42,10 @@ class Camera(ctypes.Structure):
 class Opts(ctypes.Structure):
     _fields_ = [("tile_row_begin", ctypes.c_int32), ("tile_row_end", ctypes.c_int32),
                 ("alpha_mode", ctypes.c_int32), ("early_cull", ctypes.c_int32), ("debug", ctypes.c_int32),
-                ("coverage", ctypes.c_int32), ("defer_colour", ctypes.c_int32)]
+                ("coverage", ctypes.c_int32), ("defer_colour", ctypes.c_int32), ("schedule", ctypes.c_int32)]
+
+
+SCHEDULE = {"dynamic": 0, "static": 1}  # enum tcgs_schedule (include/tcgs.h)
 
 
 COVERAGE = {"square": 0, "box": 1, "ellipse": 2}  # enum tcgs_coverage (include/tcgs.h)

@@ -68,6 +68,8 @@ int check_common(const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t
             return fail(TCGS_ERR_INVALID_ARG, "unknown alpha mode");
         if (opts->coverage < TCGS_COVER_SQUARE || opts->coverage > TCGS_COVER_ELLIPSE)
             return fail(TCGS_ERR_INVALID_ARG, "unknown coverage mode");
+        if (opts->schedule != TCGS_SCHEDULE_DYNAMIC && opts->schedule != TCGS_SCHEDULE_STATIC)
+            return fail(TCGS_ERR_INVALID_ARG, "unknown tile schedule");
         if (opts->tile_row_end > 0 && (opts->tile_row_begin < 0 || opts->tile_row_begin >= opts->tile_row_end ||
                                        opts->tile_row_end > ty))
             return fail(TCGS_ERR_INVALID_ARG, "invalid tile-row band");

@@ -84,6 +84,7 @@ struct __align__(1024) K7Smem {
     uint32_t tmem_base;
     int retire[8];
     int c_fill, c_k, c_open;  // compaction state: touched only by the producer holding the token
+    unsigned long long tslot[16];  // dynamic tile stream: (seq << 32) | tile, shared by the producers
     uint32_t c_dead;
     unsigned long long red[K7_CONSUMER_WARPS][4];
 };
@@ -256,7 +257,8 @@ __device__ __forceinline__ void make_vrow(const float v[6], uint4 &lo8, uint4 &h
 }
 
 // ------------------------------------------------------------------------------------------ producers
-// The CTA's tile stream is static (tiles blockIdx.x, +gridDim.x, ...); each tile contributes
+// The CTA's tile stream starts at tile blockIdx.x and continues from a global queue (dynamic schedule) or with
+// blockIdx.x + gridDim.x, ... (static schedule); each tile contributes
 // max(1, ceil(n/32)) chunks of 32 list entries, and one "end" chunk closes the stream.  Producer warp p
 // owns chunks p, p + NP, ...: it gathers and evaluates its chunk in parallel with the other producer,
 // then waits for the compaction token, places its live rows into the current stage, emits full stages
@@ -264,8 +266,38 @@ __device__ __forceinline__ void make_vrow(const float v[6], uint4 &lo8, uint4 &h
 struct Cursor {
     int tile, seq, c, chunks, n;
     uint32_t beg;
-    float ox, oy;  // tile centre (16tx+8, 16ty+8), tensor_path.py:21-22
+    float ox, oy;     // tile centre (16tx+8, 16ty+8), tensor_path.py:21-22
+    bool prev_valid;  // the previous tile of the stream was a real one (its end chunk closes the stream)
 };
+
+constexpr uint32_t TSLOT_CLAIMED = 0xFFFFFFFFu;
+
+// Tile of the CTA's seq-th stream position (seq >= 1), fetched from the global queue by whichever producer needs
+// it first and shared through a tagged shared-memory slot: both producers walk the same stream.  Warp-uniform.
+__device__ __forceinline__ int seq_tile(K7Smem &sm, const RenderArgs &a, int seq) {
+    int t = 0;
+    if ((threadIdx.x & 31) == 0) {
+        unsigned long long *slot = &sm.tslot[seq & 15];
+        const unsigned long long tag = (unsigned long long)(uint32_t)seq << 32;
+        for (;;) {
+            const unsigned long long v = *reinterpret_cast<volatile unsigned long long *>(slot);
+            if ((uint32_t)(v >> 32) == (uint32_t)seq) {
+                if ((uint32_t)v != TSLOT_CLAIMED) {
+                    t = (int)(uint32_t)v;
+                    break;
+                }
+                __nanosleep(32);  // the other producer is fetching it
+                continue;
+            }
+            if (atomicCAS(slot, v, tag | TSLOT_CLAIMED) == v) {
+                t = (int)gridDim.x + (int)atomicAdd(&a.ctr->tile_queue, 1u);
+                atomicExch(slot, tag | (uint32_t)t);
+                break;
+            }
+        }
+    }
+    return __shfl_sync(0xffffffffu, t, 0);
+}
 
 __device__ __forceinline__ void cursor_tile(Cursor &k, const RenderArgs &a) {
     k.c = 0;
@@ -284,29 +316,33 @@ __device__ __forceinline__ void cursor_tile(Cursor &k, const RenderArgs &a) {
     }
 }
 
-__device__ __forceinline__ void cursor_next(Cursor &k, const RenderArgs &a) {
+// DYN (TCGS_SCHEDULE_DYNAMIC): tiles after the CTA's first come from a global queue, which balances the tail of
+// a lone frame; static (tiles blockIdx.x, +gridDim.x, ...) leaves a staggered tail that other streams' kernels fill
+// when several frames share the GPU.
+template <bool DYN>
+__device__ __forceinline__ void cursor_next(Cursor &k, const RenderArgs &a, K7Smem &sm) {
     if (++k.c >= k.chunks) {
-        k.tile += gridDim.x;
+        k.prev_valid = k.tile < a.n_tiles;
         k.seq++;
+        k.tile = DYN ? seq_tile(sm, a, k.seq) : k.tile + (int)gridDim.x;
         cursor_tile(k, a);
     }
 }
 
-template <int MODE>
+template <int MODE, bool DYN>
 __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, uint32_t tmem, int p) {
     constexpr bool TC = MODE != TCGS_ALPHA_FFMA;
     constexpr int NP = K7_PRODUCERS;
     const int lane = threadIdx.x & 31;
     const unsigned FULL = 0xffffffffu, lt = lanemask_lt();
-    const int real_tiles = (int)blockIdx.x < a.n_tiles ? (a.n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-
     Cursor cur;
     cur.tile = blockIdx.x;
     cur.seq = 0;
+    cur.prev_valid = true;
     cursor_tile(cur, a);
-    for (int i = 0; i < p; i++) cursor_next(cur, a);
+    for (int i = 0; i < p; i++) cursor_next<DYN>(cur, a, sm);
     Cursor nxt = cur;
-    for (int i = 0; i < NP; i++) cursor_next(nxt, a);
+    for (int i = 0; i < NP; i++) cursor_next<DYN>(nxt, a, sm);
     auto list_id = [&](const Cursor &k) -> uint32_t {
         const int i = k.c * 32 + lane;
         return i < k.n ? ids[k.beg + i] : 0u;
@@ -321,10 +357,11 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
 
     for (int m = 0;; m++) {
         const bool end = cur.tile >= a.n_tiles;
-        if (end && !(cur.seq == real_tiles && cur.c == 0)) return;  // past the stream: the terminator is elsewhere
+        // past the stream: the first chunk after the last real tile carries the terminator, every other returns
+        if (end && !(cur.prev_valid && cur.c == 0)) return;
         // prefetch the next owned chunk's records; its successor's ids
         Cursor nx2 = nxt;
-        for (int i = 0; i < NP; i++) cursor_next(nx2, a);
+        for (int i = 0; i < NP; i++) cursor_next<DYN>(nx2, a, sm);
         Rec rn;
         if (nxt.c * 32 + lane < nxt.n) rn = a.rec[id_nxt];
         const uint32_t id_nx2 = list_id(nx2);
@@ -467,7 +504,7 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
 }
 
 // ------------------------------------------------------------------------------------------ kernel
-template <int MODE>
+template <int MODE, bool DYN>
 __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(RenderArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     K7Smem &sm = *reinterpret_cast<K7Smem *>(smem_raw);
@@ -518,6 +555,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
         sm.c_k = 0;
         sm.c_open = 0;
         sm.c_dead = 0;
+        for (int q = 0; q < 16; q++) sm.tslot[q] = ~0ull;  // no stream position fetched yet
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (TC && warp == 0) {
@@ -533,7 +571,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
 
     unsigned long long s_blend = 0, s_cull = 0, s_term = 0, s_pairs = 0;
     if (warp >= K7_CONSUMER_WARPS) {
-        producer<MODE>(sm, a, ids, tmem, warp - K7_CONSUMER_WARPS);
+        producer<MODE, DYN>(sm, a, ids, tmem, warp - K7_CONSUMER_WARPS);
     } else {
         int cur_seq = -1, cur_tile = -1;
         int px[NPIX], py[NPIX];
@@ -778,18 +816,18 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
     }
 }
 
-template <int MODE>
+template <int MODE, bool DYN>
 cudaError_t launch_mode(const RenderArgs &a, int num_sms, cudaStream_t st) {
     static bool configured_dev[TCGS_MAX_DEVICES] = {};
     bool &configured = configured_dev[current_device()];
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(render_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, K7_SMEM_BYTES);
+        cudaError_t e = cudaFuncSetAttribute(render_kernel<MODE, DYN>, cudaFuncAttributeMaxDynamicSharedMemorySize, K7_SMEM_BYTES);
         if (e != cudaSuccess) return e;
         configured = true;
     }
     const int grid = num_sms * K7_CTAS_PER_SM;
     note_launch();
-    render_kernel<MODE><<<grid, K7_THREADS, K7_SMEM_BYTES, st>>>(a);
+    render_kernel<MODE, DYN><<<grid, K7_THREADS, K7_SMEM_BYTES, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -817,13 +855,17 @@ cudaError_t launch_render(int alpha_mode, const tcgs_camera &cam, const Band &ba
     cudaError_t e = cudaMemsetAsync(&a.ctr->f_blend, 0, 4 * sizeof(unsigned long long), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(&a.ctr->tile_queue, 0, sizeof(unsigned int), st);
     if (e != cudaSuccess) return e;
+    const bool dyn = band.schedule == TCGS_SCHEDULE_DYNAMIC;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     switch (alpha_mode) {
-        case TCGS_ALPHA_TC_HILO: return launch_mode<TCGS_ALPHA_TC_HILO>(a, sms, st);
-        case TCGS_ALPHA_TC_K8: return launch_mode<TCGS_ALPHA_TC_K8>(a, sms, st);
-        case TCGS_ALPHA_FFMA: return launch_mode<TCGS_ALPHA_FFMA>(a, sms, st);
+        case TCGS_ALPHA_TC_HILO:
+            return dyn ? launch_mode<TCGS_ALPHA_TC_HILO, true>(a, sms, st) : launch_mode<TCGS_ALPHA_TC_HILO, false>(a, sms, st);
+        case TCGS_ALPHA_TC_K8:
+            return dyn ? launch_mode<TCGS_ALPHA_TC_K8, true>(a, sms, st) : launch_mode<TCGS_ALPHA_TC_K8, false>(a, sms, st);
+        case TCGS_ALPHA_FFMA:
+            return dyn ? launch_mode<TCGS_ALPHA_FFMA, true>(a, sms, st) : launch_mode<TCGS_ALPHA_FFMA, false>(a, sms, st);
         default: return cudaErrorInvalidValue;
     }
 }

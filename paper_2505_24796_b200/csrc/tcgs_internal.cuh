@@ -211,6 +211,7 @@ inline const T *at(const void *ws, size_t off) { return reinterpret_cast<const T
 struct Band {
     int tiles_x, tiles_y, y0, y1;  // tile rows [y0, y1)
     int coverage;                  // enum tcgs_coverage
+    int schedule;                  // enum tcgs_schedule (K7 tile assignment)
     int n_tiles() const { return tiles_x * (y1 - y0); }
 };
 
@@ -221,6 +222,7 @@ inline Band make_band(const tcgs_camera &cam, const tcgs_opts *o) {
     b.y0 = 0;
     b.y1 = b.tiles_y;
     b.coverage = o ? o->coverage : TCGS_COVER_SQUARE;
+    b.schedule = o ? o->schedule : TCGS_SCHEDULE_DYNAMIC;
     if (o && o->tile_row_end > 0) {
         b.y0 = o->tile_row_begin < 0 ? 0 : o->tile_row_begin;
         b.y1 = o->tile_row_end > b.tiles_y ? b.tiles_y : o->tile_row_end;

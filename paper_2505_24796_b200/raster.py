@@ -239,10 +239,15 @@ class Renderer:
     the splat capacity.
     """
 
-    def __init__(self, device=None, backend="tcgs", max_splats: int | None = None, coverage: str = "square"):
+    def __init__(self, device=None, backend="tcgs", max_splats: int | None = None, coverage: str = "square",
+                 schedule: str = "dynamic"):
         if coverage not in _abi.COVERAGE:
             raise ValueError(f"coverage must be one of {sorted(_abi.COVERAGE)}")
+        if schedule not in _abi.SCHEDULE:
+            raise ValueError(f"schedule must be one of {sorted(_abi.SCHEDULE)}")
         self.coverage = _abi.COVERAGE[coverage]  # "square": the reference's tiles; "ellipse": opt-in, fewer splats
+        # K7 tile assignment: "dynamic" (a global queue; best for a lone frame) or "static" (frames in flight)
+        self.schedule = _abi.SCHEDULE[schedule]
         self.lib = _abi.load()
         self.device = torch.device(device or "cuda")
         if self.device.type != "cuda":
@@ -263,6 +268,7 @@ class Renderer:
         o.early_cull = 1 if self.backend.early_cull else 0
         o.debug = 1 if debug else 0
         o.coverage = self.coverage
+        o.schedule = self.schedule
         return o
 
     def workspace(self, P: int, W: int, H: int, cap: int) -> torch.Tensor:
@@ -451,7 +457,9 @@ class ViewRenderer:
 
     def __init__(self, device=None, backend="tcgs", n_streams: int = 2, coverage: str = "square"):
         self.device = torch.device(device or "cuda")
-        self.renderers = [Renderer(self.device, backend, coverage=coverage) for _ in range(n_streams)]
+        # several frames share the GPU: K7's static schedule leaves a staggered tail the other streams fill
+        self.renderers = [Renderer(self.device, backend, coverage=coverage, schedule="static")
+                          for _ in range(n_streams)]
         self.streams = [torch.cuda.Stream(self.device) for _ in range(n_streams)]
         self.outputs = [None] * n_streams
         self.k = 0

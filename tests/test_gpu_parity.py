@@ -742,3 +742,21 @@ def test_deferred_colour_per_band_matches_full_frame(cfg):
         y0, y1 = band[0] * 16, min(band[1] * 16, cam.height)
         assert torch.equal(rgb[y0:y1], ref_rgb[y0:y1]), band
         assert torch.equal(cnt[y0:y1], ref_cnt[y0:y1]), band
+
+
+
+@pytest.mark.parametrize("cfg,scale", [("c2", 0.05), ("c3", 0.02)])
+def test_tile_schedules_render_the_same_frame(cfg, scale):
+    """K7's dynamic (global tile queue) and static tile schedules give bit-identical frames and FragmentStats."""
+    scene, cams = synthetic.config_scene(cfg, scale)
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    out = {}
+    for sched in ("dynamic", "static"):
+        f = tcgs.Renderer("cuda", "tcgs", schedule=sched).render_frame(cloud, cams[0], timed=False)
+        out[sched] = (f.rgb.clone(), f.T.clone(), f.n_contrib.clone(), f.stats)
+    a, b = out["dynamic"], out["static"]
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and torch.equal(a[2], b[2])
+    assert (a[3].f_blend, a[3].f_cull, a[3].f_skip, a[3].n_splats) == (b[3].f_blend, b[3].f_cull, b[3].f_skip,
+                                                                        b[3].n_splats)
+    with pytest.raises(ValueError):
+        tcgs.Renderer("cuda", "tcgs", schedule="random")

@@ -760,3 +760,33 @@ def test_tile_schedules_render_the_same_frame(cfg, scale):
                                                                         b[3].n_splats)
     with pytest.raises(ValueError):
         tcgs.Renderer("cuda", "tcgs", schedule="random")
+
+
+def test_full_scale_view_group_and_coverage():
+    """At the headline's full size (C2: 1M Gaussians, SH3, 1080p): a fused 4-view K1 group reproduces every
+    view's single-camera frame bit for bit, and both opt-in coverage modes keep the image."""
+    scene, _ = synthetic.config_scene("c2", 1.0)
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    base = synthetic.make_camera(1920, 1080)
+    views = []
+    for yaw in (0.0, 0.002, -0.004, 0.006):
+        m = np.asarray(base.view, np.float64).reshape(4, 4).copy()
+        R = np.array([[np.cos(yaw), 0, np.sin(yaw)], [0, 1, 0], [-np.sin(yaw), 0, np.cos(yaw)]])
+        m[:3, :3] = R @ m[:3, :3]
+        views.append(synthetic.CameraSpec(m, base.fx, base.fy, base.cx, base.cy, base.width, base.height, base.near))
+    r = tcgs.Renderer("cuda", "tcgs")
+    ref = []
+    for c in views:
+        f = r.render_frame(cloud, c, timed=False)
+        ref.append((f.rgb.clone(), f.n_contrib.clone(), f.stats.n_splats))
+    vr = tcgs.ViewRenderer("cuda", "tcgs", n_streams=4)
+    vr.warm(cloud, views[0])
+    outs = vr.launch_group(cloud, views)
+    vr.join()
+    torch.cuda.synchronize()
+    for j, (rgb, T, cnt) in enumerate(outs):
+        assert torch.equal(rgb, ref[j][0]) and torch.equal(cnt, ref[j][1]), j
+    for mode in ("box", "ellipse"):
+        f = tcgs.Renderer("cuda", "tcgs", coverage=mode).render_frame(cloud, views[0], timed=False)
+        assert torch.equal(f.rgb, ref[0][0]) and torch.equal(f.n_contrib, ref[0][1]), mode
+        assert f.stats.n_splats < ref[0][2]

@@ -138,7 +138,10 @@ def fixture_specs():
     specs = {
         # config 1 of BASELINE.json
         "c1": lambda: (ms(0, 10000), mc(256, 256)),
-        # acceptance criterion 1 scenes (tests/test_acceptance.py:129-135), the ones small enough to commit
+        # acceptance criterion 1 scenes (tests/test_acceptance.py:35-41), the ones small enough to commit
+        # (103-105 render 512^2-1024^2 frames: 8-25 MB fixtures each)
+        "acc101": lambda: (ms(101, 10), mc(256, 256)),
+        "acc102": lambda: (ms(102, 100), mc(256, 256)),
         # criterion 7 scenes (tests/test_acceptance.py:299-306)
         "sem701": lambda: (ms(701, 20, opacity_range=(0.2, 0.95)), mc(64, 64)),
         "sem702": lambda: (ms(702, 60, opacity_range=(0.2, 0.95)), mc(64, 64)),

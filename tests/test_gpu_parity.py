@@ -790,3 +790,22 @@ def test_full_scale_view_group_and_coverage():
         f = tcgs.Renderer("cuda", "tcgs", coverage=mode).render_frame(cloud, views[0], timed=False)
         assert torch.equal(f.rgb, ref[0][0]) and torch.equal(f.n_contrib, ref[0][1]), mode
         assert f.stats.n_splats < ref[0][2]
+
+
+def test_criterion_6_precision_at_1080p():
+    """The reference's criterion 6 (ref-tests/test_acceptance.py:139-151) on the GPU: at 1080p, the paper's
+    fp16 length-8 local vector stays >= 40 dB from the reference renderer (here its float64 oracle port), and
+    the default hi/lo mode >= 45 dB with bit-exact tile lists."""
+    scene = synthetic.make_scene(606, 10, xy_spread=3.0, depth_range=(8.0, 12.0), scale_range=(0.5, 1.0),
+                                 opacity_range=(0.2, 0.45))
+    cam = synthetic.make_camera(1920, 1080)
+    ref = oracle.render(scene["means"], scene["scales"], scene["rotations"], scene["opacities"], scene["colors"], cam)
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    for spec, pmin in (("tcgs-fp16", 40.0), ("tcgs", 45.0)):
+        r = tcgs.Renderer("cuda", spec)
+        f = r.render_frame(cloud, cam, timed=False)
+        q = psnr(f.rgb.double().cpu().numpy(), ref.rgb)
+        assert q >= pmin, (spec, q)
+        assert f.stats.n_splats == ref.stats.n_splats
+        offsets, ids = r.tile_lists(cloud.P, cam)
+        assert np.array_equal(offsets, ref.offsets) and np.array_equal(ids, ref.ids)

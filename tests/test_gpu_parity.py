@@ -809,3 +809,21 @@ def test_criterion_6_precision_at_1080p():
         assert f.stats.n_splats == ref.stats.n_splats
         offsets, ids = r.tile_lists(cloud.P, cam)
         assert np.array_equal(offsets, ref.offsets) and np.array_equal(ids, ref.ids)
+
+
+@pytest.mark.parametrize("seed,n", [(201, 30), (202, 80), (203, 150)])
+def test_criterion_2_exp_call_accounting(seed, n):
+    """The reference's criterion 2 (ref-tests/test_acceptance.py:74-88): with EarlyCull accounting on, exp_calls
+    == f_blend on termination-free scenes; off, f_blend + f_cull; same categories and image either way."""
+    scene = synthetic.make_scene(seed, n, opacity_range=(0.05, 0.3))
+    cam = synthetic.make_camera(256, 256)
+    cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
+    on = tcgs.Renderer("cuda", tcgs.make_backend("tcgs", use_early_cull=True)).render_frame(cloud, cam, timed=False)
+    on_rgb, on = on.rgb.clone(), on.stats
+    off = tcgs.Renderer("cuda", tcgs.make_backend("tcgs", use_early_cull=False)).render_frame(cloud, cam, timed=False)
+    assert on.pixels_terminated == 0
+    assert on.exp_calls == on.f_blend
+    assert off.stats.exp_calls == off.stats.f_blend + off.stats.f_cull
+    assert (on.f_blend, on.f_cull, on.f_skip) == (off.stats.f_blend, off.stats.f_cull, off.stats.f_skip)
+    assert torch.equal(on_rgb, off.rgb)
+    assert on.f_cull > 0

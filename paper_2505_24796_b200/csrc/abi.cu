@@ -169,7 +169,7 @@ int tcgs_preprocess_views(const tcgs_scene *scene, const tcgs_camera *cams, int3
     note_launch();
     init_counters_views<<<1, 32, 0, st>>>(cs, n_views);
     cudaError_t e = launch_preprocess_views(*scene, cams, bands, n_views, opts ? opts->debug : 0,
-                                            opts ? opts->coverage : 0, ws, L, st);
+                                            opts ? opts->coverage : 0, opts ? opts->defer_colour : 0, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "preprocess_views");
     return TCGS_OK;
 }

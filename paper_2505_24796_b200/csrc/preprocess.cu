@@ -612,9 +612,13 @@ cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, c
 }
 
 cudaError_t launch_preprocess_views(const tcgs_scene &scene, const tcgs_camera *cams, const Band *bands, int n_views,
-                                    int debug, int coverage, void *const *ws, const Layout *L, cudaStream_t st) {
+                                    int debug, int coverage, int defer_colour, void *const *ws, const Layout *L,
+                                    cudaStream_t st) {
     PreViews<TCGS_MAX_VIEWS_PER_PASS> pv;
-    for (int v = 0; v < n_views; v++) pv.v[v] = view_args(scene, cams[v], bands[v], debug, coverage, ws[v], L[v]);
+    for (int v = 0; v < n_views; v++) {
+        pv.v[v] = view_args(scene, cams[v], bands[v], debug, coverage, ws[v], L[v]);
+        pv.v[v].defer_colour = defer_colour;
+    }
     pv.n = n_views;
     return launch_views(pv, scene, st);
 }

@@ -236,7 +236,8 @@ cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, c
 cudaError_t launch_colour(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, void *ws,
                           const Layout &L, cudaStream_t st);
 cudaError_t launch_preprocess_views(const tcgs_scene &scene, const tcgs_camera *cams, const Band *bands, int n_views,
-                                    int debug, int coverage, void *const *ws, const Layout *L, cudaStream_t st);
+                                    int debug, int coverage, int defer_colour, void *const *ws, const Layout *L,
+                                    cudaStream_t st);
 cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st);
 cudaError_t launch_render(int alpha_mode, const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
                           void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st);

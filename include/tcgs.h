@@ -48,7 +48,10 @@ enum tcgs_status {
 enum tcgs_alpha_mode {
     TCGS_ALPHA_TC_HILO = 0, /* tcgen05 fp16 K=16: hi/lo split Gaussian vector (default) */
     TCGS_ALPHA_TC_K8 = 1,   /* tcgen05 fp16, the paper's length-8 vector (src/tilesplat/tensor_path.py:25-40) */
-    TCGS_ALPHA_FFMA = 2     /* CUDA-core FP32 quadratic form, no tensor cores (ablation baseline) */
+    TCGS_ALPHA_FFMA = 2,    /* CUDA-core FP32 quadratic form, no tensor cores (ablation baseline) */
+    TCGS_ALPHA_TC_K8_GLOBAL = 3 /* the paper's fp16 length-8 vector in GLOBAL pixel coordinates (no G2L):
+                                   tensor_path.py:92-100 with coords="global"; precision ablation only
+                                   (x^2 overflows fp16 beyond x = 255) */
 };
 
 enum tcgs_dtype { TCGS_F32 = 0, TCGS_F64 = 1 };
@@ -78,11 +81,27 @@ typedef struct tcgs_opts {
     int32_t tile_row_begin; /* render tile rows [begin, end); end <= 0 means all rows */
     int32_t tile_row_end;
     int32_t alpha_mode;     /* enum tcgs_alpha_mode */
-    int32_t early_cull;     /* exp_calls accounting: 1 = EarlyCull (tensor_path.py:148-154), 0 = reference (raster.py:94) */
+    int32_t early_cull;     /* 1 = EarlyCull: the cull is decided on the exponent before any ex2 and exp_calls
+                               = blends + terminations (tensor_path.py:148-154); 0 = EarlyCull off: alpha =
+                               exp(beta) for every active fragment, cull on alpha < 1/255 afterwards, exp_calls
+                               = every active fragment (raster.py:86-94, tensor_path.py:155-160) */
     int32_t debug;          /* 1: K1 also stores the radius and float64 conic/depth for tcgs_copy_projection */
     int32_t coverage;       /* enum tcgs_coverage (K1's tile rectangle) */
     int32_t defer_colour;   /* 1: tcgs_preprocess computes geometry only; tcgs_colour adds the colours later */
     int32_t schedule;       /* enum tcgs_schedule (how tcgs_blend hands tiles to CTAs) */
+    int32_t timing;         /* 1: time each stage with CUDA events on `stream`; the next tcgs_read_stats of this
+                               workspace reports them in ms_preprocess / ms_sort / ms_blend
+                               (FragmentStats.stage_ms, src/tilesplat/raster.py:196-200) */
+    int32_t reserved;
+    /* Debug dump (the beta tolerance oracle; NULL = off).  When both are set, tcgs_blend / tcgs_blend_lists /
+     * tcgs_render record, for every (tile-list entry e, tile pixel i = 16 row + col) the blend kernel evaluates,
+     * dump_beta[e*256 + i] = the exponent in log2 units (beta * log2 e, the value K7 compares and exponentiates)
+     * and dump_class[e*256 + i] = 1 cull / 2 blend / 3 terminate / 4 dead: the producer's box test found the
+     * Gaussian below the EarlyCull cut on the whole tile (a cull wherever the pixel is still live) / 0 not
+     * evaluated (out of the image, or after the pixel terminated).  Both [N][256] (device); the caller
+     * initialises them. */
+    float *dump_beta;
+    uint8_t *dump_class;
 } tcgs_opts;
 
 /* K7 tile assignment.  DYNAMIC (default): after its first tile a CTA takes the next from a global queue --
@@ -105,6 +124,9 @@ typedef struct tcgs_stats {
     int64_t f_blend, f_cull, f_skip, exp_calls, pixels_terminated;
     int64_t n_visible;         /* Gaussians touching at least one tile of the band */
     int64_t max_splats_needed; /* == n_splats; > max_splats on TCGS_ERR_CAPACITY */
+    float ms_preprocess, ms_sort, ms_blend; /* stage device times of the frame when it ran with opts->timing = 1
+                                               (FragmentStats.stage_ms preprocess / sorting / blending), else 0 */
+    float reserved;
 } tcgs_stats;
 
 /* Bytes of device workspace for P Gaussians, a width x height frame and at most max_splats splats. */
@@ -184,7 +206,9 @@ int tcgs_copy_lists(const void *ws, int64_t P, const tcgs_camera *cam, const tcg
                     int64_t max_splats, int32_t *ids_out, int32_t *ranges_out, void *stream);
 
 /* Debug: copy per-Gaussian projection results (device -> device): visible u8 [P], mean2d [P,2] f64,
- * conic [P,3] f64, depth [P] f64, radius [P] i32, rgb [P,3] f32. */
+ * conic [P,3] f64, depth [P] f64, radius [P] i32, rgb [P,3] f32.  Needs the frame's tcgs_preprocess to have run
+ * with opts->debug = 1 (the float64 buffers are written only then); TCGS_ERR_INVALID_ARG otherwise.
+ * Synchronises `stream`. */
 int tcgs_copy_projection(const void *ws, int64_t P, const tcgs_camera *cam, int64_t max_splats,
                          uint8_t *visible, double *mean2d, double *conic, double *depth, int32_t *radius,
                          float *rgb, void *stream);
@@ -196,7 +220,8 @@ int tcgs_copy_projection(const void *ws, int64_t P, const tcgs_camera *cam, int6
 int tcgs_tile_row_counts(const void *ws, int64_t P, const tcgs_camera *cam, int64_t max_splats, int64_t *row_counts,
                          void *stream);
 
-/* 0 if the current device is sm_100 (B200); TCGS_ERR_DEVICE otherwise. */
+/* 0 if the current device is sm_100 (B200); TCGS_ERR_DEVICE otherwise.  Every entry point that launches work
+ * runs this check (cached per device) and returns TCGS_ERR_DEVICE on another GPU. */
 int tcgs_device_check(void);
 
 /* Number of kernels libtcgs.so has launched so far in this process (all streams, all devices). */

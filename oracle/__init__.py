@@ -67,6 +67,8 @@ def _load():
         lib.oracle_blend.restype = None
         lib.oracle_blend.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P, P, P,
                                      P, P, P, P]
+        lib.oracle_classify.restype = None
+        lib.oracle_classify.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P, P, P]
         lib.oracle_blend_const_alpha.restype = None
         lib.oracle_blend_const_alpha.argtypes = [ctypes.c_int, P, P, P, P, P, P]
         lib.oracle_sh_color.restype = None
@@ -241,6 +243,23 @@ def render(means, scales, rotations, opacities, colors, cam, early_cull: bool = 
                         stage_ms={"preprocess": (t1 - t0) * 1e3, "sorting": (t2 - t1) * 1e3,
                                   "blending": (t3 - t2) * 1e3})
     return OracleFrame(rgb, T, cnt, stats, offsets, ids, proj)
+
+
+def classify(proj: Projection, offsets, ids, opacity, cam, band=None) -> np.ndarray:
+    """Per-fragment classes of the reference blend loop: uint8 [N, 256] (1 cull, 2 blend, 3 terminate, 0 not
+    reached / out of the image) for tile-list entry j and tile pixel 16 row + col (tcgs_oracle.c)."""
+    lib = _load()
+    cam = OCamera.from_any(cam)
+    r0, r1 = band if band is not None else (0, cam.tiles_y)
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    n = ids.size
+    cls = np.zeros((max(n, 1), 256), np.uint8)
+    if n == 0:
+        return cls[:0]
+    lib.oracle_classify(cam.width, cam.height, r0, r1, _p(offsets), _p(ids), _p(proj.mean2d), _p(proj.inv_cov),
+                        _p(_f64(opacity).reshape(-1)), _p(cls))
+    return cls
 
 
 def blend_const_alpha(alphas, colors):

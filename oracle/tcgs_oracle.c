@@ -303,6 +303,42 @@ void oracle_blend(int width, int height, int tile_row_begin, int tile_row_end, c
  * Single-tile blend with caller-given per-splat alpha (the ConstantAlpha
  * evaluator of tests/test_raster.py:21-29), for the reference's blend KATs.
  */
+/* Per-fragment classification of the reference blend loop (src/tilesplat/raster.py:110-146 with
+ * alpha_reference, :67-94): cls[j*256 + 16*row + col] for tile-list entry j and tile pixel (col, row) is
+ * 1 cull (alpha < 1/255), 2 blend, 3 terminate (T - alpha T < 1e-4, checked before compositing); entries the
+ * pixel never reaches (after its termination) and out-of-image pixels stay 0.  Test infrastructure: the
+ * first-divergent-fragment check of the GPU's contributor counts (tests/parity_util.py). */
+void oracle_classify(int width, int height, int tile_row_begin, int tile_row_end, const int64_t *offsets,
+                     const int32_t *ids, const double *mean2d, const double *inv_cov, const double *opacity,
+                     uint8_t *cls) {
+    int tiles_x = (width + TILE - 1) / TILE;
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+    for (int ty = tile_row_begin; ty < tile_row_end; ty++) {
+        for (int tx = 0; tx < tiles_x; tx++) {
+            int64_t t = (int64_t)ty * tiles_x + tx;
+            int64_t b = offsets[t], e = offsets[t + 1];
+            for (int py = ty * TILE; py < ty * TILE + TILE && py < height; py++) {
+                for (int px = tx * TILE; px < tx * TILE + TILE && px < width; px++) {
+                    const int64_t pix = (int64_t)(py - ty * TILE) * TILE + (px - tx * TILE);
+                    double T = 1.0;
+                    for (int64_t j = b; j < e; j++) {
+                        int64_t g = ids[j];
+                        double s11 = inv_cov[3 * g], s12 = inv_cov[3 * g + 1], s22 = inv_cov[3 * g + 2];
+                        double dx = mean2d[2 * g] - (double)px;
+                        double dy = mean2d[2 * g + 1] - (double)py;
+                        double q = s11 * dx * dx + 2.0 * s12 * dx * dy + s22 * dy * dy;
+                        double alpha = opacity[g] * exp(-0.5 * q);
+                        if (alpha < ALPHA_CULL) { cls[j * 256 + pix] = 1; continue; }
+                        if (T - alpha * T < TERM_THRESHOLD) { cls[j * 256 + pix] = 3; break; }
+                        cls[j * 256 + pix] = 2;
+                        T = T - alpha * T;
+                    }
+                }
+            }
+        }
+    }
+}
+
 void oracle_blend_const_alpha(int n, const double *alpha, const double *color, double *rgb, double *T_out,
                               int32_t *count_out, int64_t *stats) {
     int64_t fb = 0, fc = 0, fs = 0, pt = 0;

@@ -20,6 +20,7 @@ TCGS_ERR_WORKSPACE = -5
 ALPHA_TC_HILO = 0
 ALPHA_TC_K8 = 1
 ALPHA_FFMA = 2
+ALPHA_TC_K8_GLOBAL = 3
 
 IPC_HANDLE_BYTES = 64
 
@@ -42,7 +43,9 @@ class Camera(ctypes.Structure):
 class Opts(ctypes.Structure):
     _fields_ = [("tile_row_begin", ctypes.c_int32), ("tile_row_end", ctypes.c_int32),
                 ("alpha_mode", ctypes.c_int32), ("early_cull", ctypes.c_int32), ("debug", ctypes.c_int32),
-                ("coverage", ctypes.c_int32), ("defer_colour", ctypes.c_int32), ("schedule", ctypes.c_int32)]
+                ("coverage", ctypes.c_int32), ("defer_colour", ctypes.c_int32), ("schedule", ctypes.c_int32),
+                ("timing", ctypes.c_int32), ("reserved", ctypes.c_int32), ("dump_beta", ctypes.c_void_p),
+                ("dump_class", ctypes.c_void_p)]
 
 
 SCHEDULE = {"dynamic": 0, "static": 1}  # enum tcgs_schedule (include/tcgs.h)
@@ -55,7 +58,8 @@ class Stats(ctypes.Structure):
     _fields_ = [("n_splats", ctypes.c_int64), ("dropped", ctypes.c_int64), ("f_blend", ctypes.c_int64),
                 ("f_cull", ctypes.c_int64), ("f_skip", ctypes.c_int64), ("exp_calls", ctypes.c_int64),
                 ("pixels_terminated", ctypes.c_int64), ("n_visible", ctypes.c_int64),
-                ("max_splats_needed", ctypes.c_int64)]
+                ("max_splats_needed", ctypes.c_int64), ("ms_preprocess", ctypes.c_float), ("ms_sort", ctypes.c_float),
+                ("ms_blend", ctypes.c_float), ("reserved", ctypes.c_float)]
 
 
 # name -> (restype, argtypes); every symbol include/tcgs.h declares

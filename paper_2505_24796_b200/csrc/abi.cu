@@ -3,6 +3,8 @@
 #include <string.h>
 
 #include <atomic>
+#include <mutex>
+#include <unordered_map>
 
 #include "tcgs_internal.cuh"
 
@@ -10,6 +12,8 @@ using namespace tcgs;
 
 static std::atomic<unsigned long long> g_launches{0};
 void tcgs::note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+extern "C" int tcgs_device_check(void);
 
 namespace {
 
@@ -25,22 +29,73 @@ int cuda_fail(cudaError_t e, const char *where) {
     return TCGS_ERR_CUDA;
 }
 
-__global__ void init_counters(DevCounters *c) {
+__global__ void init_counters(DevCounters *c, int debug) {
     DevCounters z;
     memset(&z, 0, sizeof(z));
     z.key_min = ~0ull;
+    z.debug_written = debug;
     *c = z;
 }
 
 struct CounterSet {
     DevCounters *c[TCGS_MAX_VIEWS_PER_PASS];
 };
-__global__ void init_counters_views(const __grid_constant__ CounterSet s, int n) {
+__global__ void init_counters_views(const __grid_constant__ CounterSet s, int n, int debug) {
     if ((int)threadIdx.x < n) {
         DevCounters z;
         memset(&z, 0, sizeof(z));
         z.key_min = ~0ull;
+        z.debug_written = debug;
         *s.c[threadIdx.x] = z;
+    }
+}
+
+// sm_100 check, cached per device (every launching entry point runs it)
+int device_ok() {
+    static std::atomic<int> cache[TCGS_MAX_DEVICES];  // 0 unknown, 1 ok, -1 not sm_100
+    const int d = current_device();
+    int v = cache[d].load(std::memory_order_relaxed);
+    if (v == 0) {
+        v = tcgs_device_check() == TCGS_OK ? 1 : -1;
+        cache[d].store(v, std::memory_order_relaxed);
+    }
+    if (v < 0) return fail(TCGS_ERR_DEVICE, "libtcgs.so is built for sm_100a (B200); the current device is not sm_100");
+    return TCGS_OK;
+}
+
+// ---- stage timing (opts->timing): CUDA events per workspace, read back by tcgs_read_stats
+enum { ST_PRE = 0, ST_SORT = 1, ST_BLEND = 2 };
+struct StageTimer {
+    cudaEvent_t ev[3][2] = {};
+    bool recorded[3] = {false, false, false};
+};
+std::mutex g_timer_mu;
+std::unordered_map<const void *, StageTimer> g_timers;
+
+void time_mark(const tcgs_opts *opts, const void *ws, int stage, int end, cudaStream_t st) {
+    if (!opts || !opts->timing) return;
+    std::lock_guard<std::mutex> lk(g_timer_mu);
+    StageTimer &t = g_timers[ws];
+    cudaEvent_t &e = t.ev[stage][end];
+    if (!e && cudaEventCreate(&e) != cudaSuccess) {
+        e = nullptr;
+        return;
+    }
+    cudaEventRecord(e, st);
+    if (end) t.recorded[stage] = true;
+}
+
+// after the stream has been synchronised: the stage times recorded since the last read (0 if none)
+void time_read(const void *ws, tcgs_stats *stats) {
+    std::lock_guard<std::mutex> lk(g_timer_mu);
+    auto it = g_timers.find(ws);
+    if (it == g_timers.end()) return;
+    float *dst[3] = {&stats->ms_preprocess, &stats->ms_sort, &stats->ms_blend};
+    for (int s = 0; s < 3; s++) {
+        if (!it->second.recorded[s]) continue;
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, it->second.ev[s][0], it->second.ev[s][1]) == cudaSuccess) *dst[s] = ms;
+        it->second.recorded[s] = false;
     }
 }
 
@@ -54,7 +109,7 @@ int check_scene(const tcgs_scene *scene) {
 }
 
 int check_common(const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes, int64_t P,
-                 int64_t max_splats) {
+                 int64_t max_splats, bool device = true) {
     if (!cam || !ws) return fail(TCGS_ERR_INVALID_ARG, "null camera or workspace");
     if (cam->width <= 0 || cam->height <= 0) return fail(TCGS_ERR_INVALID_ARG, "image dimensions must be positive");
     if (!(cam->fx > 0) || !(cam->fy > 0)) return fail(TCGS_ERR_INVALID_ARG, "focal lengths must be positive");
@@ -64,7 +119,7 @@ int check_common(const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t
     const int tx = (cam->width + TILE - 1) / TILE, ty = (cam->height + TILE - 1) / TILE;
     if (tx > 32767 || ty > 32767) return fail(TCGS_ERR_INVALID_ARG, "image too large");
     if (opts) {
-        if (opts->alpha_mode < 0 || opts->alpha_mode > TCGS_ALPHA_FFMA)
+        if (opts->alpha_mode < 0 || opts->alpha_mode > TCGS_ALPHA_TC_K8_GLOBAL)
             return fail(TCGS_ERR_INVALID_ARG, "unknown alpha mode");
         if (opts->coverage < TCGS_COVER_SQUARE || opts->coverage > TCGS_COVER_ELLIPSE)
             return fail(TCGS_ERR_INVALID_ARG, "unknown coverage mode");
@@ -73,10 +128,12 @@ int check_common(const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t
         if (opts->tile_row_end > 0 && (opts->tile_row_begin < 0 || opts->tile_row_begin >= opts->tile_row_end ||
                                        opts->tile_row_end > ty))
             return fail(TCGS_ERR_INVALID_ARG, "invalid tile-row band");
+        if ((opts->dump_beta == nullptr) != (opts->dump_class == nullptr))
+            return fail(TCGS_ERR_INVALID_ARG, "dump_beta and dump_class must both be set or both be NULL");
     }
     if (ws_bytes < Layout::make(P, cam->width, cam->height, max_splats).total)
         return fail(TCGS_ERR_WORKSPACE, "workspace smaller than tcgs_workspace_size()");
-    return TCGS_OK;
+    return device ? device_ok() : TCGS_OK;
 }
 
 }  // namespace
@@ -126,11 +183,13 @@ int tcgs_preprocess(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     const Layout L = Layout::make(scene->P, cam->width, cam->height, max_splats);
+    time_mark(opts, ws, ST_PRE, 0, st);
     note_launch();
-    init_counters<<<1, 1, 0, st>>>(at<DevCounters>(ws, L.counters));
+    init_counters<<<1, 1, 0, st>>>(at<DevCounters>(ws, L.counters), opts ? opts->debug : 0);
     cudaError_t e = launch_preprocess(*scene, *cam, make_band(*cam, opts), opts ? opts->debug : 0,
                                       opts ? opts->coverage : 0, opts ? opts->defer_colour : 0, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "preprocess");
+    time_mark(opts, ws, ST_PRE, 1, st);
     return TCGS_OK;
 }
 
@@ -157,7 +216,7 @@ int tcgs_preprocess_views(const tcgs_scene *scene, const tcgs_camera *cams, int3
     Band bands[TCGS_MAX_VIEWS_PER_PASS];
     CounterSet cs;
     for (int v = 0; v < n_views; v++) {
-        rc = check_common(&cams[v], opts, ws[v], ws_bytes, scene->P, max_splats);
+        rc = check_common(&cams[v], opts, ws[v], ws_bytes, scene->P, max_splats, false);
         if (rc) return rc;
         for (int u = 0; u < v; u++)
             if (ws[u] == ws[v]) return fail(TCGS_ERR_INVALID_ARG, "views need distinct workspaces");
@@ -165,9 +224,10 @@ int tcgs_preprocess_views(const tcgs_scene *scene, const tcgs_camera *cams, int3
         bands[v] = make_band(cams[v], opts);
         cs.c[v] = at<DevCounters>(ws[v], L[v].counters);
     }
+    if ((rc = device_ok())) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     note_launch();
-    init_counters_views<<<1, 32, 0, st>>>(cs, n_views);
+    init_counters_views<<<1, 32, 0, st>>>(cs, n_views, opts ? opts->debug : 0);
     cudaError_t e = launch_preprocess_views(*scene, cams, bands, n_views, opts ? opts->debug : 0,
                                             opts ? opts->coverage : 0, opts ? opts->defer_colour : 0, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "preprocess_views");
@@ -179,8 +239,10 @@ int tcgs_bin(int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, void *ws,
     int rc = check_common(cam, opts, ws, ws_bytes, P, max_splats);
     if (rc) return rc;
     const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
+    time_mark(opts, ws, ST_SORT, 0, (cudaStream_t)stream);
     cudaError_t e = launch_bin(P, make_band(*cam, opts), ws, L, max_splats, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "bin");
+    time_mark(opts, ws, ST_SORT, 1, (cudaStream_t)stream);
     return TCGS_OK;
 }
 
@@ -190,9 +252,12 @@ int tcgs_blend(int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, void *w
     if (rc) return rc;
     if (!rgb || !T || !n_contrib) return fail(TCGS_ERR_INVALID_ARG, "null output");
     const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
-    cudaError_t e = launch_render(opts ? opts->alpha_mode : 0, *cam, make_band(*cam, opts), nullptr, ws, L, rgb, T,
-                                  n_contrib, (cudaStream_t)stream);
+    time_mark(opts, ws, ST_BLEND, 0, (cudaStream_t)stream);
+    cudaError_t e = launch_render(opts ? opts->alpha_mode : 0, opts ? opts->early_cull : 1,
+                                  opts ? opts->dump_beta : nullptr, opts ? opts->dump_class : nullptr, *cam,
+                                  make_band(*cam, opts), nullptr, ws, L, rgb, T, n_contrib, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "render");
+    time_mark(opts, ws, ST_BLEND, 1, (cudaStream_t)stream);
     return TCGS_OK;
 }
 
@@ -233,7 +298,9 @@ int tcgs_read_stats(const void *ws, int64_t P, const tcgs_opts *opts, tcgs_stats
     cudaError_t e = cudaMemcpyAsync(&c, ws, sizeof(c), cudaMemcpyDeviceToHost, st);  // counters sit at offset 0
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "read_stats");
-    return decode_stats(c, opts, stats);
+    const int rc = decode_stats(c, opts, stats);
+    time_read(ws, stats);
+    return rc;
 }
 
 size_t tcgs_counters_bytes(void) { return sizeof(DevCounters); }
@@ -299,11 +366,12 @@ int tcgs_blend_lists(int64_t P, const double *mean2d, const double *conic, const
     const Layout L = Layout::make(P, cam->width, cam->height, 1);
     const Band band = make_band(*cam, opts);
     note_launch();
-    init_counters<<<1, 1, 0, st>>>(at<DevCounters>(ws, L.counters));
+    init_counters<<<1, 1, 0, st>>>(at<DevCounters>(ws, L.counters), 0);
     cudaError_t e = launch_pack_lists(P, mean2d, conic, opacity, colors, offsets, band, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "pack_lists");
-    e = launch_render(opts ? opts->alpha_mode : 0, *cam, band, reinterpret_cast<const uint32_t *>(ids), ws, L, rgb, T,
-                      n_contrib, st);
+    e = launch_render(opts ? opts->alpha_mode : 0, opts ? opts->early_cull : 1, opts ? opts->dump_beta : nullptr,
+                      opts ? opts->dump_class : nullptr, *cam, band, reinterpret_cast<const uint32_t *>(ids), ws, L,
+                      rgb, T, n_contrib, st);
     if (e != cudaSuccess) return cuda_fail(e, "render");
     return TCGS_OK;
 }
@@ -311,6 +379,7 @@ int tcgs_blend_lists(int64_t P, const double *mean2d, const double *conic, const
 int tcgs_copy_lists(const void *ws, int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, int64_t max_splats,
                     int32_t *ids_out, int32_t *ranges_out, void *stream) {
     if (!ws || !cam || !ids_out || !ranges_out) return fail(TCGS_ERR_INVALID_ARG, "null argument");
+    if (int rc = device_ok()) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
     DevCounters c;
@@ -332,6 +401,7 @@ int tcgs_tile_row_counts(const void *ws, int64_t P, const tcgs_camera *cam, int6
                          void *stream) {
     if (!ws || !cam || !row_counts) return fail(TCGS_ERR_INVALID_ARG, "null argument");
     if (cam->width <= 0 || cam->height <= 0) return fail(TCGS_ERR_INVALID_ARG, "image dimensions must be positive");
+    if (int rc = device_ok()) return rc;
     const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
     cudaError_t e = launch_row_counts(P, make_band(*cam, nullptr), ws, L, row_counts, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "tile_row_counts");
@@ -367,10 +437,18 @@ extern "C" int tcgs_copy_projection(const void *ws, int64_t P, const tcgs_camera
                                     float *rgb, void *stream) {
     if (!ws || !cam || !visible || !mean2d || !conic || !depth || !radius || !rgb)
         return fail(TCGS_ERR_INVALID_ARG, "null argument");
+    if (int rc = device_ok()) return rc;
     if (P <= 0) return TCGS_OK;
     const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
+    cudaStream_t st = (cudaStream_t)stream;
+    DevCounters c;
+    cudaError_t e0 = cudaMemcpyAsync(&c, ws, sizeof(c), cudaMemcpyDeviceToHost, st);
+    if (e0 == cudaSuccess) e0 = cudaStreamSynchronize(st);
+    if (e0 != cudaSuccess) return cuda_fail(e0, "copy_projection");
+    if (!c.debug_written)
+        return fail(TCGS_ERR_INVALID_ARG, "tcgs_copy_projection needs the frame preprocessed with opts->debug = 1");
     note_launch();
-    copy_projection_kernel<<<(unsigned)((P + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+    copy_projection_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(
         P, at<int32_t>(ws, L.radius), at<Rec>(ws, L.rec), at<double>(ws, L.dbg_conic), at<double>(ws, L.dbg_depth),
         at<double>(ws, L.dbg_mean2d), visible, mean2d, conic, depth, radius, rgb);
     cudaError_t e = cudaGetLastError();

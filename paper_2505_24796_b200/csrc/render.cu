@@ -61,7 +61,17 @@ struct RenderArgs {
     float *rgb;
     float *T;
     int32_t *n_contrib;
+    float *dump_beta;      // debug (FL_DUMP): beta' of every evaluated (list entry, pixel), [N][256]
+    uint8_t *dump_class;   // debug (FL_DUMP): 1 cull, 2 blend, 3 terminate; 0 = not evaluated, [N][256]
 };
+
+// K7 variants (template flags): FL_ECOFF = EarlyCull off -- alpha = 2^beta' for every active fragment and the
+// cull on alpha < 1/255 afterwards (the reference's alpha_reference order, src/tilesplat/raster.py:86-94 /
+// tensor_path.py:155-160), no dead-Gaussian box test in the producer; FL_DUMP = debug dump of beta' and the
+// per-fragment classification (the a19 tolerance oracle, tests/test_gpu_beta.py).
+constexpr int FL_ECOFF = 1;
+constexpr int FL_DUMP = 2;
+constexpr float ALPHA_CUT = 1.0f / 255.0f;  // src/tilesplat/raster.py:15
 
 struct StageMeta {
     int tile;        // -1: no more tiles
@@ -79,6 +89,8 @@ struct __align__(1024) K7Smem {
     float4 vf[S][K7_BATCH][2];          // FFMA mode: fp32 coefficients
     float4 col[S][K7_BATCH];            // colours
     uint32_t dead_before[S][K7_BATCH];  // dead Gaussians before each live one (list order)
+    uint32_t pos[S][K7_BATCH];          // FL_DUMP: tile-list index of each live row
+    __half Ug[S][2][128 * 16];          // TC_K8_GLOBAL: per-stage A operands (global pixel coordinates)
     StageMeta meta[S];
     unsigned long long full[S], empty[S], mma_done[NB], tmem_empty[NB], tok[K7_PRODUCERS];
     uint32_t tmem_base;
@@ -173,6 +185,8 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // tile's pixel box [-8,7]^2: the minimum of the convex quadratic q(d - u) over the box is exact (interior
 // minimiser or the clamped minimiser on one of the four edges), and the test keeps a 0.01 margin on
 // beta, so every fragment of a dead Gaussian in this tile is a cull in exact arithmetic too.
+// BOXCULL = false (EarlyCull off, global coordinates): every Gaussian of the list is live.
+template <bool BOXCULL>
 __device__ __forceinline__ bool gaussian_coeffs(const Rec &r, float ox, float oy, float v[6]) {
     // mean - centre in fp32: hi - centre is exact for frame coordinates (both on the hi value's grid),
     // then one rounding with the lo part -- the float64 difference to within an ulp of dx, with no FP64 op
@@ -180,7 +194,7 @@ __device__ __forceinline__ bool gaussian_coeffs(const Rec &r, float ox, float oy
     const float s11 = r.s11, s12 = r.s12, s22 = r.s22;
     const float q = s11 * dx * dx + 2.0f * s12 * dx * dy + s22 * dy * dy;
     const bool outside = !(dx >= -8.0f && dx <= 7.0f && dy >= -8.0f && dy <= 7.0f);
-    if (outside && s11 > 1e-30f && s22 > 1e-30f) {
+    if (BOXCULL && outside && s11 > 1e-30f && s22 > 1e-30f) {
         // (the minimiser only needs to be accurate to first order: q is flat there, and the test keeps a margin;
         // the normal-range guard above lets the reciprocal skip denormal handling)
         const float r11 = s12 * rcp_approx(s11), r22 = s12 * rcp_approx(s22);
@@ -223,7 +237,7 @@ __device__ __forceinline__ float f32(__half x) { return __half2float(x); }
 template <int MODE>
 __device__ __forceinline__ void make_vrow(const float v[6], uint4 &lo8, uint4 &hi8) {
     __align__(16) __half e[16];
-    if (MODE == TCGS_ALPHA_TC_K8) {  // [v0/3, v0/3, v0/3, v1..v5] in fp16, the rest zero
+    if (MODE == TCGS_ALPHA_TC_K8 || MODE == TCGS_ALPHA_TC_K8_GLOBAL) {  // [v0/3, v0/3, v0/3, v1..v5] in fp16, the rest zero
         const __half third = h16(v[0] / 3.0f);
         e[0] = third;
         e[1] = third;
@@ -329,9 +343,38 @@ __device__ __forceinline__ void cursor_next(Cursor &k, const RenderArgs &a, K7Sm
     }
 }
 
-template <int MODE, bool DYN>
+// Global-coordinate A operand of one stage (TC_K8_GLOBAL, the paper's Frag2Mat-without-G2L ablation): pixel
+// rows [1, 1, 1, x, y, x^2, xy, y^2, 0 ...] in fp16 (x^2 overflows for x >= 256, as tensor_path.py:92-100 with
+// coords="global" does under the fp16 model), in the consumer's TMEM-lane order.
+__device__ __forceinline__ void write_global_u(__half (*ug)[128 * 16], int tile, const RenderArgs &a, int lane) {
+    const int tx = tile % a.tiles_x, ty = a.band_y0 + tile / a.tiles_x;
+#pragma unroll 1
+    for (int q = 0; q < 8; q++) {
+        const int row = q * 32 + lane;  // 0..255: half row >> 7, TMEM lane row & 127
+        const int h = row >> 7, r = row & 127;
+        const int w = (r >> 5) + 4 * h;  // consumer warp owning the lane
+        const float x = (float)(tx * TILE + 8 * (w & 1) + (lane & 7));
+        const float y = (float)(ty * TILE + 4 * ((w >> 1) & 3) + (lane >> 3));
+        __align__(16) __half e[16];
+        e[0] = e[1] = e[2] = __float2half_rn(1.0f);
+        e[3] = __float2half_rn(x);
+        e[4] = __float2half_rn(y);
+        e[5] = __float2half_rn(x * x);
+        e[6] = __float2half_rn(x * y);
+        e[7] = __float2half_rn(y * y);
+#pragma unroll
+        for (int k = 8; k < 16; k++) e[k] = __float2half_rn(0.0f);
+        *reinterpret_cast<uint4 *>(ug[h] + kmaj_off(r, 0)) = reinterpret_cast<const uint4 *>(e)[0];
+        *reinterpret_cast<uint4 *>(ug[h] + kmaj_off(r, 8)) = reinterpret_cast<const uint4 *>(e)[1];
+    }
+}
+
+template <int MODE, bool DYN, int FL>
 __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, uint32_t tmem, int p) {
     constexpr bool TC = MODE != TCGS_ALPHA_FFMA;
+    constexpr bool GLOBAL = MODE == TCGS_ALPHA_TC_K8_GLOBAL;
+    constexpr bool BOXCULL = !(FL & FL_ECOFF) && !GLOBAL;
+    constexpr bool DUMP = (FL & FL_DUMP) != 0;
     constexpr int NP = K7_PRODUCERS;
     const int lane = threadIdx.x & 31;
     const unsigned FULL = 0xffffffffu, lt = lanemask_lt();
@@ -378,7 +421,14 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
         const bool valid = cur.c * 32 + lane < cur.n;
         float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool live = false;
-        if (valid) live = gaussian_coeffs(rc, cur.ox, cur.oy, v);  // tile_center (tensor_path.py:21-22)
+        // tile_center (tensor_path.py:21-22); the global-coordinate ablation keeps the origin at (0, 0)
+        if (valid) live = gaussian_coeffs<BOXCULL>(rc, GLOBAL ? 0.0f : cur.ox, GLOBAL ? 0.0f : cur.oy, v);
+        if (DUMP && valid && !live) {  // dead on the whole tile (box test): class 4 at every pixel
+            uint4 *row = reinterpret_cast<uint4 *>(a.dump_class + (size_t)(cur.beg + cur.c * 32 + lane) * 256);
+            const uint4 four = make_uint4(0x04040404u, 0x04040404u, 0x04040404u, 0x04040404u);
+#pragma unroll 1
+            for (int q = 0; q < 16; q++) row[q] = four;
+        }
         uint4 vlo = make_uint4(0, 0, 0, 0), vhi = make_uint4(0, 0, 0, 0);
         if (TC && live) make_vrow<MODE>(v, vlo, vhi);
         const float4 col = make_float4(rc.r, rc.g, rc.b, 0.f);
@@ -408,6 +458,7 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
                     sm.vf[st][row][1] = make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
+            if (GLOBAL && tile >= 0) write_global_u(sm.Ug[st], tile, a, lane);
             if (TC) fence_async_smem();
             __syncwarp();
             if (lane == 0) {
@@ -427,7 +478,8 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
                     const uint64_t bdesc = umma_desc(sm.V[st]);
 #pragma unroll
                     for (int h = 0; h < 2; h++)
-                        mma_f16(tmem + b * (2 * K7_BATCH) + h * K7_BATCH, umma_desc(sm.U[h]), bdesc, IDESC);
+                        mma_f16(tmem + b * (2 * K7_BATCH) + h * K7_BATCH, umma_desc(GLOBAL ? sm.Ug[st][h] : sm.U[h]),
+                                bdesc, IDESC);
                     mma_commit(&sm.mma_done[b]);
                 }
             }
@@ -465,6 +517,7 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
                 }
                 sm.col[st][row] = col;
                 sm.dead_before[st][row] = my_dead;
+                if (DUMP) sm.pos[st][row] = cur.beg + (uint32_t)(cur.c * 32 + lane);
             };
             if (nl > 0) acquire();
             if (live && slot < K7_BATCH) put(slot);
@@ -504,12 +557,16 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
 }
 
 // ------------------------------------------------------------------------------------------ kernel
-template <int MODE, bool DYN>
+template <int MODE, bool DYN, int FL>
 __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(RenderArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     K7Smem &sm = *reinterpret_cast<K7Smem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr bool TC = MODE != TCGS_ALPHA_FFMA;
+    constexpr bool EC = !(FL & FL_ECOFF);       // EarlyCull: the cull decided on beta' before any ex2
+    constexpr bool DUMP = (FL & FL_DUMP) != 0;
+    constexpr bool GLOBAL = MODE == TCGS_ALPHA_TC_K8_GLOBAL;
+    constexpr float INF = __builtin_huge_valf();
     const unsigned FULL = 0xffffffffu;
 
     // pixels owned by a consumer thread.  NPIX = 1: warp w covers an 8x4 block, TMEM lanes 32(w%4).. of
@@ -571,7 +628,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
 
     unsigned long long s_blend = 0, s_cull = 0, s_term = 0, s_pairs = 0;
     if (warp >= K7_CONSUMER_WARPS) {
-        producer<MODE, DYN>(sm, a, ids, tmem, warp - K7_CONSUMER_WARPS);
+        producer<MODE, DYN, FL>(sm, a, ids, tmem, warp - K7_CONSUMER_WARPS);
     } else {
         int cur_seq = -1, cur_tile = -1;
         int px[NPIX], py[NPIX];
@@ -663,9 +720,10 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 for (int h = 0; h < NPIX; h++) {
                     live0[h] = !done[h];
                     jt[h] = K7_BATCH;
-                    // pass threshold of beta: the EarlyCull cut while the pixel is live, +inf once it has
-                    // terminated (a float, so the test stays one FSETP and the update a predicated move)
-                    thr[h] = done[h] ? __int_as_float(0x7f800000) : CUT_LOG2;
+                    // pass threshold: the EarlyCull cut of beta' (EC) or the 1/255 cut of alpha (EarlyCull off)
+                    // while the pixel is live, +inf once it has terminated (a float, so the test stays one FSETP
+                    // and the update a predicated move)
+                    thr[h] = done[h] ? INF : (EC ? CUT_LOG2 : ALPHA_CUT);
                     fcnt0[h] = fcnt[h];
                     tb[h] = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (2 * K7_BATCH) + hf[h] * K7_BATCH;
                 }
@@ -673,10 +731,33 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 // +inf once done); a warp vote skips the column when no pixel of the warp passes (uniform branch)
                 auto column = [&](const uint32_t (&rb)[NPIX], int col) {
                     bool p[NPIX], any = false;
+                    float alv[NPIX];
 #pragma unroll
                     for (int h = 0; h < NPIX; h++) {
-                        p[h] = __uint_as_float(rb[h]) >= thr[h];  // (columns >= n_live hold beta = -65504: never pass)
+                        const float bt = __uint_as_float(rb[h]);
+                        if (EC) {
+                            p[h] = bt >= thr[h];  // (columns >= n_live hold beta = -65504: never pass)
+                            // fp16 global coordinates can overflow: a non-finite beta is a cull (tensor_path.py:113)
+                            if (GLOBAL) p[h] = p[h] && bt < INF;
+                        } else {  // EarlyCull off: the exponential of every active fragment, then the alpha cut
+                            alv[h] = ex2_approx(bt);
+                            p[h] = alv[h] >= thr[h];
+                        }
                         any = any || p[h];
+                    }
+                    if (DUMP) {
+                        const uint32_t e = sm.pos[st][col < nl ? col : 0];
+#pragma unroll
+                        for (int h = 0; h < NPIX; h++) {
+                            if (col < nl && inside[h]) {
+                                const size_t o = (size_t)e * 256 + (size_t)(ly[h] * TILE + lx[h]);
+                                a.dump_beta[o] = __uint_as_float(rb[h]);
+                                if (thr[h] != INF) {  // reached: classify as the blend below does
+                                    const float al = ex2_approx(__uint_as_float(rb[h]));
+                                    a.dump_class[o] = !p[h] ? 1 : (fmaf(-al, T[h], T[h]) < TERM_T ? 3 : 2);
+                                }
+                            }
+                        }
                     }
                     if (__any_sync(FULL, any)) {
 #ifdef TCGS_K7_PROFILE
@@ -687,7 +768,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                         for (int h = 0; h < NPIX; h++) {
                             // alpha = 2^beta' (no min(alpha, 1): alpha > 1 only by rounding, and then
                             // T - alpha T < 1e-4 terminates exactly as alpha = 1 would)
-                            const float al = ex2_approx(__uint_as_float(rb[h]));
+                            const float al = EC ? ex2_approx(__uint_as_float(rb[h])) : alv[h];
                             const float tn = fmaf(-al, T[h], T[h]);
                             if (p[h] && tn < TERM_T) {  // termination precedes compositing
                                 jt[h] = col;
@@ -816,24 +897,36 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
     }
 }
 
-template <int MODE, bool DYN>
+template <int MODE, bool DYN, int FL>
 cudaError_t launch_mode(const RenderArgs &a, int num_sms, cudaStream_t st) {
     static bool configured_dev[TCGS_MAX_DEVICES] = {};
     bool &configured = configured_dev[current_device()];
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(render_kernel<MODE, DYN>, cudaFuncAttributeMaxDynamicSharedMemorySize, K7_SMEM_BYTES);
+        cudaError_t e = cudaFuncSetAttribute(render_kernel<MODE, DYN, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             K7_SMEM_BYTES);
         if (e != cudaSuccess) return e;
         configured = true;
     }
     const int grid = num_sms * K7_CTAS_PER_SM;
     note_launch();
-    render_kernel<MODE, DYN><<<grid, K7_THREADS, K7_SMEM_BYTES, st>>>(a);
+    render_kernel<MODE, DYN, FL><<<grid, K7_THREADS, K7_SMEM_BYTES, st>>>(a);
     return cudaGetLastError();
+}
+
+// EarlyCull on/off for the lone-frame (dynamic) and frames-in-flight (static) schedules; the debug dump runs
+// with the static schedule.
+template <int MODE>
+cudaError_t launch_variant(const RenderArgs &a, bool dyn, bool early_cull, bool dump, int sms, cudaStream_t st) {
+    if (dump) return early_cull ? launch_mode<MODE, false, FL_DUMP>(a, sms, st)
+                                : launch_mode<MODE, false, FL_DUMP | FL_ECOFF>(a, sms, st);
+    if (early_cull) return dyn ? launch_mode<MODE, true, 0>(a, sms, st) : launch_mode<MODE, false, 0>(a, sms, st);
+    return dyn ? launch_mode<MODE, true, FL_ECOFF>(a, sms, st) : launch_mode<MODE, false, FL_ECOFF>(a, sms, st);
 }
 
 }  // namespace
 
-cudaError_t launch_render(int alpha_mode, const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
+cudaError_t launch_render(int alpha_mode, int early_cull, float *dump_beta, uint8_t *dump_class,
+                          const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
                           void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st) {
     static_assert(sizeof(K7Smem) + 1024 <= K7_SMEM_BYTES, "K7 shared memory");
     RenderArgs a;
@@ -851,6 +944,9 @@ cudaError_t launch_render(int alpha_mode, const tcgs_camera &cam, const Band &ba
     a.rgb = rgb;
     a.T = T;
     a.n_contrib = n_contrib;
+    a.dump_beta = dump_beta;
+    a.dump_class = dump_class;
+    const bool dump = dump_beta != nullptr && dump_class != nullptr;
     // per-launch counters: the tile queue and the fragment statistics (f_blend, f_cull, terminated, pairs)
     cudaError_t e = cudaMemsetAsync(&a.ctr->f_blend, 0, 4 * sizeof(unsigned long long), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(&a.ctr->tile_queue, 0, sizeof(unsigned int), st);
@@ -859,13 +955,14 @@ cudaError_t launch_render(int alpha_mode, const tcgs_camera &cam, const Band &ba
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const bool ec = early_cull != 0;
     switch (alpha_mode) {
-        case TCGS_ALPHA_TC_HILO:
-            return dyn ? launch_mode<TCGS_ALPHA_TC_HILO, true>(a, sms, st) : launch_mode<TCGS_ALPHA_TC_HILO, false>(a, sms, st);
-        case TCGS_ALPHA_TC_K8:
-            return dyn ? launch_mode<TCGS_ALPHA_TC_K8, true>(a, sms, st) : launch_mode<TCGS_ALPHA_TC_K8, false>(a, sms, st);
-        case TCGS_ALPHA_FFMA:
-            return dyn ? launch_mode<TCGS_ALPHA_FFMA, true>(a, sms, st) : launch_mode<TCGS_ALPHA_FFMA, false>(a, sms, st);
+        case TCGS_ALPHA_TC_HILO: return launch_variant<TCGS_ALPHA_TC_HILO>(a, dyn, ec, dump, sms, st);
+        case TCGS_ALPHA_TC_K8: return launch_variant<TCGS_ALPHA_TC_K8>(a, dyn, ec, dump, sms, st);
+        case TCGS_ALPHA_FFMA: return launch_variant<TCGS_ALPHA_FFMA>(a, dyn, ec, dump, sms, st);
+        case TCGS_ALPHA_TC_K8_GLOBAL:  // ablation only: EarlyCull on, static schedule
+            return dump ? launch_mode<TCGS_ALPHA_TC_K8_GLOBAL, false, FL_DUMP>(a, sms, st)
+                        : launch_mode<TCGS_ALPHA_TC_K8_GLOBAL, false, 0>(a, sms, st);
         default: return cudaErrorInvalidValue;
     }
 }

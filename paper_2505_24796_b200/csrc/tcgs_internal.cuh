@@ -144,6 +144,8 @@ struct DevCounters {
     int depth_cur, tile_cur;
     int depth_shift;           // K2: prefix shift of the depth key (0: the prefix sort is exact)
     unsigned int n_long_runs;  // K2 fix-up: runs of equal prefixes longer than a thread handles
+    int debug_written;         // K1 ran with opts.debug (tcgs_copy_projection's float64 buffers are valid)
+    int pad_;
 };
 
 // Per-sort bookkeeping of the onesweep LSD radix sort (all decided on the device).
@@ -239,7 +241,8 @@ cudaError_t launch_preprocess_views(const tcgs_scene &scene, const tcgs_camera *
                                     int debug, int coverage, int defer_colour, void *const *ws, const Layout *L,
                                     cudaStream_t st);
 cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st);
-cudaError_t launch_render(int alpha_mode, const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
+cudaError_t launch_render(int alpha_mode, int early_cull, float *dump_beta, uint8_t *dump_class,
+                          const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
                           void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st);
 cudaError_t launch_pack_lists(int64_t P, const double *mean2d, const double *conic, const double *opacity,
                               const float *colors, const int64_t *offsets, const Band &band, void *ws,

@@ -17,7 +17,6 @@ blend kernel.  Nothing here computes pixels on the CPU.
 from __future__ import annotations
 
 import ctypes
-import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -84,43 +83,83 @@ class ImageBuffer:
 
 @dataclass(frozen=True)
 class Backend:
-    """Selects the alpha mode of the single B200 blend kernel."""
+    """Selects the alpha mode of the single B200 blend kernel.
+
+    ``arith`` says what the kernel computes (it is not the reference's emulation model):
+    ``"fp32"`` (CUDA-core quadratic form), ``"fp16-hilo"`` (tcgen05 fp16, hi/lo split vector, ~22 bits),
+    ``"fp16"`` (tcgen05 fp16, the paper's length-8 vector); ``coords`` is "local" (G2L) or "global".
+    """
 
     name: str
     alpha_mode: int
     early_cull: bool = True
+    coords: str = "local"
+    arith: str = "fp16-hilo"
 
     def tile_evaluator(self, *a, **k):  # the per-fragment protocol (raster.py:86-107) is not crossed
         raise NotImplementedError("the B200 renderer blends whole tiles on the GPU; use render()")
 
 
+# This package's own specs: spec -> (alpha mode, arith)
 _SPECS = {
-    # spec: (alpha mode, EarlyCull accounting)
-    "tcgs": (_abi.ALPHA_TC_HILO, True),
-    "tcgs-hilo": (_abi.ALPHA_TC_HILO, True),
-    "tcgs-fp16": (_abi.ALPHA_TC_K8, True),
-    "tcgs-k8": (_abi.ALPHA_TC_K8, True),
-    "tcgs-ffma": (_abi.ALPHA_FFMA, True),
-    # reference spellings (src/tilesplat/raster.py:149-158, src/tilesplat/cli.py:15)
-    "reference": (_abi.ALPHA_FFMA, False),
-    "frag2mat": (_abi.ALPHA_TC_HILO, True),
-    "frag2mat-fp16": (_abi.ALPHA_TC_K8, True),
-    # tf32 inputs (11-bit mantissa) are served by the hi/lo fp16 split (~22 bits): never less accurate
-    "frag2mat-tf32": (_abi.ALPHA_TC_HILO, True),
+    "tcgs": (_abi.ALPHA_TC_HILO, "fp16-hilo"),
+    "tcgs-hilo": (_abi.ALPHA_TC_HILO, "fp16-hilo"),
+    "tcgs-fp16": (_abi.ALPHA_TC_K8, "fp16"),
+    "tcgs-k8": (_abi.ALPHA_TC_K8, "fp16"),
+    "tcgs-ffma": (_abi.ALPHA_FFMA, "fp32"),
 }
+# The reference's spellings (src/tilesplat/raster.py:149-158, cli.py:15).
+REFERENCE_SPECS = ("reference", "frag2mat", "frag2mat-fp16", "frag2mat-tf32")
 
 
-def make_backend(spec: str = "tcgs", coords: str = "local", batch_width: int = 64,
+def make_backend(spec: str = "tcgs", coords: str | None = None, batch_width: int = 16,
                  use_early_cull: bool = True) -> Backend:
-    """Backend factory mirroring src/tilesplat/raster.py:149-158 (ValueError on unknown specs)."""
+    """Backend factory mirroring src/tilesplat/raster.py:149-158 (ValueError on unknown specs, coordinate modes
+    and batch widths, as src/tilesplat/tensor_path.py:175-181).  ``coords=None`` is the reference's default
+    ("global") for the reference's spellings and "local" for this package's own ``tcgs*`` specs.
+
+    How each reference spelling maps onto the one B200 kernel (nothing is silently approximated):
+
+    * ``"reference"`` -- ReferenceBackend (raster.py:77-107): alpha = o exp(-q/2) for every active fragment,
+      cull on alpha < 1/255 afterwards (EarlyCull off), in fp32 on CUDA cores.  ``coords`` and
+      ``use_early_cull`` are ignored, as the reference ignores them.
+    * ``"frag2mat"`` -- exact arithmetic (float64 in the reference) is served by the fp32 CUDA-core form in
+      tile-local coordinates whatever ``coords`` says: exact global and local evaluation agree to 1e-5
+      (the reference's own criterion 1, tests/test_acceptance.py:44-68), and fp32 global coordinates would
+      only lose precision.  ``use_early_cull`` selects the cull order (tensor_path.py:148-160).
+    * ``"frag2mat-fp16"`` -- the paper's fp16 length-8 vector on tcgen05, in local (G2L) or global
+      coordinates (the precision ablation).
+    * ``"frag2mat-tf32"`` -- not reproduced: ValueError.
+    * ``"tcgs"`` (this package's default), ``"tcgs-fp16"``, ``"tcgs-ffma"`` -- hi/lo fp16 tcgen05, paper
+      K8, fp32 CUDA cores; tile-local coordinates only.
+
+    ``batch_width`` only validates: the kernel's batch (32 live Gaussians per MMA) does not change the
+    output, which the reference requires of every batch width (tests/test_tensor_path.py:155-165).
+    """
+    own = spec in _SPECS
+    if coords is None:
+        coords = "local" if own else "global"
+    if coords not in ("global", "local"):
+        raise ValueError(f"unknown coordinate mode {coords!r}")
+    if batch_width < 1:
+        raise ValueError("batch width must be positive")
+    if spec == "reference":
+        return Backend("reference", _abi.ALPHA_FFMA, False, "local", "fp32")
+    if spec == "frag2mat":
+        return Backend(f"frag2mat-exact-{coords}", _abi.ALPHA_FFMA, bool(use_early_cull), "local", "fp32")
+    if spec == "frag2mat-fp16":
+        mode = _abi.ALPHA_TC_K8 if coords == "local" else _abi.ALPHA_TC_K8_GLOBAL
+        return Backend(f"frag2mat-fp16-{coords}", mode, bool(use_early_cull), coords, "fp16")
+    if spec == "frag2mat-tf32":
+        raise ValueError("backend 'frag2mat-tf32': the B200 kernel does not reproduce the tf32 arithmetic model "
+                         "(use 'frag2mat' for exact or 'frag2mat-fp16' for the paper's fp16 path)")
     if spec not in _SPECS:
         raise ValueError(f"unknown backend {spec!r}")
     if coords != "local":
-        raise ValueError(f"coordinate mode {coords!r}: the B200 kernel evaluates in tile-local coordinates only")
-    if batch_width < 1:
-        raise ValueError("batch width must be positive")
-    mode, early = _SPECS[spec]
-    return Backend(spec, mode, early and use_early_cull)
+        raise ValueError(f"backend {spec!r} evaluates in tile-local coordinates only (global coordinates: "
+                         "'frag2mat-fp16' with coords='global')")
+    mode, arith = _SPECS[spec]
+    return Backend(spec, mode, bool(use_early_cull), "local", arith)
 
 
 def computation_model(stats: FragmentStats, k_alpha: float, k_cull: float, k_blend: float) -> float:
@@ -259,9 +298,14 @@ class Renderer:
         self.ws = None
         self.ws_key = None
         self._out = {}
+        self._timing = False  # render_frame: the library times the stages (tcgs_opts.timing)
+        self._dump = None     # (beta, class) device tensors: the K7 debug dump (dump_frame / blend_lists)
 
     def _opts(self, band=None, debug=False, defer_colour=False) -> _abi.Opts:
         o = _abi.Opts()
+        o.timing = 1 if self._timing else 0
+        if self._dump is not None:
+            o.dump_beta, o.dump_class = self._dump[0].data_ptr(), self._dump[1].data_ptr()
         o.defer_colour = 1 if defer_colour else 0
         o.tile_row_begin, o.tile_row_end = (band if band is not None else (0, 0))
         o.alpha_mode = self.backend.alpha_mode
@@ -343,6 +387,9 @@ class Renderer:
         fs = FragmentStats(f_blend=st_.f_blend, f_cull=st_.f_cull, f_skip=st_.f_skip, exp_calls=st_.exp_calls,
                            n_splats=st_.n_splats, dropped=st_.dropped, pixels_terminated=st_.pixels_terminated,
                            n_visible=st_.n_visible)
+        if o.timing:  # src/tilesplat/raster.py:196-200: exactly these three keys
+            fs.stage_ms = {"preprocess": float(st_.ms_preprocess), "sorting": float(st_.ms_sort),
+                           "blending": float(st_.ms_blend)}
         return rc, fs
 
     def finish(self, cloud: GaussianCloud, cam, band=None, with_stats=True, outputs=None) -> Frame:
@@ -360,20 +407,42 @@ class Renderer:
         raise RuntimeError("splat capacity could not be satisfied")
 
     def render_frame(self, cloud: GaussianCloud, cam, band=None, debug=False, timed=True) -> Frame:
+        """One frame, synchronously, with its FragmentStats (stage device times from the library when
+        ``timed``: tcgs_opts.timing -> tcgs_stats.ms_*)."""
         with torch.cuda.device(self.device):
-            for _attempt in range(3):
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timed else None
-                rgb, T, cnt = self.launch(cloud, cam, band, debug, timers=ev)
-                rc, fs = self.read_stats(cloud.P, band)
-                if rc == _abi.TCGS_ERR_CAPACITY:
-                    self.max_splats = int(fs.n_splats * 1.25) + 1024
-                    continue
-                _abi.check(rc, "tcgs_read_stats")
-                if ev:
-                    fs.stage_ms = {"preprocess": ev[0].elapsed_time(ev[1]), "sorting": ev[1].elapsed_time(ev[2]),
-                                   "blending": ev[2].elapsed_time(ev[3])}
-                return Frame(rgb, T, cnt, fs)
+            self._timing = bool(timed)
+            try:
+                for _attempt in range(3):
+                    rgb, T, cnt = self.launch(cloud, cam, band, debug)
+                    rc, fs = self.read_stats(cloud.P, band)
+                    if rc == _abi.TCGS_ERR_CAPACITY:
+                        self.max_splats = int(fs.n_splats * 1.25) + 1024
+                        continue
+                    _abi.check(rc, "tcgs_read_stats")
+                    return Frame(rgb, T, cnt, fs)
+            finally:
+                self._timing = False
         raise RuntimeError("splat capacity could not be satisfied")
+
+    def dump_frame(self, cloud: GaussianCloud, cam, band=None, host: bool = True):
+        """Debug: render one frame with K7's beta/classification dump (the a19 tolerance oracle).
+
+        Returns (Frame, beta float32 [N,256], cls uint8 [N,256]) as numpy: for tile-list entry e (the order of
+        ``tile_lists``) and tile pixel i = 16 row + col, beta = K7's exponent in log2 units and cls = 1 cull /
+        2 blend / 3 terminate / 4 dead on the whole tile (box test) / 0 not evaluated (NaN beta)."""
+        f = self.render_frame(cloud, cam, band, timed=False)  # sizes the workspace and learns N
+        n = max(int(f.stats.n_splats), 1)
+        beta = torch.full((n, 256), float("nan"), dtype=torch.float32, device=self.device)
+        cls = torch.zeros((n, 256), dtype=torch.uint8, device=self.device)
+        self._dump = (beta, cls)
+        try:
+            f = self.render_frame(cloud, cam, band, timed=False)
+        finally:
+            self._dump = None
+        n = int(f.stats.n_splats)
+        if not host:  # device tensors (full-size frames: the caller fetches the rows it needs)
+            return f, beta[:n], cls[:n]
+        return f, beta[:n].cpu().numpy(), cls[:n].cpu().numpy()
 
     # -- debug accessors (tests) ------------------------------------------------------------
     def tile_lists(self, P: int, cam, band=None):
@@ -416,8 +485,9 @@ class Renderer:
         return {k: v[:P].cpu().numpy() for k, v in
                 dict(visible=vis, mean2d=m2, inv_cov=con, depth=dep, radius=rad, rgb=rgb).items()}
 
-    def blend_lists(self, mean2d, conic, opacity, colors, offsets, ids, cam, band=None):
-        """K7 alone on caller-given projected records and CSR tile lists (tests/KATs)."""
+    def blend_lists(self, mean2d, conic, opacity, colors, offsets, ids, cam, band=None, dump=False):
+        """K7 alone on caller-given projected records and CSR tile lists (tests/KATs).  ``dump``: also return
+        K7's beta / classification per (list entry, tile pixel), as ``dump_frame`` does."""
         d = self.device
         c = camera_struct(cam)
         P = int(np.asarray(mean2d).reshape(-1, 2).shape[0])
@@ -435,7 +505,12 @@ class Renderer:
         rgb = torch.zeros((c.height, c.width, 3), dtype=torch.float32, device=d)
         T = torch.ones((c.height, c.width), dtype=torch.float32, device=d)
         cnt = torch.zeros((c.height, c.width), dtype=torch.int32, device=d)
+        n = max(int(np.size(ids)), 1)
+        if dump:
+            self._dump = (torch.full((n, 256), float("nan"), dtype=torch.float32, device=d),
+                          torch.zeros((n, 256), dtype=torch.uint8, device=d))
         o = self._opts(band)
+        dumped, self._dump = self._dump, None
         st = torch.cuda.current_stream(d).cuda_stream
         with torch.cuda.device(d):
             _abi.check(self.lib.tcgs_blend_lists(P, m2.data_ptr(), con.data_ptr(), op.data_ptr(), col.data_ptr(),
@@ -443,6 +518,9 @@ class Renderer:
                                                  rgb.data_ptr(), T.data_ptr(), cnt.data_ptr(), st), "tcgs_blend_lists")
             rc, fs = self.read_stats(P, band)
             _abi.check(rc, "tcgs_read_stats")
+        if dump:
+            m = int(np.size(ids))
+            return Frame(rgb, T, cnt, fs), dumped[0][:m].cpu().numpy(), dumped[1][:m].cpu().numpy()
         return Frame(rgb, T, cnt, fs)
 
 
@@ -535,29 +613,31 @@ _DEFAULT = {}
 
 
 def _renderer(device, backend) -> Renderer:
-    key = (str(device), backend.name if isinstance(backend, Backend) else backend)
+    key = (str(device), backend if isinstance(backend, Backend) else make_backend(backend))
     if key not in _DEFAULT:
         _DEFAULT[key] = Renderer(device, backend)
     return _DEFAULT[key]
 
 
-def render(scene, cam, backend="tcgs", device=None) -> tuple[ImageBuffer, FragmentStats]:
-    """Drop-in for ``tilesplat.render(scene, cam, backend)`` (src/tilesplat/raster.py:161-201).
+def render(scene, cam, backend="reference", device=None) -> tuple[ImageBuffer, FragmentStats]:
+    """Drop-in for ``tilesplat.render(scene, cam, backend="reference")`` (src/tilesplat/raster.py:161-201).
 
     ``scene`` is a reference ``Scene`` (or a ``GaussianCloud``); background is
     black; boundary tiles are full 16x16 tiles with out-of-image pixels masked.
-    Returns float64 RGB like the reference plus ``T``/``n_contrib`` extras.
+    The default backend is the reference's ("reference": alpha for every active
+    fragment, the cull on alpha afterwards); pass ``"tcgs"`` for the tensor-core
+    path with EarlyCull.  ``stats.stage_ms`` holds exactly the reference's keys
+    (preprocess / sorting / blending), as device times.  Returns float64 RGB
+    like the reference plus ``T``/``n_contrib`` extras.
     """
     if isinstance(backend, str):
         backend = make_backend(backend)
     device = torch.device(device or "cuda")
-    t0 = time.perf_counter()
     cloud = scene if isinstance(scene, GaussianCloud) else GaussianCloud.from_scene(scene, device)
     r = _renderer(device, backend)
     frame = r.render_frame(cloud, cam)
     img = ImageBuffer(frame.rgb.double().cpu().numpy(), frame.T.double().cpu().numpy(),
                       frame.n_contrib.cpu().numpy())
-    frame.stats.stage_ms["total_wall"] = (time.perf_counter() - t0) * 1e3
     return img, frame.stats
 
 

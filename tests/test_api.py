@@ -15,25 +15,49 @@ def test_constants_match_reference():  # src/tilesplat/raster.py:15-16, tiling.p
     assert tcgs.TILE_SIZE == 16
 
 
-@pytest.mark.parametrize("spec,mode,early", [
-    ("tcgs", _abi.ALPHA_TC_HILO, True), ("frag2mat", _abi.ALPHA_TC_HILO, True),
-    ("frag2mat-fp16", _abi.ALPHA_TC_K8, True), ("frag2mat-tf32", _abi.ALPHA_TC_HILO, True),
-    ("tcgs-ffma", _abi.ALPHA_FFMA, True), ("reference", _abi.ALPHA_FFMA, False)])
-def test_backend_specs(spec, mode, early):
+@pytest.mark.parametrize("spec,mode,early,name", [
+    ("tcgs", _abi.ALPHA_TC_HILO, True, "tcgs"), ("tcgs-fp16", _abi.ALPHA_TC_K8, True, "tcgs-fp16"),
+    ("tcgs-ffma", _abi.ALPHA_FFMA, True, "tcgs-ffma"),
+    # the reference's spellings keep its default coords="global" (src/tilesplat/raster.py:149)
+    ("frag2mat", _abi.ALPHA_FFMA, True, "frag2mat-exact-global"),
+    ("frag2mat-fp16", _abi.ALPHA_TC_K8_GLOBAL, True, "frag2mat-fp16-global"),
+    ("reference", _abi.ALPHA_FFMA, False, "reference")])
+def test_backend_specs(spec, mode, early, name):
     b = make_backend(spec)
-    assert (b.name, b.alpha_mode, b.early_cull) == (spec, mode, early)
+    assert (b.name, b.alpha_mode, b.early_cull) == (name, mode, early)
+    # EarlyCull off is a different kernel (alpha for every active fragment), not only a different count;
+    # the reference backend has no EarlyCull at all
     assert make_backend(spec, use_early_cull=False).early_cull is False
 
 
-def test_backend_errors():  # reference tests/test_raster.py:165-167 ("splatzilla")
+def test_reference_spellings_and_coordinates():
+    # G2L for the paper's fp16 vector; exact arithmetic ignores coords (criterion 1: global == local to 1e-5)
+    assert make_backend("frag2mat-fp16", coords="local").alpha_mode == _abi.ALPHA_TC_K8
+    assert make_backend("frag2mat", coords="local").alpha_mode == _abi.ALPHA_FFMA
+    assert make_backend("reference", coords="global").alpha_mode == _abi.ALPHA_FFMA
+    assert make_backend("reference", coords="local", use_early_cull=True).early_cull is False
+    assert make_backend("frag2mat-fp16", coords="global").coords == "global"
+
+
+def test_backend_errors():  # reference tests/test_raster.py:165-167 ("splatzilla"), tensor_path.py:175-181
     with pytest.raises(ValueError):
         make_backend("splatzilla")
     with pytest.raises(ValueError):
-        make_backend("frag2mat", coords="global")
+        make_backend("frag2mat", coords="polar")
     with pytest.raises(ValueError):
         make_backend("frag2mat", batch_width=0)
+    with pytest.raises(ValueError):  # tf32 arithmetic is not reproduced: refused, not approximated
+        make_backend("frag2mat-tf32")
+    with pytest.raises(ValueError):  # this package's own specs are tile-local only
+        make_backend("tcgs", coords="global")
     with pytest.raises(NotImplementedError):
         make_backend("tcgs").tile_evaluator(0, 0, [])
+
+
+def test_render_defaults_to_the_reference_backend():
+    import inspect
+
+    assert inspect.signature(tcgs.render).parameters["backend"].default == "reference"
 
 
 def test_fragment_stats_contract():  # src/tilesplat/raster.py:19-49

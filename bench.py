@@ -3,18 +3,26 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
 
 One step = one full frame of the hot path (K1 preprocess -> K2-K6 binning ->
-K7 tensor-core alpha + blend) for the config-2 workload: 1M synthetic
-Gaussians with SH degree 3 at 1920x1080, inputs resident in HBM (the 236 MB
-scene exceeds the 126 MB L2, so no flush is needed between frames).  N > 1
-shards camera views across ranks (one process per GPU, no collective on the
-data path; weak scaling: every rank renders K frames).  ``--config c3``
-renders 4K frames split into tile-row bands across the ranks with one NCCL
-gather to rank 0 per frame (strong scaling).
+K7 tensor-core alpha + blend) of a new camera view of the config-2 workload:
+1M synthetic Gaussians with SH degree 3 at 1920x1080, inputs resident in HBM
+(the 236 MB scene exceeds the 126 MB L2, so no flush is needed between frames).
+
+* ``value`` is the single-camera frame rate: lone frames back to back on one
+  CUDA stream (the K7 dynamic tile queue), each frame fully re-projected,
+  re-binned and re-blended.  ``views_in_flight`` reports the multi-view
+  throughput (16 frames on 16 streams, one fused K1 per 8 views) separately.
+* N > 1 shards camera views across ranks (one process per GPU, no collective on
+  the data path; weak scaling: every rank renders K frames).  ``--gpus N``
+  without torchrun re-launches itself under ``torch.distributed.run``.
+  ``--config c3`` renders 4K frames split into tile-row bands across the ranks
+  (strong scaling; K7 writes into rank 0's frame over NVLink peer memory).
 
 The JSON line carries the device-timed throughput (`value`), the end-to-end
 throughput through the public API with host buffers (`e2e`), the roofline of
-the dominant kernel (K7), the CPU baseline (the oracle's C port of the
-reference renderer on this host's cores), clocks and the kernel-launch count.
+the dominant kernel (K7: issue-bound; tensor, MUFU and issue fractions side
+by side), the alpha-blend ablation (Frag2Mat x EarlyCull, the paper's table),
+the CPU baseline (the oracle's C port of the reference renderer on this
+host's cores, whole frames), clocks and the kernel-launch count.
 """
 
 from __future__ import annotations
@@ -56,6 +64,11 @@ def parse():
                          "view.  Two groups in flight: the next group's K1 overlaps this group's K2-K7")
     ap.add_argument("--band-output", default="peer", choices=["peer", "gather"],
                     help="c3 tile bands: K7 writes into rank 0's frame over peer memory, or one NCCL gather")
+    ap.add_argument("--no-ablation", action="store_true",
+                    help="skip the alpha-blend ablation (K7 per alpha mode x EarlyCull on/off)")
+    ap.add_argument("--no-in-flight", action="store_true", help="skip the views-in-flight throughput")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="CPU baseline leg: whole oracle frames until this much CPU time has been spent")
     return ap.parse_args()
 
 
@@ -215,17 +228,15 @@ def e2e_resident(vr, cloud, views, base, dev, world, dist):
             "d2h_bytes_per_step": base.width * base.height * 12 + nb, "steps": steps}
 
 
-def stage_rooflines(scene, P, st, stage_ms, peaks, cam, group=0):
+def stage_rooflines(scene, P, st, stage_ms, peaks, cam):
     """Algorithmic bytes per stage / isolated stage time, against the measured HBM copy peak.
     K1: P x (inputs + 76 B of outputs); binning: P (8 B depth + 4 B index) read + write, N (2 B tile key +
     4 B id) written and sorted once, N x 2 B of ranges; K7: N x 52 B (id + 48 B record) + 20 B per pixel.
-    The fused multi-view K1 reads the inputs once per group of views: P x (inputs / group + 76 B) per view."""
+    """
     feats = 3 * 4 * ((scene.get("sh_degree", 0) + 1) ** 2 if scene.get("sh_degree", 0) > 0 else 1)
     N = st.n_splats
     work = {"preprocess": P * (44 + feats + 76), "binning": P * 12 * 2 + N * 6 * 2 + N * 2,
             "blend": N * 52 + cam.width * cam.height * 20}
-    if group > 1:
-        work["preprocess_fused_per_view"] = P * ((44 + feats) / group + 76)
     out = {}
     for k, b in work.items():
         ms = stage_ms.get(k) if isinstance(stage_ms, dict) else None
@@ -239,24 +250,29 @@ def stage_rooflines(scene, P, st, stage_ms, peaks, cam, group=0):
 
 def issue_roofline(traffic, blend_ms, clocks):
     """K7's binding resource: warp-instruction issue (4 per clock per SM).  Instructions per launch come from
-    the committed ncu capture (smsp__inst_executed.sum), the duration from this run's CUDA events."""
+    the committed ncu capture of the same build and workload (smsp__inst_executed.sum), the duration from this
+    run's CUDA events, the clock from the NVML samples of this run's timed region."""
     inst = (traffic or {}).get("warp_inst_per_launch")
     mhz = (clocks or {}).get("sm_mhz") or 1965.0
     if not inst:
         return None
     peak = 4 * 148 * mhz * 1e6
     ach = inst / (blend_ms * 1e-3)
-    return {"achieved_warp_inst_per_s": ach, "peak_warp_inst_per_s": peak, "frac": ach / peak,
-            "warp_inst_per_launch": inst, "note": "instructions from the committed ncu profile; clock = median "
-                                                  "SM clock sampled during the timed region"}
+    return {"achieved": ach, "peak": peak, "unit": "warp-instructions/s", "frac": ach / peak,
+            "warp_inst_per_launch": inst, "source": traffic.get("source"),
+            "note": "instructions from the committed ncu profile; clock = median SM clock sampled during the timed "
+                    "region"}
 
 
-def profile_traffic():
-    """K7 DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the newest committed
-    ncu --set full summary under profiles/ (scripts/ncu_summary.py), if present."""
+def profile_traffic(config="c2"):
+    """K7 DRAM bytes and warp instructions per launch (dram__bytes_read.sum + dram__bytes_write.sum,
+    smsp__inst_executed.sum) from the newest committed ncu --set full summary under profiles/
+    (scripts/ncu_summary.py).  Those captures are of the C2 workload; other configs get None."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_k7_ncu.json")))  # r1_ < r1e_ < r1j_ < ...
+    if config != "c2":
+        return None
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_k7_ncu.json")))  # r1_ < ... < r2a_ < r2b_
     for p in reversed(files):
         with open(p) as f:
             rows = [e for e in json.load(f) if "render_kernel" in e.get("kernel", "")]
@@ -270,9 +286,9 @@ def profile_traffic():
 
 # ------------------------------------------------------------------------------------------ CPU side
 
-def cpu_reference_frame(scene, cam, rows):
-    """The oracle's C port of the reference renderer (project, build_tiles, blend) on host cores.
-    Blend runs on a band of `rows` tile rows and is extrapolated to the frame."""
+def cpu_reference_frame(scene, cam):
+    """One WHOLE frame of the oracle's C port of the reference renderer (tilesplat.render 'reference',
+    src/tilesplat/raster.py:161-201: project, build_tiles, blend every tile) on the host cores (OpenMP)."""
     import oracle
 
     t0 = time.perf_counter()
@@ -283,14 +299,20 @@ def cpu_reference_frame(scene, cam, rows):
     t1 = time.perf_counter()
     off, ids = oracle.build_tiles(proj, cam)
     t2 = time.perf_counter()
-    tiles_y = (cam.height + 15) // 16
-    r0 = max(0, tiles_y // 2 - rows // 2)
-    r1 = min(tiles_y, r0 + rows)
-    oracle.blend(proj, off, ids, scene["opacities"], colors, cam, band=(r0, r1))
+    oracle.blend(proj, off, ids, scene["opacities"], colors, cam)
     t3 = time.perf_counter()
-    frame_s = (t1 - t0) + (t2 - t1) + (t3 - t2) * tiles_y / (r1 - r0)
-    return frame_s, {"preprocess_s": t1 - t0, "sort_s": t2 - t1, "blend_band_s": t3 - t2,
-                     "band_rows": r1 - r0, "tile_rows": tiles_y}
+    return t3 - t0, {"preprocess_s": t1 - t0, "sort_s": t2 - t1, "blend_s": t3 - t2}
+
+
+def cpu_frames(scene, cam, budget_s, max_frames=20):
+    """Whole oracle frames until ``budget_s`` seconds have been spent (at least one)."""
+    times, det = [], None
+    spent = 0.0
+    while not times or (spent < budget_s and len(times) < max_frames):
+        s_, det = cpu_reference_frame(scene, cam)
+        times.append(s_)
+        spent += s_
+    return times, det
 
 
 def bench_config(args, scene, cam, world):
@@ -315,6 +337,8 @@ def cpu_threads():
 
 
 def run_reference(args):
+    """The reference arm: the oracle's C port of tilesplat.render 'reference' (float64), WHOLE frames on all of
+    this host's cores; rank 0 only (the other ranks of a torchrun launch exit without work)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -323,26 +347,25 @@ def run_reference(args):
     os.environ.setdefault("OMP_NUM_THREADS", str(cpu_threads()))
     scene, cams = synthetic.config_scene(args.config, args.scale)
     cam = cams[0]
-    rows = 2
     for _ in range(max(args.warmup, 0)):
-        cpu_reference_frame(scene, cam, rows)
+        cpu_reference_frame(scene, cam)
     times = []
     detail = None
     for _ in range(args.steps):
-        s, detail = cpu_reference_frame(scene, cam, rows)
-        times.append(s)
+        s_, detail = cpu_reference_frame(scene, cam)
+        times.append(s_)
     mean_s = sum(times) / len(times)
     fps = 1.0 / mean_s
+    n = max(world, args.gpus)
     line = {
-        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": n,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
         "scaling": "strong" if args.config == "c3" else "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": bench_config(args, scene, cam, world),
+        "data": "synthetic", "config": bench_config(args, scene, cam, n),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
                          "kind": "port",
-                         "sample": f"oracle C port (float64 restatement of tilesplat.render 'reference'): full "
-                                   f"project + build_tiles, blend on {detail['band_rows']} of {detail['tile_rows']} "
-                                   f"tile rows extrapolated to the frame"},
+                         "sample": "oracle C port (float64 restatement of tilesplat.render 'reference'): whole "
+                                   "frames (project + build_tiles + blend of every tile), one camera"},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "detail": detail,
     }
@@ -351,12 +374,54 @@ def run_reference(args):
 
 # ------------------------------------------------------------------------------------------ GPU side
 
+def blend_ablation(tcgs, cloud, cam, dev, reps=10):
+    """The paper's alpha-blend ablation on B200: K7 alone, re-run on one binned
+    frame, for every alpha mode (Frag2Mat on tcgen05: hi/lo and the paper's K8 vector; off: the FFMA quadratic
+    form) x EarlyCull on/off.  Device ms per launch (CUDA events on the launching stream) + fragment counts."""
+    import torch
+
+    out = {}
+    for spec in ("tcgs", "tcgs-fp16", "tcgs-ffma"):
+        for ec in (True, False):
+            r = tcgs.Renderer(dev, tcgs.make_backend(spec, use_early_cull=ec), schedule="dynamic")
+            f = r.render_frame(cloud, cam, timed=False)
+            c = tcgs.camera_struct(cam)
+            o = r._opts()
+            rgb, T, cnt = r.outputs(c.width, c.height)
+            st = torch.cuda.current_stream(dev).cuda_stream
+
+            def k7():
+                rc = r.lib.tcgs_blend(cloud.P, c, o, r.ws.data_ptr(), r.ws.numel(), r.max_splats, rgb.data_ptr(),
+                                      T.data_ptr(), cnt.data_ptr(), st)
+                if rc:
+                    raise RuntimeError(f"tcgs_blend rc={rc}")
+
+            for _ in range(2):
+                k7()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            e0.record()
+            for _ in range(reps):
+                k7()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            s_ = f.stats
+            out[f"{spec}/earlycull_{'on' if ec else 'off'}"] = {
+                "blend_ms": e0.elapsed_time(e1) / reps, "f_blend": s_.f_blend, "f_cull": s_.f_cull,
+                "exp_calls": s_.exp_calls, "pixels_terminated": s_.pixels_terminated}
+            del r
+    base = out["tcgs-ffma/earlycull_off"]["blend_ms"]
+    for v in out.values():
+        v["speedup_vs_ffma_no_earlycull"] = base / v["blend_ms"]
+    return out
+
+
 def run_tcgs(args):
     import torch
     import torch.distributed as dist
 
     import paper_2505_24796_b200 as tcgs
-    from paper_2505_24796_b200 import _abi, shard, synthetic
+    from paper_2505_24796_b200 import shard, synthetic
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -377,42 +442,30 @@ def run_tcgs(args):
         my_views = [mine[k % len(mine)] for k in range(per_rank)]
 
     cloud = tcgs.GaussianCloud.from_arrays(scene, dev)
+    stream = torch.cuda.current_stream(dev)
     if bands_mode:
         if world == 1 and not dist.is_initialized():
             dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % (29500 + os.getpid() % 1000),
                                     rank=0, world_size=1)
         br = shard.BandRenderer(dev, args.backend, output=args.band_output if world > 1 else "gather")
         r = br.r
-        first = br.render(cloud, base, with_stats=True)  # sizes the workspace
-        st0 = first.stats
-    else:
-        vr = tcgs.ViewRenderer(dev, args.backend, max(1, args.streams), coverage=args.coverage)
-        r = vr.renderers[0]
-        st0 = vr.warm(cloud, base)  # sizes the workspaces; stats of the base view
-    stream = torch.cuda.current_stream(dev)
+        st0 = br.render(cloud, base, with_stats=True).stats  # sizes the workspace
 
-    group = 0 if bands_mode else max(0, min(args.view_group, max(1, args.streams), 8))
-
-    def frame(cam, ev=None):
-        if bands_mode:
+        def frame(cam, ev=None):
             return br.render(cloud, cam, with_stats=False, timers=ev)
-        return vr.launch(cloud, cam, timers=ev)
+    else:
+        # the single-camera path: one renderer, one stream, frames back to back (K7's dynamic tile queue)
+        r = tcgs.Renderer(dev, args.backend, coverage=args.coverage, schedule="dynamic")
+        st0 = r.render_frame(cloud, base, timed=False).stats  # sizes the workspace
 
-    def frames(k0, n, ev=None):  # frames k0 .. k0+n-1 of my_views: one at a time, or in fused-K1 groups
-        if not group:
-            for k in range(k0, k0 + n):
-                frame(my_views[k], ev[k - k0] if ev else None)
-            return
-        for g0 in range(k0, k0 + n, group):
-            g1 = min(g0 + group, k0 + n)
-            vr.launch_group(cloud, my_views[g0:g1], timers=ev[g0 - k0] if ev else None)
+        def frame(cam, ev=None):
+            return r.launch(cloud, cam, timers=ev)
 
-    frames(0, args.warmup)
-    if not bands_mode:
-        vr.join()
+    for k in range(args.warmup):
+        frame(my_views[k])
     torch.cuda.synchronize(dev)
 
-    # ---- timed region: K frames, inputs resident in HBM
+    # ---- timed region: K lone frames, inputs resident in HBM
     nev = 5 if bands_mode else 4
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nev)] for _ in range(args.steps)]
     start = torch.cuda.Event(enable_timing=True)
@@ -423,21 +476,15 @@ def run_tcgs(args):
     launches0 = r.lib.tcgs_launch_count()
     with ClockSampler(local) as clk:
         start.record(stream)
-        frames(args.warmup, args.steps, evs)
-        if not bands_mode:
-            vr.join()
+        for k in range(args.steps):
+            frame(my_views[args.warmup + k], evs[k])
         stop.record(stream)
         torch.cuda.synchronize(dev)
     launches = r.lib.tcgs_launch_count() - launches0
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(stop)
-    if group:  # one event set per group (recorded on its first frame): fused K1 per view, last view's K2-K7
-        evs = [evs[k] for k in range(0, args.steps, group)]
-        sizes = [min(group, args.steps - k) for k in range(0, args.steps, group)]
-        pre_ms = [e[0].elapsed_time(e[1]) / n for e, n in zip(evs, sizes)]
-    else:
-        pre_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    pre_ms = [e[0].elapsed_time(e[1]) for e in evs]
     bin_ms = [e[1].elapsed_time(e[2]) for e in evs]
     blend_ms = [e[2].elapsed_time(e[3]) for e in evs]
     gather_ms = [e[3].elapsed_time(e[4]) for e in evs] if bands_mode else None
@@ -445,31 +492,48 @@ def run_tcgs(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, blend_max = float(t[0].item()), float(t[1].item())
-
-    # per-frame stats of this rank's last timed view (device counters; the band's in bands mode)
-    # isolated per-stage device times (one view at a time on one stream): with several views in flight the
-    # timed region overlaps stages of different views, so its per-stage events include interference
-    iso = None
-    if not bands_mode and len(vr.renderers) > 1:
-        r0 = vr.renderers[0]
-        iso_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(min(10, args.steps))]
-        for k, ev in enumerate(iso_ev):
-            r0.launch(cloud, my_views[args.warmup + k], timers=ev)
-        torch.cuda.synchronize(dev)
-        iso = {"preprocess": sum(e[0].elapsed_time(e[1]) for e in iso_ev) / len(iso_ev),
-               "binning": sum(e[1].elapsed_time(e[2]) for e in iso_ev) / len(iso_ev),
-               "blend": sum(e[2].elapsed_time(e[3]) for e in iso_ev) / len(iso_ev)}
-        if group > 1:  # the fused K1 alone: one pass over the scene for `group` views, per view
-            gev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-            vr.launch_group(cloud, my_views[args.warmup:args.warmup + group], timers=gev)
-            vr.join()
-            torch.cuda.synchronize(dev)
-            iso["preprocess_fused_per_view"] = gev[0].elapsed_time(gev[1]) / group
     if bands_mode:
         st_last = br.render(cloud, my_views[-1], with_stats=True).local.stats
     else:
-        last = vr.renderers[(args.warmup + args.steps - 1 + len(vr.renderers)) % len(vr.renderers)]
-        rc, st_last = last.read_stats(cloud.P)
+        rc, st_last = r.read_stats(cloud.P)
+
+    # ---- views in flight: many cameras at once (16 streams, one fused K1 per group of 8 views)
+    inflight = None
+    vr = None
+    if not bands_mode and not args.no_in_flight:
+        vr = tcgs.ViewRenderer(dev, args.backend, max(1, args.streams), coverage=args.coverage)
+        vr.warm(cloud, base)
+        group = max(0, min(args.view_group, max(1, args.streams), 8))
+        n_if = max(args.steps, 2 * max(1, args.streams))
+        views_if = [my_views[k % len(my_views)] for k in range(n_if)]
+
+        def frames_if(lst):
+            if not group:
+                for cam in lst:
+                    vr.launch(cloud, cam)
+                return
+            for g0 in range(0, len(lst), group):
+                vr.launch_group(cloud, lst[g0:g0 + group])
+
+        frames_if(views_if[:2 * group or 2])
+        vr.join()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        frames_if(views_if)
+        vr.join()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ti = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ti, op=dist.ReduceOp.MAX)
+        inflight = {"value": world * n_if / (float(ti.item()) / 1e3), "unit": "frames/s", "frames_per_rank": n_if,
+                    "streams": max(1, args.streams), "view_group": group,
+                    "what": "independent cameras rendered concurrently: one workspace + CUDA stream per view in "
+                            "flight, one fused K1 pass per group of views (tcgs_preprocess_views), static K7 "
+                            "schedule; every frame fully re-projected, re-binned and re-blended"}
 
     # ---- end to end through the public API: host scene -> device, render, image -> host
     e2e = None
@@ -479,7 +543,7 @@ def run_tcgs(args):
                 for k in ("means", "scales", "rotations", "opacities", feats_key)}
         dev_bufs = {k: torch.empty_like(v, device=dev) for k, v in host.items()}
         out_host = torch.empty((base.height, base.width, 3), dtype=torch.float32).pin_memory()
-        stats_bytes = 9 * 8
+        stats_bytes = int(r.lib.tcgs_counters_bytes())
         h2d = sum(v.numel() * v.element_size() for v in host.values())
         d2h = (out_host.numel() * 4 if (rank == 0 or not bands_mode) else 0) + stats_bytes
         e2e_steps = max(3, min(args.steps, 20))
@@ -541,8 +605,12 @@ def run_tcgs(args):
         per_rank_fps = e2e["value"] / (1 if bands_mode else world)
         e2e["h2d_achieved_GBps"] = h2d * per_rank_fps / 1e9
         e2e["h2d_link_GBps"] = pinned_h2d_GBps(host, dev)
-        if not bands_mode:
+        if vr is not None:
             e2e["resident_scene"] = e2e_resident(vr, cloud, my_views, base, dev, world, dist)
+
+    ablation = None
+    if world == 1 and not bands_mode and not args.no_ablation:
+        ablation = blend_ablation(tcgs, cloud, base, dev)
 
     if bands_mode:
         br.close()  # unmaps / frees the peer frame (collective)
@@ -553,33 +621,46 @@ def run_tcgs(args):
 
     frames = args.steps if bands_mode else world * args.steps
     value = frames / (ms_max / 1e3)
-    blend_avg = iso["blend"] if iso else sum(blend_ms) / len(blend_ms)
+    blend_avg = sum(blend_ms) / len(blend_ms)
     peaks, peak_kind = measured_peaks()
-    traffic = profile_traffic()
+    traffic = profile_traffic(args.config)
+    clocks = clk.summary()
     # K7 algorithmic work: F_alpha = f_blend + f_cull + pixels_terminated fragments, 16 flops each
     # (length-8 dot = 2*8 flops, src/tilesplat/tensor_path.py:40,53); ex2 = f_blend + terminated.
     F_alpha = st_last.f_blend + st_last.f_cull + st_last.pixels_terminated
     tc_tflops = 16.0 * F_alpha / (blend_avg * 1e-3) / 1e12
     ex2_rate = (st_last.f_blend + st_last.pixels_terminated) / (blend_avg * 1e-3)
-    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
     ex2_peak = 148 * 16 * sm_mhz * 1e6  # MUFU: 16 ex2/clk/SM (nominal)
-    clocks = clk.summary()
+    issue = issue_roofline(traffic, blend_avg, clocks)
+    tensor = {"achieved": tc_tflops, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+              "frac": tc_tflops / peaks["bf16_tflops"], "peak_kind": peak_kind,
+              "work": "16 flops x F_alpha (F_alpha = f_blend + f_cull + pixels_terminated)"}
+    mufu = {"achieved": ex2_rate, "peak": ex2_peak, "unit": "ex2/s", "frac": ex2_rate / ex2_peak,
+            "peak_kind": "nominal 16/clk/SM at the sampled SM clock", "work": "f_blend + pixels_terminated ex2"}
+    if issue:
+        roof = {"kernel": "K7 render_kernel (alpha + blend)", "bound": "issue", "achieved": issue["achieved"],
+                "peak": issue["peak"], "unit": "warp-instructions/s", "frac": issue["frac"],
+                "traffic": (traffic or {}).get("bytes_per_launch"), "traffic_source": (traffic or {}).get("source"),
+                "issue": issue, "tensor": tensor, "mufu": mufu}
+    else:  # no committed instruction count for this workload: the tensor-pipe fraction, labelled as such
+        roof = {"kernel": "K7 render_kernel (alpha + blend)", "bound": "tensor", "achieved": tc_tflops,
+                "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": tc_tflops / peaks["bf16_tflops"],
+                "traffic": None, "note": "K7 is issue-bound; no committed ncu instruction count for this config",
+                "tensor": tensor, "mufu": mufu}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         threads = cpu_threads()
         os.environ["OMP_NUM_THREADS"] = str(threads)
-        s, det = cpu_reference_frame(scene, base, rows=2)
-        cpu = {"value": 1.0 / s, "unit": "frames/s", "cores": threads, "kind": "port",
-               "sample": f"oracle C port of tilesplat.render 'reference' (float64, OpenMP over tiles), view 0: full "
-                         f"project + build_tiles, blend on {det['band_rows']}/{det['tile_rows']} tile rows "
-                         f"extrapolated to the frame",
-               "detail": det}
-    stage = {"preprocess": sum(pre_ms) / len(pre_ms), "binning": sum(bin_ms) / len(bin_ms),
-             "blend": sum(blend_ms) / len(blend_ms)}
+        times, det = cpu_frames(scene, base, args.cpu_seconds)
+        mean_s = sum(times) / len(times)
+        cpu = {"value": 1.0 / mean_s, "unit": "frames/s", "cores": threads, "kind": "port",
+               "sample": f"oracle C port of tilesplat.render 'reference' (float64, OpenMP over tiles): "
+                         f"{len(times)} whole frame(s) of view 0 (project + build_tiles + blend of every tile)",
+               "detail": {**det, "frames": len(times)}}
+    stage = {"preprocess": sum(pre_ms) / len(pre_ms), "binning": sum(bin_ms) / len(bin_ms), "blend": blend_avg}
     if gather_ms:
         stage["gather"] = sum(gather_ms) / len(gather_ms)
-    if iso:
-        stage = {"isolated": iso, "in_flight": stage}
     line = {
         "metric": METRIC,
         "value": value,
@@ -595,24 +676,18 @@ def run_tcgs(args):
         "data": "synthetic (SURVEY.md Appendix B generators; random scene, no dataset)",
         "config": bench_config(args, scene, base, world),
         "backend": args.backend,
-        "views_in_flight": 1 if bands_mode else max(1, args.streams),
-        "view_group": group,
+        "what": ("one 4K frame at a time, tile-row bands across the ranks" if bands_mode else
+                 "single-camera frames back to back on one stream (a new view each frame)"),
         "coverage": args.coverage,
         "band_output": (args.band_output if world > 1 else "local") if bands_mode else None,
         "alpha_blend_ms": blend_avg,
-        "stage_rooflines": stage_rooflines(scene, cloud.P, st_last, iso or stage, peaks, base, group),
         "alpha_blend_ms_max_over_ranks": blend_max,
         "stage_ms": stage,
+        "stage_rooflines": stage_rooflines(scene, cloud.P, st_last, stage, peaks, base),
         "frame_stats": {**st_last.to_dict(), "n_visible": st_last.n_visible},
-        "roofline": {"kernel": "K7 render_kernel (alpha + blend)", "bound": "tensor", "achieved": tc_tflops,
-                     "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": tc_tflops / peaks["bf16_tflops"],
-                     "traffic": (traffic or {}).get("bytes_per_launch") if args.config == "c2" else None,
-                     "traffic_source": (traffic or {}).get("source"), "peak_kind": peak_kind,
-                     "work": "16 flops x F_alpha (F_alpha = f_blend + f_cull + pixels_terminated)",
-                     "mufu": {"achieved_ex2_per_s": ex2_rate, "peak_ex2_per_s": ex2_peak,
-                              "frac": ex2_rate / ex2_peak, "peak_kind": "nominal 16/clk/SM"},
-                     # the committed K7 profile is of the C2 workload: its instruction count only applies there
-                     "issue": issue_roofline(traffic, blend_avg, clocks) if args.config == "c2" else None},
+        "roofline": roof,
+        "views_in_flight": inflight,
+        "alpha_blend_ablation": ablation,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -623,12 +698,32 @@ def run_tcgs(args):
         dist.destroy_process_group()
 
 
+def relaunch_under_torchrun(args) -> int:
+    """``--gpus N`` (N > 1) outside torchrun: start N ranks of this script, one per GPU."""
+    import socket
+    import subprocess
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    _, world, _ = dist_env()
+    launched = "WORLD_SIZE" in os.environ
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_tcgs(args)
+        return
+    if args.gpus > 1 and not launched:
+        sys.exit(relaunch_under_torchrun(args))
+    if launched and world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+        sys.exit(2)
+    run_tcgs(args)
 
 
 if __name__ == "__main__":

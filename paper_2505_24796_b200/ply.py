@@ -2,7 +2,8 @@
 
 The reference reads binary little-endian PLY in the 3DGS layout, keeping only
 the SH DC term (``tilesplat.scene.load_ply``, src/tilesplat/scene.py:141-212).
-This loader uses the same header parsing, activations and error behaviour:
+This loader keeps the reference's activations, exception types and messages; its header parser is its own
+(a statement regex grouped by element):
 
 * opacity = sigmoid(stored);
 * scale = exp(stored);
@@ -21,6 +22,8 @@ through pinned host memory with non-blocking copies.
 """
 
 from __future__ import annotations
+
+import re
 
 import numpy as np
 import torch
@@ -48,6 +51,53 @@ _TYPES = {  # src/tilesplat/scene.py:125-138
 _REST_COUNT_TO_DEGREE = {0: 0, 9: 1, 24: 2, 45: 3}
 
 
+_HEADER_END = re.compile(rb"^end_header\r?\n", re.M)
+# one header statement per line: a keyword and its arguments (PLY 1.0 header grammar)
+_STATEMENT = re.compile(r"^\s*(format|element|property|comment|obj_info)\b\s*(.*?)\s*$", re.M)
+
+
+def _split_header(path: str, data: bytes) -> tuple[str, bytes]:
+    """(header text, body bytes); SceneFormatError unless the file starts with the PLY magic and has an end."""
+    m = _HEADER_END.search(data)
+    if not data.startswith(b"ply") or m is None:
+        raise SceneFormatError(f"{path}: not a PLY file")
+    return data[: m.start()].decode("ascii", errors="replace"), data[m.end():]
+
+
+def _vertex_layout(path: str, head: str) -> tuple[int, list[tuple[str, str]]]:
+    """Vertex count and the vertex element's (name, numpy type) fields, with the reference's checks
+    (src/tilesplat/scene.py:148-193: binary little-endian, scalar properties of known types, the 3DGS fields)."""
+    stmts = [(m.group(1), m.group(2).split()) for m in _STATEMENT.finditer(head)]
+    formats = [a for k, a in stmts if k == "format"]
+    if not formats or not formats[-1] or formats[-1][0] != "binary_little_endian":
+        raise SceneFormatError(f"{path}: expected binary_little_endian format")
+    # group property statements under the element statement that precedes them
+    elements: dict[str, tuple[int, list[list[str]]]] = {}
+    current = None
+    for kind, args in stmts:
+        if kind == "element":
+            current = args[0] if args else ""
+            elements[current] = (int(args[1]) if len(args) > 1 else 0, [])
+        elif kind == "property" and current is not None:
+            elements[current][1].append(args)
+    if "vertex" not in elements:
+        raise SceneFormatError(f"{path}: no vertex element")
+    count, props = elements["vertex"]
+    if count == 0:
+        raise SceneValidationError(f"{path}: scene contains zero vertices")
+    fields = []
+    for args in props:
+        if args and args[0] == "list":
+            raise SceneFormatError(f"{path}: list properties unsupported")
+        if not args or args[0] not in _TYPES:
+            raise SceneFormatError(f"{path}: unsupported property type {args[0] if args else ''}")
+        fields.append((args[1], _TYPES[args[0]]))
+    missing = [p for p in _REQUIRED if p not in {n for n, _ in fields}]
+    if missing:
+        raise SceneFormatError(f"{path}: missing vertex property '{missing[0]}'")
+    return count, fields
+
+
 def read_ply(path: str) -> dict:
     """Parse a 3DGS PLY into SoA float64 arrays (reference activations) plus SH features.
 
@@ -57,43 +107,10 @@ def read_ply(path: str) -> dict:
     """
     with open(path, "rb") as fh:
         data = fh.read()
-    end_tag = b"end_header\n"
-    end = data.find(end_tag)
-    if not data.startswith(b"ply") or end < 0:
-        raise SceneFormatError(f"{path}: not a PLY file")
-    header = data[:end].decode("ascii", errors="replace").splitlines()
-    count = None
-    names: list[str] = []
-    fields: list[tuple[str, str]] = []
-    in_vertex = fmt_ok = False
-    for line in header:
-        tok = line.split()
-        if not tok:
-            continue
-        if tok[0] == "format":
-            fmt_ok = tok[1] == "binary_little_endian"
-        elif tok[0] == "element":
-            in_vertex = tok[1] == "vertex"
-            if in_vertex:
-                count = int(tok[2])
-        elif tok[0] == "property" and in_vertex:
-            if tok[1] == "list":
-                raise SceneFormatError(f"{path}: list properties unsupported")
-            if tok[1] not in _TYPES:
-                raise SceneFormatError(f"{path}: unsupported property type {tok[1]}")
-            names.append(tok[2])
-            fields.append((tok[2], _TYPES[tok[1]]))
-    if not fmt_ok:
-        raise SceneFormatError(f"{path}: expected binary_little_endian format")
-    if count is None:
-        raise SceneFormatError(f"{path}: no vertex element")
-    if count == 0:
-        raise SceneValidationError(f"{path}: scene contains zero vertices")
-    for prop in _REQUIRED:
-        if prop not in names:
-            raise SceneFormatError(f"{path}: missing vertex property '{prop}'")
+    head, body = _split_header(path, data)
+    count, fields = _vertex_layout(path, head)
+    names = [n for n, _ in fields]
     dt = np.dtype(fields)
-    body = data[end + len(end_tag):]
     if len(body) < count * dt.itemsize:
         raise SceneFormatError(f"{path}: truncated vertex data")
     v = np.frombuffer(body[: count * dt.itemsize], dtype=dt)

@@ -164,18 +164,26 @@ class _CudaArray:
 
 
 class PeerFrame:
-    """Rank 0's full-frame outputs (rgb [H,W,3] f32, T [H,W] f32, n_contrib [H,W] i32) in one allocation,
-    mapped into every rank of ``group`` with CUDA IPC (NVLink peer memory between GPUs of one box).
+    """Rank 0's full-frame outputs (rgb [H,W,3] f32, T [H,W] f32, n_contrib [H,W] i32), double-buffered in one
+    allocation, mapped into every rank of ``group`` with CUDA IPC (NVLink peer memory between GPUs of one box).
 
-    Every rank passes these tensors as K7's outputs: K7 stores the pixels of its tile-row band straight
+    Every rank passes a slot's tensors as K7's outputs: K7 stores the pixels of its tile-row band straight
     into rank 0's frame, tile by tile, so the band gather disappears.
+
+    Ordering.  Frame k uses slot k % 2.  Rank 0 may read frame k (for example an async D2H on its current
+    stream) until it enqueues frame k + 1's completion all-reduce; every other rank's K7 of frame k + 2 -- the
+    next writer of that slot -- is stream-ordered after that all-reduce.  So a frame returned to rank 0 stays
+    intact while rank 0 consumes it on its current stream (or synchronously) before rendering frame k + 2.
     """
+
+    SLOTS = 2
 
     def __init__(self, lib, W: int, H: int, device, group=None):
         self.lib, self.group = lib, group
         self.rank = dist.get_rank(group)
         n = W * H
-        self.nbytes = 20 * n  # 12 n (rgb) + 4 n (T) + 4 n (n_contrib)
+        self.slot_bytes = 20 * n  # 12 n (rgb) + 4 n (T) + 4 n (n_contrib)
+        self.nbytes = self.SLOTS * self.slot_bytes
         handle = None
         with torch.cuda.device(device):
             if self.rank == 0:
@@ -194,15 +202,23 @@ class PeerFrame:
                                              ctypes.byref(p)), "tcgs_ipc_open")
                 self.ptr = p.value
             dev = torch.device(device)
-            self.rgb = torch.as_tensor(_CudaArray(self.ptr, (H, W, 3), "<f4"), device=dev)
-            self.T = torch.as_tensor(_CudaArray(self.ptr + 12 * n, (H, W), "<f4"), device=dev)
-            self.n_contrib = torch.as_tensor(_CudaArray(self.ptr + 16 * n, (H, W), "<i4"), device=dev)
+            self.slots = []
+            for k in range(self.SLOTS):
+                base = self.ptr + k * self.slot_bytes
+                self.slots.append((torch.as_tensor(_CudaArray(base, (H, W, 3), "<f4"), device=dev),
+                                   torch.as_tensor(_CudaArray(base + 12 * n, (H, W), "<f4"), device=dev),
+                                   torch.as_tensor(_CudaArray(base + 16 * n, (H, W), "<i4"), device=dev)))
             if self.rank == 0:
-                self.rgb.zero_()
-                self.T.fill_(1.0)
-                self.n_contrib.zero_()
+                for rgb, T, cnt in self.slots:
+                    rgb.zero_()
+                    T.fill_(1.0)
+                    cnt.zero_()
                 torch.cuda.synchronize(dev)
         dist.barrier(group)
+
+    def slot(self, k: int):
+        """(rgb, T, n_contrib) of frame k's slot."""
+        return self.slots[k % self.SLOTS]
 
     def close(self):
         dist.barrier(self.group)
@@ -233,6 +249,7 @@ class BandRenderer:
         self._peer = {}
         self._rows = None
         self._flag = None
+        self._frames = 0  # frames rendered: selects the peer frame's slot (the same on every rank)
 
     def peer_frame(self, W: int, H: int) -> PeerFrame:
         if (W, H) not in self._peer:
@@ -274,7 +291,8 @@ class BandRenderer:
         return self._full[key]
 
     def render(self, cloud: GaussianCloud, cam, with_stats: bool = True, timers=None) -> BandFrame:
-        """One frame: ``timers`` (5 CUDA events) bracket K1 | partition + K2-K6 | K7 | gather."""
+        """One frame: ``timers`` (5 CUDA events) bracket K1 | partition + K2-K6 | K7 | gather.  With peer output,
+        rank 0's returned tensors are valid until it renders the frame after next (see ``PeerFrame``)."""
         rank = dist.get_rank(self.group)
         ev = timers
         with torch.cuda.device(self.device):
@@ -294,7 +312,8 @@ class BandRenderer:
             outs = None
             if self.output == "peer":
                 pf = self.peer_frame(c.width, c.height)
-                outs = (pf.rgb, pf.T, pf.n_contrib)
+                outs = pf.slot(self._frames)
+            self._frames += 1
             if with_stats:
                 frame = self.r.finish(cloud, cam, band, with_stats=True, outputs=outs)
             else:

@@ -41,6 +41,21 @@ def test_reference_arm_only_rank0_prints_under_torchrun():
     assert not [l for l in r.stdout.splitlines() if l.startswith("{")]
 
 
+def test_gpu_arm_refuses_a_world_size_mismatch():
+    """Under torchrun, --gpus must equal WORLD_SIZE (a plain `bench.py --gpus 8` re-launches itself instead)."""
+    r = _bench(["--gpus", "3", "--config", "c1", "--steps", "1"], {"RANK": "0", "WORLD_SIZE": "2", "LOCAL_RANK": "0"},
+               timeout=120)
+    assert r.returncode == 2
+    assert "WORLD_SIZE" in r.stdout
+
+
+def test_reference_arm_reports_the_requested_gpu_count():
+    r = _bench(["--impl", "reference", "--gpus", "4", "--config", "c1", "--steps", "1", "--warmup", "0"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["n_gpus"] == 4
+
+
 def test_gpu_arm_options():
     r = _bench(["--help"], timeout=120)
     assert r.returncode == 0
@@ -64,6 +79,6 @@ def test_gpu_arm_line_has_the_contract_keys():
     assert d["value"] > 0 and d["steps"] == 4 and d["warmup"] == 3 and d["gpu_launches"] > 0
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     rf = d["roofline"]
-    assert rf["bound"] in ("hbm", "tensor") and rf["peak"] > 0 and 0 < rf["frac"] < 1
+    assert rf["bound"] in ("hbm", "tensor", "issue") and rf["peak"] > 0 and 0 < rf["frac"] < 1
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
     assert d["clocks"]["sm_mhz"] > 0

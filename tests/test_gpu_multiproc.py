@@ -33,15 +33,22 @@ def _worker(rank, world, port, q):
         cam = synthetic.make_camera(640, 360)
         cloud = tcgs.GaussianCloud.from_arrays(scene, "cuda")
         br = shard.BandRenderer("cuda", output="peer")
+        cam2 = synthetic.CameraSpec(cam.view, cam.fx * 1.1, cam.fy * 1.1, cam.cx, cam.cy, cam.width, cam.height,
+                                    cam.near)
+        cams = [cam, cam2, cam]
         results = []
-        for k in range(2):  # two frames: the mapping is reused
-            bf = br.render(cloud, cam, with_stats=True)
+        prev = None
+        for k, c in enumerate(cams):  # three frames, two cameras: the mapping and both slots are reused
+            bf = br.render(cloud, c, with_stats=True)
             if rank == 0:
-                ref = tcgs.Renderer("cuda").render_frame(cloud, cam, timed=False)
+                ref = tcgs.Renderer("cuda").render_frame(cloud, c, timed=False)
                 results.append((torch.equal(bf.rgb, ref.rgb), torch.equal(bf.T, ref.T),
                                 torch.equal(bf.n_contrib, ref.n_contrib),
                                 bf.stats.f_blend == ref.stats.f_blend, bf.stats.n_splats == ref.stats.n_splats,
                                 bf.bands))
+                if prev is not None:  # double buffering: the previous frame is still intact on rank 0
+                    results.append(tuple([torch.equal(prev[0], prev[1])] * 5) + (bf.bands,))
+                prev = (bf.rgb, ref.rgb.clone())
         br.close()
         if rank == 0:
             q.put(results)

@@ -380,12 +380,14 @@ def blend_ablation(tcgs, cloud, cam, dev, reps=10):
     form) x EarlyCull on/off.  Device ms per launch (CUDA events on the launching stream) + fragment counts."""
     import torch
 
+    from paper_2505_24796_b200.raster import camera_struct
+
     out = {}
     for spec in ("tcgs", "tcgs-fp16", "tcgs-ffma"):
         for ec in (True, False):
             r = tcgs.Renderer(dev, tcgs.make_backend(spec, use_early_cull=ec), schedule="dynamic")
             f = r.render_frame(cloud, cam, timed=False)
-            c = tcgs.camera_struct(cam)
+            c = camera_struct(cam)
             o = r._opts()
             rgb, T, cnt = r.outputs(c.width, c.height)
             st = torch.cuda.current_stream(dev).cuda_stream

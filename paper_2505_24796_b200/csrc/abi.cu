@@ -1,5 +1,6 @@
 // abi.cu -- the extern "C" boundary of libtcgs.so (include/tcgs.h).
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -12,6 +13,16 @@ using namespace tcgs;
 
 static std::atomic<unsigned long long> g_launches{0};
 void tcgs::note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+thread_local bool tcgs::g_pdl_frame = true;
+
+bool tcgs::pdl_enabled() {
+    static const bool on = [] {
+        const char *v = getenv("TCGS_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
 
 extern "C" int tcgs_device_check(void);
 
@@ -30,6 +41,8 @@ int cuda_fail(cudaError_t e, const char *where) {
 }
 
 __global__ void init_counters(DevCounters *c, int debug) {
+    pdl_wait();
+    pdl_launch();
     DevCounters z;
     memset(&z, 0, sizeof(z));
     z.key_min = ~0ull;
@@ -41,6 +54,8 @@ struct CounterSet {
     DevCounters *c[TCGS_MAX_VIEWS_PER_PASS];
 };
 __global__ void init_counters_views(const __grid_constant__ CounterSet s, int n, int debug) {
+    pdl_wait();
+    pdl_launch();
     if ((int)threadIdx.x < n) {
         DevCounters z;
         memset(&z, 0, sizeof(z));
@@ -177,6 +192,7 @@ size_t tcgs_workspace_size(int64_t P, int32_t width, int32_t height, int64_t max
 
 int tcgs_preprocess(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts *opts, void *ws,
                     size_t ws_bytes, int64_t max_splats, void *stream) {
+    pdl_for(opts);
     int rc = check_scene(scene);
     if (rc) return rc;
     rc = check_common(cam, opts, ws, ws_bytes, scene->P, max_splats);
@@ -184,9 +200,9 @@ int tcgs_preprocess(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_
     cudaStream_t st = (cudaStream_t)stream;
     const Layout L = Layout::make(scene->P, cam->width, cam->height, max_splats);
     time_mark(opts, ws, ST_PRE, 0, st);
-    note_launch();
-    init_counters<<<1, 1, 0, st>>>(at<DevCounters>(ws, L.counters), opts ? opts->debug : 0);
-    cudaError_t e = launch_preprocess(*scene, *cam, make_band(*cam, opts), opts ? opts->debug : 0,
+    cudaError_t e = launch_k(init_counters, 1, 1, 0, st, at<DevCounters>(ws, L.counters), opts ? opts->debug : 0);
+    if (e != cudaSuccess) return cuda_fail(e, "init_counters");
+    e = launch_preprocess(*scene, *cam, make_band(*cam, opts), opts ? opts->debug : 0,
                                       opts ? opts->coverage : 0, opts ? opts->defer_colour : 0, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "preprocess");
     time_mark(opts, ws, ST_PRE, 1, st);
@@ -195,6 +211,7 @@ int tcgs_preprocess(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_
 
 int tcgs_colour(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes,
                 int64_t max_splats, void *stream) {
+    pdl_for(opts);
     int rc = check_scene(scene);
     if (rc) return rc;
     rc = check_common(cam, opts, ws, ws_bytes, scene->P, max_splats);
@@ -207,6 +224,7 @@ int tcgs_colour(const tcgs_scene *scene, const tcgs_camera *cam, const tcgs_opts
 
 int tcgs_preprocess_views(const tcgs_scene *scene, const tcgs_camera *cams, int32_t n_views, const tcgs_opts *opts,
                           void *const *ws, size_t ws_bytes, int64_t max_splats, void *stream) {
+    pdl_for(opts);
     int rc = check_scene(scene);
     if (rc) return rc;
     if (!cams || !ws) return fail(TCGS_ERR_INVALID_ARG, "null cameras or workspaces");
@@ -226,9 +244,9 @@ int tcgs_preprocess_views(const tcgs_scene *scene, const tcgs_camera *cams, int3
     }
     if ((rc = device_ok())) return rc;
     cudaStream_t st = (cudaStream_t)stream;
-    note_launch();
-    init_counters_views<<<1, 32, 0, st>>>(cs, n_views, opts ? opts->debug : 0);
-    cudaError_t e = launch_preprocess_views(*scene, cams, bands, n_views, opts ? opts->debug : 0,
+    cudaError_t e = launch_k(init_counters_views, 1, 32, 0, st, cs, n_views, opts ? opts->debug : 0);
+    if (e != cudaSuccess) return cuda_fail(e, "init_counters_views");
+    e = launch_preprocess_views(*scene, cams, bands, n_views, opts ? opts->debug : 0,
                                             opts ? opts->coverage : 0, opts ? opts->defer_colour : 0, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "preprocess_views");
     return TCGS_OK;
@@ -236,6 +254,7 @@ int tcgs_preprocess_views(const tcgs_scene *scene, const tcgs_camera *cams, int3
 
 int tcgs_bin(int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes,
              int64_t max_splats, void *stream) {
+    pdl_for(opts);
     int rc = check_common(cam, opts, ws, ws_bytes, P, max_splats);
     if (rc) return rc;
     const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
@@ -248,6 +267,7 @@ int tcgs_bin(int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, void *ws,
 
 int tcgs_blend(int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, void *ws, size_t ws_bytes,
                int64_t max_splats, float *rgb, float *T, int32_t *n_contrib, void *stream) {
+    pdl_for(opts);
     int rc = check_common(cam, opts, ws, ws_bytes, P, max_splats);
     if (rc) return rc;
     if (!rgb || !T || !n_contrib) return fail(TCGS_ERR_INVALID_ARG, "null output");
@@ -358,6 +378,7 @@ int tcgs_decode_stats(const void *snapshot, const tcgs_opts *opts, tcgs_stats *s
 int tcgs_blend_lists(int64_t P, const double *mean2d, const double *conic, const double *opacity, const float *colors,
                      const int64_t *offsets, const int32_t *ids, const tcgs_camera *cam, const tcgs_opts *opts,
                      void *ws, size_t ws_bytes, float *rgb, float *T, int32_t *n_contrib, void *stream) {
+    pdl_for(opts);
     int rc = check_common(cam, opts, ws, ws_bytes, P, 1);
     if (rc) return rc;
     if (P > 0 && (!mean2d || !conic || !opacity || !colors)) return fail(TCGS_ERR_INVALID_ARG, "null records");
@@ -365,9 +386,9 @@ int tcgs_blend_lists(int64_t P, const double *mean2d, const double *conic, const
     cudaStream_t st = (cudaStream_t)stream;
     const Layout L = Layout::make(P, cam->width, cam->height, 1);
     const Band band = make_band(*cam, opts);
-    note_launch();
-    init_counters<<<1, 1, 0, st>>>(at<DevCounters>(ws, L.counters), 0);
-    cudaError_t e = launch_pack_lists(P, mean2d, conic, opacity, colors, offsets, band, ws, L, st);
+    cudaError_t e = launch_k(init_counters, 1, 1, 0, st, at<DevCounters>(ws, L.counters), 0);
+    if (e != cudaSuccess) return cuda_fail(e, "init_counters");
+    e = launch_pack_lists(P, mean2d, conic, opacity, colors, offsets, band, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "pack_lists");
     e = launch_render(opts ? opts->alpha_mode : 0, opts ? opts->early_cull : 1, opts ? opts->dump_beta : nullptr,
                       opts ? opts->dump_class : nullptr, *cam, band, reinterpret_cast<const uint32_t *>(ids), ws, L,
@@ -414,6 +435,8 @@ namespace {
 __global__ void copy_projection_kernel(int64_t P, const int32_t *radius, const Rec *rec, const double *dconic,
                                        const double *ddepth, const double *dmean2d, uint8_t *visible, double *mean2d, double *conic,
                                        double *depth, int32_t *rad_out, float *rgb) {
+    pdl_wait();
+    pdl_launch();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P) return;
     const int32_t r = radius[i];
@@ -447,11 +470,9 @@ extern "C" int tcgs_copy_projection(const void *ws, int64_t P, const tcgs_camera
     if (e0 != cudaSuccess) return cuda_fail(e0, "copy_projection");
     if (!c.debug_written)
         return fail(TCGS_ERR_INVALID_ARG, "tcgs_copy_projection needs the frame preprocessed with opts->debug = 1");
-    note_launch();
-    copy_projection_kernel<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(
+    cudaError_t e = launch_k(copy_projection_kernel, (unsigned)((P + 255) / 256), 256, 0, st,
         P, at<int32_t>(ws, L.radius), at<Rec>(ws, L.rec), at<double>(ws, L.dbg_conic), at<double>(ws, L.dbg_depth),
         at<double>(ws, L.dbg_mean2d), visible, mean2d, conic, depth, radius, rgb);
-    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "copy_projection");
     return TCGS_OK;
 }

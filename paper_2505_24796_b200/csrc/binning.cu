@@ -104,6 +104,8 @@ __device__ __forceinline__ int depth_shift(unsigned long long range) {
 
 __global__ void __launch_bounds__(256) depth_fix_hist(const unsigned long long *src, uint32_t *keys, uint32_t *idx,
                                                       int64_t P, DevCounters *ctr, SortState *ss) {
+    pdl_wait();
+    pdl_launch();
     __shared__ uint32_t h[DEPTH_PASSES][RADIX];
     for (int e = threadIdx.x; e < DEPTH_PASSES * RADIX; e += blockDim.x) (&h[0][0])[e] = 0;
     __syncthreads();
@@ -165,6 +167,8 @@ constexpr int FIX_SMEM = 4096;
 __global__ void __launch_bounds__(256) depth_fixup(const uint32_t *k0, const uint32_t *k1, uint32_t *i0, uint32_t *i1,
                                                    const unsigned long long *src, int64_t P, DevCounters *ctr,
                                                    uint32_t *long_runs) {
+    pdl_wait();
+    pdl_launch();
     if (ctr->depth_shift == 0) return;  // the prefix is the whole key
     const uint32_t *key = ctr->depth_cur ? k1 : k0;
     uint32_t *idx = ctr->depth_cur ? i1 : i0;
@@ -213,6 +217,8 @@ __global__ void __launch_bounds__(256) depth_fixup_long(const uint32_t *k0, cons
                                                         uint32_t *i1, const unsigned long long *src, int64_t P,
                                                         DevCounters *ctr, const uint32_t *long_runs,
                                                         unsigned long long *gscratch) {
+    pdl_wait();
+    pdl_launch();
     __shared__ unsigned long long sf[FIX_SMEM];
     __shared__ uint32_t sg[FIX_SMEM];
     const unsigned nruns = ctr->n_long_runs;
@@ -286,6 +292,8 @@ template <typename KT, int IPT, int DB>
 __global__ void __launch_bounds__(OS_THREADS) radix_upsweep(const KT *k0, const KT *k1, const unsigned long long *n_dev,
                                                             int64_t n_host, int64_t cap, int pass, int shift,
                                                             const SortState *ss, uint32_t *table, int64_t T) {
+    pdl_wait();
+    pdl_launch();
     if (!ss->pass_do[pass]) return;
     constexpr int TILE_ITEMS = OS_THREADS * IPT;
     __shared__ uint32_t wh[OS_WARPS][RADIX];
@@ -319,6 +327,8 @@ __global__ void __launch_bounds__(OS_THREADS) radix_upsweep(const KT *k0, const 
 template <int IPT>
 __global__ void __launch_bounds__(256) radix_rowscan(const unsigned long long *n_dev, int64_t n_host, int64_t cap,
                                                      int pass, SortState *ss, uint32_t *table, int64_t T) {
+    pdl_wait();
+    pdl_launch();
     if (!ss->pass_do[pass]) return;
     constexpr int TILE_ITEMS = OS_THREADS * IPT;
     __shared__ uint32_t wt[8];
@@ -351,6 +361,8 @@ __global__ void __launch_bounds__(OS_THREADS, 3) radix_downsweep(KT *k0, KT *k1,
                                                               const unsigned long long *n_dev, int64_t n_host,
                                                               int64_t cap, int pass, int shift, const SortState *ss,
                                                               const uint32_t *table, int64_t T) {
+    pdl_wait();
+    pdl_launch();
     if (!ss->pass_do[pass]) return;
     constexpr int TILE_ITEMS = OS_THREADS * IPT;
     extern __shared__ __align__(16) unsigned char os_smem[];
@@ -454,14 +466,13 @@ cudaError_t launch_radix_pass_db(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, con
     const int64_t tiles = div_up(n_dev ? cap : n_host, OS_THREADS * IPT);
     const unsigned grid = (unsigned)(tiles > 0 ? tiles : 1);
     uint32_t *table = table_all + (int64_t)pass * RADIX * tiles;
-    note_launch();
-    radix_upsweep<KT, IPT, DB><<<grid, OS_THREADS, 0, st>>>(k0, k1, n_dev, n_host, cap, pass, shift, ss, table, tiles);
-    note_launch();
-    radix_rowscan<IPT><<<RADIX, 256, 0, st>>>(n_dev, n_host, cap, pass, ss, table, tiles);
-    note_launch();
-    radix_downsweep<KT, IPT, DB><<<grid, OS_THREADS, smem, st>>>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss,
-                                                                 table, tiles);
-    return cudaGetLastError();
+    cudaError_t e = launch_k(radix_upsweep<KT, IPT, DB>, grid, OS_THREADS, 0, st, k0, k1, n_dev, n_host, cap, pass,
+                             shift, (const SortState *)ss, table, tiles);
+    if (e == cudaSuccess) e = launch_k(radix_rowscan<IPT>, RADIX, 256, 0, st, n_dev, n_host, cap, pass, ss, table, tiles);
+    if (e == cudaSuccess)
+        e = launch_k(radix_downsweep<KT, IPT, DB>, grid, OS_THREADS, (size_t)smem, st, k0, k1, v0, v1, n_dev, n_host,
+                     cap, pass, shift, (const SortState *)ss, (const uint32_t *)table, tiles);
+    return e;
 }
 
 // One pass on digit bits [shift, shift + db) (db <= RADIX_BITS): fewer digit bits, fewer warp ballots.
@@ -566,6 +577,8 @@ __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx
                                                              int band_y0, int band_y1,
                                                              int64_t P, unsigned long long *blocksum, int64_t cap,
                                                              SortState *ss_tile, int npass) {
+    pdl_wait();
+    pdl_launch();
     const uint32_t *order = ctr->depth_cur ? idx1 : idx0;
     const int64_t beg = (int64_t)blockIdx.x * DUP_ITEMS;
     unsigned long long s = 0;
@@ -606,6 +619,8 @@ __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx
 
 __global__ void __launch_bounds__(256) bin_init(uint4 *zero, int64_t n16, uint2 *ranges, int64_t n_ranges,
                                                 DevCounters *ctr) {
+    pdl_wait();
+    pdl_launch();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = t; i < n16; i += step) zero[i] = make_uint4(0u, 0u, 0u, 0u);
     for (int64_t i = t; i < n_ranges; i += step) ranges[i] = make_uint2(0u, 0u);
@@ -628,6 +643,8 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                                                               const unsigned long long *blockoff, int tiles_x,
                                                               int band_y0, int band_y1, int64_t cap, KT *tkey,
                                                               uint32_t *tval) {
+    pdl_wait();
+    pdl_launch();
     __shared__ uint32_t incl[DUP_THREADS];
     __shared__ uint32_t gid[DUP_THREADS];
     __shared__ short4 rc[DUP_THREADS];
@@ -787,6 +804,8 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
 template <typename KT>
 __global__ void __launch_bounds__(256) tile_ranges(const KT *k0, const KT *k1, const DevCounters *ctr, int64_t cap,
                                                    uint2 *ranges) {
+    pdl_wait();
+    pdl_launch();
     const KT *keys = ctr->tile_cur ? k1 : k0;
     const unsigned long long nn = ctr->n_splats;
     const int64_t n = (int64_t)(nn < (unsigned long long)cap ? nn : (unsigned long long)cap);
@@ -822,6 +841,8 @@ __global__ void __launch_bounds__(256) tile_ranges(const KT *k0, const KT *k1, c
 // Debug / KAT entry: pack caller-given projected records and CSR offsets.
 __global__ void pack_records(int64_t P, const double *mean2d, const double *conic, const double *opacity,
                              const float *colors, Rec *rec) {
+    pdl_wait();
+    pdl_launch();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P) return;
     Rec r;
@@ -841,6 +862,8 @@ __global__ void pack_records(int64_t P, const double *mean2d, const double *coni
 }
 
 __global__ void pack_ranges(const int64_t *offsets, int band_tile0, int n_tiles, uint2 *ranges) {
+    pdl_wait();
+    pdl_launch();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_tiles) return;
     ranges[t] = make_uint2((uint32_t)offsets[band_tile0 + t], (uint32_t)offsets[band_tile0 + t + 1]);
@@ -851,6 +874,8 @@ __global__ void pack_ranges(const int64_t *offsets, int band_tile0, int n_tiles,
 __global__ void __launch_bounds__(256) row_counts_kernel(int64_t P, const short4 *rect,
                                                          const Rec *rec, int coverage, int tiles_y,
                                                          unsigned long long *out) {
+    pdl_wait();
+    pdl_launch();
     constexpr int SMEM_ROWS = 4096;
     __shared__ unsigned long long h[SMEM_ROWS];
     const bool priv = tiles_y <= SMEM_ROWS;
@@ -891,18 +916,19 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     unsigned long long *blocksum = at<unsigned long long>(ws, L.blocksum);
     const int nblk = (int)div_up(P > 0 ? P : 1, DUP_ITEMS);
     // K3
-    note_launch();
     const bool exact = band.coverage == TCGS_COVER_ELLIPSE;
-    (exact ? count_upsweep<true> : count_upsweep<false>)<<<nblk, DUP_THREADS, 0, st>>>(
-        at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr,
-        at<short4>(ws, L.rect), at<Rec>(ws, L.rec), at<unsigned long long>(ws, L.tmask), band.y0, band.y1, P,
-        blocksum, cap, ss_tile, npass);
+    cudaError_t e0 = launch_k(exact ? count_upsweep<true> : count_upsweep<false>, nblk, DUP_THREADS, 0, st,
+        (const uint32_t *)at<uint32_t>(ws, L.idx[0]), (const uint32_t *)at<uint32_t>(ws, L.idx[1]), ctr,
+        (const short4 *)at<short4>(ws, L.rect), (const Rec *)at<Rec>(ws, L.rec), at<unsigned long long>(ws, L.tmask),
+        band.y0, band.y1, P, blocksum, cap, ss_tile, npass);
+    if (e0 != cudaSuccess) return e0;
     // K4
-    note_launch();
-    (exact ? duplicate_keys<KT, true> : duplicate_keys<KT, false>)<<<nblk, DUP_THREADS, 0, st>>>(
-        at<uint32_t>(ws, L.idx[0]), at<uint32_t>(ws, L.idx[1]), ctr,
-        at<short4>(ws, L.rect), at<Rec>(ws, L.rec), at<unsigned long long>(ws, L.tmask), P, blocksum,
+    e0 = launch_k(exact ? duplicate_keys<KT, true> : duplicate_keys<KT, false>, nblk, DUP_THREADS, 0, st,
+        (const uint32_t *)at<uint32_t>(ws, L.idx[0]), (const uint32_t *)at<uint32_t>(ws, L.idx[1]),
+        (const DevCounters *)ctr, (const short4 *)at<short4>(ws, L.rect), (const Rec *)at<Rec>(ws, L.rec),
+        (const unsigned long long *)at<unsigned long long>(ws, L.tmask), P, (const unsigned long long *)blocksum,
         band.tiles_x, band.y0, band.y1, cap, tk0, tv0);
+    if (e0 != cudaSuccess) return e0;
     // K5
     // the key's bits split as evenly as possible over the passes (13 bits: 7 + 6, not 8 + 5)
     const int db0 = TCGS_TILE_DIGITS_EVEN ? (bits + npass - 1) / npass : RADIX_BITS;
@@ -914,9 +940,8 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
         if (e != cudaSuccess) return e;
     }
     // K6
-    note_launch();
-    tile_ranges<KT><<<(unsigned)div_up(div_up(cap, 8), 256), 256, 0, st>>>(tk0, tk1, ctr, cap, at<uint2>(ws, L.ranges));
-    return cudaGetLastError();
+    return launch_k(tile_ranges<KT>, (unsigned)div_up(div_up(cap, 8), 256), 256, 0, st, (const KT *)tk0, (const KT *)tk1,
+                    (const DevCounters *)ctr, cap, at<uint2>(ws, L.ranges));
 }
 
 }  // namespace
@@ -926,12 +951,9 @@ cudaError_t launch_row_counts(int64_t P, const Band &band, const void *ws, const
     cudaError_t e = cudaMemsetAsync(out, 0, sizeof(int64_t) * (size_t)band.tiles_y, st);
     if (e != cudaSuccess || P <= 0) return e;
     const int64_t blocks = div_up(P, 256 * 8);
-    note_launch();
-    row_counts_kernel<<<(unsigned)(blocks < 4 * 148 ? blocks : 4 * 148), 256, 0, st>>>(
-        P, at<short4>(ws, L.rect), at<Rec>(ws, L.rec), band.coverage,
-        band.tiles_y,
-        reinterpret_cast<unsigned long long *>(out));
-    return cudaGetLastError();
+    return launch_k(row_counts_kernel, (unsigned)(blocks < 4 * 148 ? blocks : 4 * 148), 256, 0, st, P,
+                    (const short4 *)at<short4>(ws, L.rect), (const Rec *)at<Rec>(ws, L.rec), band.coverage,
+                    band.tiles_y, reinterpret_cast<unsigned long long *>(out));
 }
 
 int tile_key_bits(const Band &band) {
@@ -946,11 +968,9 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
     SortState *ss_depth = at<SortState>(ws, L.sort_state[0]);
     // one kernel clears the sort state, the tile ranges and the per-binning counters (K1's dropped /
     // n_visible / key_min / key_max stay)
-    note_launch();
-    bin_init<<<64, 256, 0, st>>>(reinterpret_cast<uint4 *>(static_cast<char *>(ws) + L.zero_begin),
-                                 (int64_t)(L.zero_bytes / sizeof(uint4)), at<uint2>(ws, L.ranges),
-                                 (int64_t)(band.n_tiles() ? band.n_tiles() : 1), ctr);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_k(bin_init, 64, 256, 0, st, reinterpret_cast<uint4 *>(static_cast<char *>(ws) + L.zero_begin),
+                             (int64_t)(L.zero_bytes / sizeof(uint4)), at<uint2>(ws, L.ranges),
+                             (int64_t)(band.n_tiles() ? band.n_tiles() : 1), ctr);
     if (e != cudaSuccess) return e;
     uint32_t *k0 = at<uint32_t>(ws, L.key64[0]);
     uint32_t *k1 = at<uint32_t>(ws, L.key64[1]);
@@ -959,20 +979,20 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
     if (P > 0) {
         // K2: 24-bit depth-prefix radix sort + exact float64 fix-up of equal prefixes
         const unsigned long long *src = at<unsigned long long>(ws, L.key_src);
-        note_launch();
-        depth_fix_hist<<<2 * 148, 256, 0, st>>>(src, k0, i0, P, ctr, ss_depth);
+        e = launch_k(depth_fix_hist, 2 * 148, 256, 0, st, src, k0, i0, P, ctr, ss_depth);
+        if (e != cudaSuccess) return e;
         for (int p = 0; p < DEPTH_PASSES; p++) {
             e = launch_radix_pass<uint32_t, DEPTH_IPT>(k0, k1, i0, i1, nullptr, P, P, p, RADIX_BITS * p, RADIX_BITS,
                                                        ss_depth,
                                                       at<uint32_t>(ws, L.lb_depth), st);
             if (e != cudaSuccess) return e;
         }
-        note_launch();
-        depth_fixup<<<(unsigned)std::min<int64_t>(div_up(P, 256), 8 * 148), 256, 0, st>>>(
-            k0, k1, i0, i1, src, P, ctr, at<uint32_t>(ws, L.long_runs));
-        note_launch();
-        depth_fixup_long<<<148, 256, 0, st>>>(k0, k1, i0, i1, src, P, ctr, at<uint32_t>(ws, L.long_runs),
-                                              at<unsigned long long>(ws, L.fix_scratch));
+        e = launch_k(depth_fixup, (unsigned)std::min<int64_t>(div_up(P, 256), 8 * 148), 256, 0, st,
+                     (const uint32_t *)k0, (const uint32_t *)k1, i0, i1, src, P, ctr, at<uint32_t>(ws, L.long_runs));
+        if (e == cudaSuccess)
+            e = launch_k(depth_fixup_long, 148, 256, 0, st, (const uint32_t *)k0, (const uint32_t *)k1, i0, i1, src, P,
+                         ctr, (const uint32_t *)at<uint32_t>(ws, L.long_runs), at<unsigned long long>(ws, L.fix_scratch));
+        if (e != cudaSuccess) return e;
     }
     if (band.n_tiles() <= 65536) return bin_tiles<uint16_t>(P, band, ws, L, cap, st);
     return bin_tiles<uint32_t>(P, band, ws, L, cap, st);
@@ -981,16 +1001,13 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
 cudaError_t launch_pack_lists(int64_t P, const double *mean2d, const double *conic, const double *opacity,
                               const float *colors, const int64_t *offsets, const Band &band, void *ws,
                               const Layout &L, cudaStream_t st) {
-    if (P > 0) {
-        note_launch();
-        pack_records<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(P, mean2d, conic, opacity, colors, at<Rec>(ws, L.rec));
-    }
+    cudaError_t e = cudaSuccess;
+    if (P > 0) e = launch_k(pack_records, (unsigned)((P + 255) / 256), 256, 0, st, P, mean2d, conic, opacity, colors,
+                            at<Rec>(ws, L.rec));
     const int nt = band.n_tiles();
-    if (nt > 0) {
-        note_launch();
-        pack_ranges<<<(nt + 255) / 256, 256, 0, st>>>(offsets, band.y0 * band.tiles_x, nt, at<uint2>(ws, L.ranges));
-    }
-    return cudaGetLastError();
+    if (e == cudaSuccess && nt > 0)
+        e = launch_k(pack_ranges, (nt + 255) / 256, 256, 0, st, offsets, band.y0 * band.tiles_x, nt, at<uint2>(ws, L.ranges));
+    return e;
 }
 
 }  // namespace tcgs

@@ -263,6 +263,10 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
     for (int q = 0; q < 5; q++)  // ragged / unaligned segments: coalesced cooperative copy
         if (!bulk[q])
             for (int e = threadIdx.x; e < n * per[q]; e += NT) seg[q][e] = src[q][base * per[q] + e];
+    // PDL: the scene inputs above are never written by a libtcgs kernel, so they stream in while the previous
+    // kernel of the stream finishes; everything below writes the workspace
+    pdl_wait();
+    pdl_launch();
     auto wait_bar = [&](int g) {
         if (any_bulk[g]) {
             asm volatile(
@@ -501,11 +505,9 @@ cudaError_t launch_k1(const PreViews<NV> &pv, const tcgs_scene &scene, int F, in
         configured = smem;
     }
     const unsigned blocks = (unsigned)((scene.P + nt - 1) / nt);
-    note_launch();
-    preprocess_kernel<T, NV><<<blocks, nt, smem, st>>>(pv, (const T *)scene.means, (const T *)scene.scales,
-                                                      (const T *)scene.rotations, (const T *)scene.opacities,
-                                                      (const T *)scene.features);
-    return cudaGetLastError();
+    return launch_k(preprocess_kernel<T, NV>, blocks, nt, smem, st, pv, (const T *)scene.means,
+                    (const T *)scene.scales, (const T *)scene.rotations, (const T *)scene.opacities,
+                    (const T *)scene.features);
 }
 
 PreArgs view_args(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug, int coverage,
@@ -557,6 +559,8 @@ struct ColourArgs {
 template <typename T>
 __global__ void __launch_bounds__(256) colour_kernel(ColourArgs c, const T *__restrict__ g_means,
                                                      const T *__restrict__ g_feats) {
+    pdl_wait();
+    pdl_launch();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= c.P) return;
     const short4 r = c.rect[i];
@@ -594,12 +598,11 @@ cudaError_t launch_colour(const tcgs_scene &scene, const tcgs_camera &cam, const
     c.rect = a.rect;
     c.rec = a.rec;
     const unsigned blocks = (unsigned)((scene.P + 255) / 256);
-    note_launch();
     if (scene.dtype == TCGS_F64)
-        colour_kernel<double><<<blocks, 256, 0, st>>>(c, (const double *)scene.means, (const double *)scene.features);
-    else
-        colour_kernel<float><<<blocks, 256, 0, st>>>(c, (const float *)scene.means, (const float *)scene.features);
-    return cudaGetLastError();
+        return launch_k(colour_kernel<double>, blocks, 256, 0, st, c, (const double *)scene.means,
+                        (const double *)scene.features);
+    return launch_k(colour_kernel<float>, blocks, 256, 0, st, c, (const float *)scene.means,
+                    (const float *)scene.features);
 }
 
 cudaError_t launch_preprocess(const tcgs_scene &scene, const tcgs_camera &cam, const Band &band, int debug,

@@ -119,7 +119,22 @@ constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(K7_BATCH >> 3) << 17) | ((uin
 __device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
+#ifndef TCGS_K7_WAIT
+#define TCGS_K7_WAIT 0
+#endif
+#ifdef TCGS_K7_TIMING  // experiment builds: cycles spent waiting, per barrier kind (tcgs_k7_timing reads them)
+__device__ unsigned long long g_k7_wait[8];
+#define K7_TWAIT(kind, call)                                        \
+    do {                                                            \
+        const long long t0_ = clock64();                            \
+        call;                                                       \
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_k7_wait[kind], (unsigned long long)(clock64() - t0_)); \
+    } while (0)
+#else
+#define K7_TWAIT(kind, call) call
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
+#if TCGS_K7_WAIT == 0
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
@@ -131,6 +146,24 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t pari
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity), "r"(0x989680u)  // suspend-time hint: sleep until the phase flips instead of spinning
         : "memory");
+#else
+    // experiment: try_wait without a hint, then back off with nanosleep (TCGS_K7_WAIT ns) so a waiting warp
+    // leaves its issue slots to the working ones
+    uint32_t ok;
+    for (;;) {
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P1;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) break;
+        __nanosleep(TCGS_K7_WAIT);
+    }
+#endif
 }
 __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
     asm volatile(
@@ -434,12 +467,12 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
         const float4 col = make_float4(rc.r, rc.g, rc.b, 0.f);
 
         // wait for the compaction token
-        if (!(p == 0 && m == 0)) mbar_wait(&sm.tok[p], p == 0 ? ((m - 1) & 1) : (m & 1));
+        if (!(p == 0 && m == 0)) K7_TWAIT(0, mbar_wait(&sm.tok[p], p == 0 ? ((m - 1) & 1) : (m & 1)));
         int k = sm.c_k;
         bool open = sm.c_open != 0;
         auto acquire = [&]() {
             if (!open) {
-                mbar_wait(&sm.empty[k % S], ((k / S) & 1) ^ 1);
+                K7_TWAIT(1, mbar_wait(&sm.empty[k % S], ((k / S) & 1) ^ 1));
                 open = true;
             }
         };
@@ -473,7 +506,7 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
                 mbar_arrive(&sm.full[st]);
                 if (TC && tile >= 0) {
                     const int b = k % NB;
-                    mbar_wait(&sm.tmem_empty[b], ((k / NB) & 1) ^ 1);
+                    K7_TWAIT(2, mbar_wait(&sm.tmem_empty[b], ((k / NB) & 1) ^ 1));
                     tc_fence_after();
                     const uint64_t bdesc = umma_desc(sm.V[st]);
 #pragma unroll
@@ -623,6 +656,13 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
     if (TC) tc_fence_before();
     __syncthreads();
     if (TC) tc_fence_after();
+    // PDL: the set-up above (A operand, barriers, TMEM) overlapped the previous kernel; the lists, records and
+    // counters it reads below are written by the kernels before it
+    pdl_wait();
+    pdl_launch();
+#ifdef TCGS_K7_TIMING
+    const long long t_start = clock64();
+#endif
     const uint32_t tmem = TC ? sm.tmem_base : 0u;
     const uint32_t *ids = a.ids_override ? a.ids_override : (a.ctr->tile_cur ? a.ids1 : a.ids0);
 
@@ -676,7 +716,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
         };
         for (int k = 0;; k++) {
             const int st = k % S, b = k % NB;
-            mbar_wait(&sm.full[st], (k / S) & 1);
+            K7_TWAIT(3, mbar_wait(&sm.full[st], (k / S) & 1));
             const StageMeta m = sm.meta[st];
             if (m.seq != cur_seq || m.tile < 0) {
                 if (cur_seq >= 0) flush();
@@ -703,7 +743,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 if (warp_done && lane == 0) atomicAdd(&sm.retire[cur_seq & 7], 1);
             }
             if (TC) {
-                mbar_wait(&sm.mma_done[b], (k / NB) & 1);
+                K7_TWAIT(4, mbar_wait(&sm.mma_done[b], (k / NB) & 1));
                 tc_fence_after();
             }
             bool tmem_released = false;
@@ -862,6 +902,9 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
         }
     }
 
+#ifdef TCGS_K7_TIMING
+    if (lane == 0) atomicAdd(&g_k7_wait[warp >= K7_CONSUMER_WARPS ? 5 : 6], (unsigned long long)(clock64() - t_start));
+#endif
     // the outputs may be another GPU's frame mapped over NVLink (tile-band peer output): make this thread's
     // pixel stores visible system-wide before the CTA retires
     if (warp < K7_CONSUMER_WARPS) __threadfence_system();
@@ -897,6 +940,13 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
     }
 }
 
+__global__ void k7_reset(DevCounters *ctr) {
+    pdl_wait();
+    pdl_launch();
+    if (threadIdx.x < 4) (&ctr->f_blend)[threadIdx.x] = 0ull;
+    if (threadIdx.x == 0) ctr->tile_queue = 0u;
+}
+
 template <int MODE, bool DYN, int FL>
 cudaError_t launch_mode(const RenderArgs &a, int num_sms, cudaStream_t st) {
     static bool configured_dev[TCGS_MAX_DEVICES] = {};
@@ -908,9 +958,7 @@ cudaError_t launch_mode(const RenderArgs &a, int num_sms, cudaStream_t st) {
         configured = true;
     }
     const int grid = num_sms * K7_CTAS_PER_SM;
-    note_launch();
-    render_kernel<MODE, DYN, FL><<<grid, K7_THREADS, K7_SMEM_BYTES, st>>>(a);
-    return cudaGetLastError();
+    return launch_k(render_kernel<MODE, DYN, FL>, grid, K7_THREADS, (size_t)K7_SMEM_BYTES, st, a);
 }
 
 // EarlyCull on/off for the lone-frame (dynamic) and frames-in-flight (static) schedules; the debug dump runs
@@ -948,8 +996,7 @@ cudaError_t launch_render(int alpha_mode, int early_cull, float *dump_beta, uint
     a.dump_class = dump_class;
     const bool dump = dump_beta != nullptr && dump_class != nullptr;
     // per-launch counters: the tile queue and the fragment statistics (f_blend, f_cull, terminated, pairs)
-    cudaError_t e = cudaMemsetAsync(&a.ctr->f_blend, 0, 4 * sizeof(unsigned long long), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(&a.ctr->tile_queue, 0, sizeof(unsigned int), st);
+    cudaError_t e = launch_k(k7_reset, 1, 32, 0, st, a.ctr);
     if (e != cudaSuccess) return e;
     const bool dyn = band.schedule == TCGS_SCHEDULE_DYNAMIC;
     int dev = 0, sms = 148;
@@ -968,3 +1015,16 @@ cudaError_t launch_render(int alpha_mode, int early_cull, float *dump_beta, uint
 }
 
 }  // namespace tcgs
+
+#ifdef TCGS_K7_TIMING
+// experiment builds only (not in include/tcgs.h): read and clear the K7 wait counters -- cycles summed over warps:
+// [0] producer token, [1] producer empty stage, [2] producer TMEM buffer, [3] consumer full stage,
+// [4] consumer MMA done, [5] producer total, [6] consumer total
+extern "C" int tcgs_k7_timing(unsigned long long *out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, tcgs::g_k7_wait, sizeof(unsigned long long) * 8);
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(tcgs::g_k7_wait, z, sizeof(z));
+    return 0;
+}
+#endif

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "tcgs.h"
 
 namespace tcgs {
@@ -30,7 +32,10 @@ constexpr int DUP_THREADS = 256;
 #endif
 constexpr int K7_PIX = TCGS_K7_PIX;              // pixels per consumer thread (1 or 2)
 constexpr int K7_CONSUMER_WARPS = 8 / K7_PIX;  // 256 pixels of a 16x16 tile
-constexpr int K7_PRODUCERS = 2;       // producer warps (alternate 32-entry chunks, token-ordered compaction)
+#ifndef TCGS_K7_PRODUCERS
+#define TCGS_K7_PRODUCERS 2
+#endif
+constexpr int K7_PRODUCERS = TCGS_K7_PRODUCERS;  // producer warps (alternate 32-entry chunks, token-ordered compaction)
 constexpr int K7_THREADS = 32 * (K7_CONSUMER_WARPS + K7_PRODUCERS);
 #ifndef TCGS_K7_BATCH
 #define TCGS_K7_BATCH 32
@@ -259,6 +264,40 @@ inline int current_device() {
     int d = 0;
     cudaGetDevice(&d);
     return d < 0 ? 0 : (d >= TCGS_MAX_DEVICES ? TCGS_MAX_DEVICES - 1 : d);
+}
+
+// ---------------------------------------------------------------- programmatic dependent launch (PDL)
+// Every kernel of a frame is launched with programmatic stream serialisation: the next kernel's CTAs are
+// scheduled as soon as every CTA of the current one has reached pdl_launch(), so its launch latency and its
+// prologue overlap the current kernel's tail.  Each kernel calls pdl_wait() before it touches memory an earlier
+// kernel of the stream writes (griddepcontrol.wait returns once the preceding grid has completed and its
+// writes are visible; it returns at once for an ordinary launch).  Work before pdl_wait() may only read memory
+// no libtcgs kernel writes (the caller's scene arrays).  TCGS_PDL=0 in the environment turns the attribute off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+bool pdl_enabled();
+// Set by each entry point from its options: frames in flight on several streams (static K7 schedule) launch
+// without PDL -- early-launched dependents would occupy SM slots the other streams' kernels fill better.
+extern thread_local bool g_pdl_frame;
+inline void pdl_for(const tcgs_opts *o) { g_pdl_frame = !(o && o->schedule == TCGS_SCHEDULE_STATIC); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args &&...args) {
+    note_launch();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (pdl_enabled() && g_pdl_frame) ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- PTX helpers

@@ -72,10 +72,16 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t *war
     return pre + x - v;
 }
 
-// Lanes of the warp holding the same 8-bit digit (invalid items: digit >= RADIX match only each other).
-// Nine ballots instead of MATCH.ANY, whose throughput is far lower.
+#ifndef TCGS_MATCH
+#define TCGS_MATCH 0
+#endif
+// Lanes of the warp holding the same digit (invalid items: digit >= RADIX match only each other).  Nine ballots:
+// MATCH.ANY has the higher throughput in isolation (B200: 1.9 vs 13.3 ns per warp-wide peer mask per SM,
+// scripts/micro/match_vs_ballot.cu) but its latency sits on the downsweep's serial rank chain -- with it the
+// binning took 297 instead of 251 us (r2g).  TCGS_MATCH=1 selects it.
 template <int DB = RADIX_BITS>  // digit bits (<= RADIX_BITS); invalid items carry d = RADIX
 __device__ __forceinline__ unsigned warp_peers(int d) {
+    if (TCGS_MATCH) return __match_any_sync(0xffffffffu, d);
     unsigned peers = __ballot_sync(0xffffffffu, d < RADIX);
     if (d >= RADIX) peers = ~peers;
 #pragma unroll
@@ -103,9 +109,13 @@ __device__ __forceinline__ int depth_shift(unsigned long long range) {
 }
 
 __global__ void __launch_bounds__(256) depth_fix_hist(const unsigned long long *src, uint32_t *keys, uint32_t *idx,
-                                                      int64_t P, DevCounters *ctr, SortState *ss) {
+                                                      int64_t P, DevCounters *ctr, SortState *ss, OsHeader *hdr) {
     pdl_wait();
     pdl_launch();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // a new look-back epoch for this binning's radix passes
+        hdr->magic = OS_MAGIC;
+        hdr->epoch = hdr->epoch + 1u;
+    }
     __shared__ uint32_t h[DEPTH_PASSES][RADIX];
     for (int e = threadIdx.x; e < DEPTH_PASSES * RADIX; e += blockDim.x) (&h[0][0])[e] = 0;
     __syncthreads();
@@ -442,6 +452,129 @@ __global__ void __launch_bounds__(OS_THREADS, 3) radix_downsweep(KT *k0, KT *k1,
     }
 }
 
+// ---------------------------------------------------------------- onesweep pass (decoupled look-back)
+// One kernel per stable LSD radix pass: a CTA claims the next radix tile (atomic counter: tiles are claimed in
+// launch order, so every earlier tile is being processed and the look-back always progresses), ranks its items
+// locally (ballot multi-split, as the downsweep), publishes its per-digit counts, looks back over the earlier
+// tiles' published counts (inclusive prefixes stop the walk) to get its global offset per digit, and scatters
+// through shared memory.  Digit totals come from one histogram computed before the pass (depth_fix_hist for
+// the depth key, duplicate_keys for the tile key), so no separate upsweep / row-scan kernels run.
+constexpr uint64_t OS_FLAG_AGG = 1ull << 30, OS_FLAG_INC = 2ull << 30, OS_COUNT = (1ull << 30) - 1;
+
+__device__ __forceinline__ void os_store(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t os_load(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <typename KT, int IPT, int DB>
+__global__ void __launch_bounds__(OS_THREADS, 3) radix_onesweep(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1,
+                                                              const unsigned long long *n_dev, int64_t n_host,
+                                                              int64_t cap, int pass, int shift, SortState *ss,
+                                                              uint64_t *look, const OsHeader *hdr) {
+    pdl_wait();
+    pdl_launch();
+    if (!ss->pass_do[pass]) return;
+    constexpr int TILE_ITEMS = OS_THREADS * IPT;
+    extern __shared__ __align__(16) unsigned char os_smem[];
+    KT *skey = reinterpret_cast<KT *>(os_smem);
+    uint32_t *sval = reinterpret_cast<uint32_t *>(os_smem + sizeof(KT) * TILE_ITEMS);
+    __shared__ uint32_t wh[OS_WARPS][RADIX];
+    __shared__ uint32_t loc[RADIX], gofs[RADIX], wt[8];
+    __shared__ int s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t n = dev_count(n_dev, n_host, cap);
+    const int64_t ntiles = (n + TILE_ITEMS - 1) / TILE_ITEMS;
+    if (tid == 0) s_tile = (int)atomicAdd(&ss->tile_ctr[pass], 1u);
+    for (int e = lane; e < RADIX; e += 32) wh[warp][e] = 0;
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= ntiles) return;
+    const uint64_t epoch = (uint64_t)hdr->epoch << 32;
+    const int in = ss->pass_in[pass];
+    const KT *kin = in ? k1 : k0;
+    KT *kout = in ? k0 : k1;
+    const uint32_t *vin = in ? v1 : v0;
+    uint32_t *vout = in ? v0 : v1;
+    const int64_t base = tile * TILE_ITEMS;
+    const int tile_n = (int)(n - base < TILE_ITEMS ? n - base : TILE_ITEMS);
+    const int64_t seg = base + (int64_t)warp * 32 * IPT;
+    const uint32_t dtot = ss->ghist[pass][tid];
+
+    KT k[IPT];
+    uint32_t val[IPT];
+    uint32_t dr[IPT];  // digit (bits 16..24, RADIX = invalid) | rank within the warp's digit (bits 0..15)
+#pragma unroll
+    for (int it = 0; it < IPT; it++) {
+        const int64_t idx = seg + it * 32 + lane;
+        const bool valid = idx < n;
+        k[it] = valid ? kin[idx] : (KT)0;
+        val[it] = valid ? vin[idx] : 0u;
+    }
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int it = 0; it < IPT; it++) {
+        const bool valid = seg + it * 32 + lane < n;
+        const int d = valid ? (int)((k[it] >> shift) & ((1u << DB) - 1u)) : RADIX;
+        const unsigned peers = warp_peers<DB>(d);
+        uint32_t b = 0;
+        if (d < RADIX) b = wh[warp][d];
+        __syncwarp();
+        if (d < RADIX && lane == (int)(__ffs(peers) - 1)) wh[warp][d] = b + __popc(peers);
+        __syncwarp();
+        dr[it] = ((uint32_t)d << 16) | (b + __popc(peers & lt));
+    }
+    __syncthreads();
+    const int d = tid;
+    uint32_t total = 0;
+#pragma unroll
+    for (int w = 0; w < OS_WARPS; w++) {
+        const uint32_t v = wh[w][d];
+        wh[w][d] = total;
+        total += v;
+    }
+    // publish this tile's count of digit d, then look back for the exclusive prefix over the earlier tiles
+    uint64_t *my = look + (size_t)tile * RADIX + d;
+    if (tile == 0) {
+        os_store(my, epoch | OS_FLAG_INC | total);
+    } else {
+        os_store(my, epoch | OS_FLAG_AGG | total);
+    }
+    uint32_t excl = 0;
+    for (int64_t t = tile - 1; t >= 0;) {
+        const uint64_t v = os_load(look + (size_t)t * RADIX + d);
+        if ((v & ~(OS_COUNT | OS_FLAG_AGG | OS_FLAG_INC)) != epoch || (v & (OS_FLAG_AGG | OS_FLAG_INC)) == 0) continue;
+        excl += (uint32_t)(v & OS_COUNT);
+        if (v & OS_FLAG_INC) break;
+        t--;
+    }
+    if (tile > 0) os_store(my, epoch | OS_FLAG_INC | (excl + total));
+    const uint32_t lo = block_excl_scan256(total, wt, nullptr);  // (contains __syncthreads)
+    const uint32_t dbase = block_excl_scan256(dtot, wt, nullptr);
+    loc[d] = lo;
+    gofs[d] = dbase + excl - lo;
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < IPT; it++) {
+        const uint32_t dd = dr[it] >> 16;
+        if (dd < RADIX) {
+            const uint32_t lp = loc[dd] + wh[warp][dd] + (dr[it] & 0xffffu);
+            skey[lp] = k[it];
+            sval[lp] = val[it];
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < tile_n; i += OS_THREADS) {
+        const KT key = skey[i];
+        const uint32_t pos = gofs[(unsigned)(key >> shift) & ((1u << DB) - 1u)] + (uint32_t)i;
+        kout[pos] = key;
+        vout[pos] = sval[i];
+    }
+}
+
 template <typename KT, int IPT>
 constexpr int downsweep_smem() {
     return (int)((sizeof(KT) + sizeof(uint32_t)) * OS_THREADS * IPT);
@@ -475,11 +608,47 @@ cudaError_t launch_radix_pass_db(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, con
     return e;
 }
 
+#ifndef TCGS_ONESWEEP
+#define TCGS_ONESWEEP 0  // 1: single-kernel passes with decoupled look-back (measured slower, r2f: 276 vs 251 us)
+#endif
+
+template <typename KT, int IPT, int DB>
+cudaError_t launch_onesweep_db(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const unsigned long long *n_dev,
+                               int64_t n_host, int64_t cap, int pass, int shift, SortState *ss, uint64_t *look_all,
+                               const OsHeader *hdr, cudaStream_t st) {
+    static bool configured_dev[TCGS_MAX_DEVICES] = {};
+    bool &configured = configured_dev[current_device()];
+    constexpr int smem = downsweep_smem<KT, IPT>();
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(radix_onesweep<KT, IPT, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(radix_onesweep<KT, IPT, DB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int64_t tiles = div_up(n_dev ? cap : n_host, OS_THREADS * IPT);
+    const unsigned grid = (unsigned)(tiles > 0 ? tiles : 1);
+    uint64_t *look = look_all + (int64_t)pass * RADIX * tiles;
+    return launch_k(radix_onesweep<KT, IPT, DB>, grid, OS_THREADS, (size_t)smem, st, k0, k1, v0, v1, n_dev, n_host, cap,
+                    pass, shift, ss, look, hdr);
+}
+
 // One pass on digit bits [shift, shift + db) (db <= RADIX_BITS): fewer digit bits, fewer warp ballots.
 template <typename KT, int IPT>
 cudaError_t launch_radix_pass(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const unsigned long long *n_dev,
                               int64_t n_host, int64_t cap, int pass, int shift, int db, SortState *ss,
-                              uint32_t *table_all, cudaStream_t st) {
+                              uint32_t *table_all, const OsHeader *hdr, cudaStream_t st) {
+    if (TCGS_ONESWEEP) {
+        uint64_t *look = reinterpret_cast<uint64_t *>(table_all);
+        switch (db) {
+            case 5: return launch_onesweep_db<KT, IPT, 5>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, look, hdr, st);
+            case 6: return launch_onesweep_db<KT, IPT, 6>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, look, hdr, st);
+            case 7: return launch_onesweep_db<KT, IPT, 7>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, look, hdr, st);
+            default: return launch_onesweep_db<KT, IPT, 8>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, look, hdr, st);
+        }
+    }
     switch (db) {
         case 5: return launch_radix_pass_db<KT, IPT, 5>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st);
         case 6: return launch_radix_pass_db<KT, IPT, 6>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st);
@@ -618,11 +787,15 @@ __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx
 }
 
 __global__ void __launch_bounds__(256) bin_init(uint4 *zero, int64_t n16, uint2 *ranges, int64_t n_ranges,
-                                                DevCounters *ctr) {
+                                                DevCounters *ctr, const OsHeader *hdr, uint4 *look, int64_t look16) {
     pdl_wait();
     pdl_launch();
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = t; i < n16; i += step) zero[i] = make_uint4(0u, 0u, 0u, 0u);
+    // a fresh workspace: clear the onesweep look-back tables once (depth_fix_hist then stamps the header; nothing
+    // here writes it, so every CTA sees the same answer)
+    if (hdr->magic != OS_MAGIC)
+        for (int64_t i = t; i < look16; i += step) look[i] = make_uint4(0u, 0u, 0u, 0u);
     for (int64_t i = t; i < n_ranges; i += step) ranges[i] = make_uint2(0u, 0u);
     if (t == 0) {
         ctr->n_splats = 0ull;
@@ -642,9 +815,16 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                                                               const unsigned long long *tmask, int64_t P,
                                                               const unsigned long long *blockoff, int tiles_x,
                                                               int band_y0, int band_y1, int64_t cap, KT *tkey,
-                                                              uint32_t *tval) {
+                                                              uint32_t *tval, SortState *ss_tile, int npass) {
     pdl_wait();
     pdl_launch();
+    // digit histograms of the tile-key radix passes (the onesweep passes' digit totals), per CTA then global
+    __shared__ uint32_t dhist[TILE_MAX_PASSES][RADIX];
+    for (int e = threadIdx.x; e < TILE_MAX_PASSES * RADIX; e += DUP_THREADS) (&dhist[0][0])[e] = 0u;
+    __syncthreads();
+    auto count_key = [&](uint32_t key) {
+        for (int p = 0; p < npass; p++) atomicAdd(&dhist[p][(key >> (RADIX_BITS * p)) & (RADIX - 1)], 1u);
+    };
     __shared__ uint32_t incl[DUP_THREADS];
     __shared__ uint32_t gid[DUP_THREADS];
     __shared__ short4 rc[DUP_THREADS];
@@ -745,8 +925,10 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
             for (uint32_t s2 = tid; s2 < total; s2 += DUP_THREADS) {
                 const unsigned long long pos = base + s2;
                 if (pos < (unsigned long long)cap) {
-                    tkey[pos] = skey[s2];
+                    const KT key = skey[s2];
+                    tkey[pos] = key;
                     tval[pos] = sval[s2];
+                    count_key((uint32_t)key);
                 }
             }
         } else {  // a round with huge rectangles: search-based expansion straight to global memory
@@ -791,11 +973,16 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                 if (pos < (unsigned long long)cap) {
                     tkey[pos] = (KT)key;
                     tval[pos] = gid[lo];
+                    count_key(key);
                 }
             }
         }
         base += total;
         __syncthreads();
+    }
+    for (int e = threadIdx.x; e < npass * RADIX; e += DUP_THREADS) {
+        const uint32_t c = (&dhist[0][0])[e];
+        if (c) atomicAdd(&(&ss_tile->ghist[0][0])[e], c);
     }
 }
 
@@ -927,7 +1114,7 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
         (const uint32_t *)at<uint32_t>(ws, L.idx[0]), (const uint32_t *)at<uint32_t>(ws, L.idx[1]),
         (const DevCounters *)ctr, (const short4 *)at<short4>(ws, L.rect), (const Rec *)at<Rec>(ws, L.rec),
         (const unsigned long long *)at<unsigned long long>(ws, L.tmask), P, (const unsigned long long *)blocksum,
-        band.tiles_x, band.y0, band.y1, cap, tk0, tv0);
+        band.tiles_x, band.y0, band.y1, cap, tk0, tv0, ss_tile, npass);
     if (e0 != cudaSuccess) return e0;
     // K5
     // the key's bits split as evenly as possible over the passes (13 bits: 7 + 6, not 8 + 5)
@@ -935,7 +1122,8 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     for (int p = 0, shift = 0; p < npass; p++) {
         const int db = std::min(db0, bits - shift);
         cudaError_t e = launch_radix_pass<KT, TILEKEY_IPT>(tk0, tk1, tv0, tv1, &ctr->n_splats, 0, cap, p, shift, db,
-                                                          ss_tile, at<uint32_t>(ws, L.lb_tile), st);
+                                                          ss_tile, at<uint32_t>(ws, L.lb_tile),
+                                                          at<OsHeader>(ws, L.os_hdr), st);
         shift += db;
         if (e != cudaSuccess) return e;
     }
@@ -968,9 +1156,12 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
     SortState *ss_depth = at<SortState>(ws, L.sort_state[0]);
     // one kernel clears the sort state, the tile ranges and the per-binning counters (K1's dropped /
     // n_visible / key_min / key_max stay)
-    cudaError_t e = launch_k(bin_init, 64, 256, 0, st, reinterpret_cast<uint4 *>(static_cast<char *>(ws) + L.zero_begin),
+    cudaError_t e = launch_k(bin_init, 2 * 148, 256, 0, st,
+                             reinterpret_cast<uint4 *>(static_cast<char *>(ws) + L.zero_begin),
                              (int64_t)(L.zero_bytes / sizeof(uint4)), at<uint2>(ws, L.ranges),
-                             (int64_t)(band.n_tiles() ? band.n_tiles() : 1), ctr);
+                             (int64_t)(band.n_tiles() ? band.n_tiles() : 1), ctr, (const OsHeader *)at<OsHeader>(ws, L.os_hdr),
+                             reinterpret_cast<uint4 *>(static_cast<char *>(ws) + L.lb_depth),
+                             (int64_t)(L.lb_bytes / sizeof(uint4)));
     if (e != cudaSuccess) return e;
     uint32_t *k0 = at<uint32_t>(ws, L.key64[0]);
     uint32_t *k1 = at<uint32_t>(ws, L.key64[1]);
@@ -979,12 +1170,12 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
     if (P > 0) {
         // K2: 24-bit depth-prefix radix sort + exact float64 fix-up of equal prefixes
         const unsigned long long *src = at<unsigned long long>(ws, L.key_src);
-        e = launch_k(depth_fix_hist, 2 * 148, 256, 0, st, src, k0, i0, P, ctr, ss_depth);
+        e = launch_k(depth_fix_hist, 2 * 148, 256, 0, st, src, k0, i0, P, ctr, ss_depth, at<OsHeader>(ws, L.os_hdr));
         if (e != cudaSuccess) return e;
         for (int p = 0; p < DEPTH_PASSES; p++) {
             e = launch_radix_pass<uint32_t, DEPTH_IPT>(k0, k1, i0, i1, nullptr, P, P, p, RADIX_BITS * p, RADIX_BITS,
-                                                       ss_depth,
-                                                      at<uint32_t>(ws, L.lb_depth), st);
+                                                       ss_depth, at<uint32_t>(ws, L.lb_depth),
+                                                       at<OsHeader>(ws, L.os_hdr), st);
             if (e != cudaSuccess) return e;
         }
         e = launch_k(depth_fixup, (unsigned)std::min<int64_t>(div_up(P, 256), 8 * 148), 256, 0, st,

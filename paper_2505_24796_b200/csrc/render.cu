@@ -122,6 +122,9 @@ __device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t coun
 #ifndef TCGS_K7_WAIT
 #define TCGS_K7_WAIT 0
 #endif
+#ifndef TCGS_K7_LOOKAHEAD
+#define TCGS_K7_LOOKAHEAD 1  // producer chunks of cursor / list ids prefetched ahead of the one being gathered
+#endif
 #ifdef TCGS_K7_TIMING  // experiment builds: cycles spent waiting, per barrier kind (tcgs_k7_timing reads them)
 __device__ unsigned long long g_k7_wait[8];
 #define K7_TWAIT(kind, call)                                        \
@@ -267,6 +270,9 @@ __device__ __forceinline__ float f32(__half x) { return __half2float(x); }
 
 // One B-operand row (16 fp16, as two uint4) for MODE: hi/lo split (0) or the paper's K8 vector (1).
 // U row: [1, 1, 1, ux, uy, ux^2, ux uy, uy^2, ux, uy, ux^2, ux uy, uy^2, 1, 0, 0]
+#ifndef TCGS_K7_VROW2
+#define TCGS_K7_VROW2 0
+#endif
 template <int MODE>
 __device__ __forceinline__ void make_vrow(const float v[6], uint4 &lo8, uint4 &hi8) {
     __align__(16) __half e[16];
@@ -279,6 +285,26 @@ __device__ __forceinline__ void make_vrow(const float v[6], uint4 &lo8, uint4 &h
         for (int i = 1; i <= 5; i++) e[2 + i] = h16(v[i]);
 #pragma unroll
         for (int k = 8; k < 16; k++) e[k] = h16(0.0f);
+    } else if (TCGS_K7_VROW2) {  // the same hi/lo vector with paired conversions (cvt.rn.f16x2.f32)
+        const __half2 h12 = __floats2half2_rn(v[1], v[2]), h34 = __floats2half2_rn(v[3], v[4]);
+        const __half2 h50 = __floats2half2_rn(v[5], v[0]);
+        const float2 f12 = __half22float2(h12), f34 = __half22float2(h34), f50 = __half22float2(h50);
+        const __half2 l12 = __floats2half2_rn(v[1] - f12.x, v[2] - f12.y);
+        const __half2 l34 = __floats2half2_rn(v[3] - f34.x, v[4] - f34.y);
+        const float r1 = v[0] - f50.y;
+        const __half2 l5b = __floats2half2_rn(v[5] - f50.x, r1);  // (lo of v5, second piece of v0)
+        const float r2 = r1 - __high2float(l5b);
+        const __half c = h16(r2);
+        const __half d = h16(r2 - f32(c));
+        const __half2 w[8] = {__halves2half2(__high2half(h50), __high2half(l5b)), __halves2half2(c, __low2half(h12)),
+                              __halves2half2(__high2half(h12), __low2half(h34)),
+                              __halves2half2(__high2half(h34), __low2half(h50)), l12, l34,
+                              __halves2half2(__low2half(l5b), d), __floats2half2_rn(0.0f, 0.0f)};
+        lo8 = make_uint4(*reinterpret_cast<const uint32_t *>(&w[0]), *reinterpret_cast<const uint32_t *>(&w[1]),
+                         *reinterpret_cast<const uint32_t *>(&w[2]), *reinterpret_cast<const uint32_t *>(&w[3]));
+        hi8 = make_uint4(*reinterpret_cast<const uint32_t *>(&w[4]), *reinterpret_cast<const uint32_t *>(&w[5]),
+                         *reinterpret_cast<const uint32_t *>(&w[6]), *reinterpret_cast<const uint32_t *>(&w[7]));
+        return;
     } else {  // hi/lo: v0 = a + b + c + d (four fp16 pieces), v1..v5 = hi + lo
         const __half a = h16(v[0]);
         const float r1 = v[0] - f32(a);
@@ -430,17 +456,34 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
         if (cur.c * 32 + lane < cur.n) rc = a.rec[id0];
     }
     uint32_t id_nxt = list_id(nxt);
+#if TCGS_K7_LOOKAHEAD >= 2
+    // one more owned chunk of cursor and ids in flight: the tile-queue fetch and the range / id loads of a tile
+    // transition get two producer iterations of latency budget
+    Cursor nxa = nxt;
+    for (int i = 0; i < NP; i++) cursor_next<DYN>(nxa, a, sm);
+    uint32_t id_nxa = list_id(nxa);
+#endif
 
     for (int m = 0;; m++) {
         const bool end = cur.tile >= a.n_tiles;
         // past the stream: the first chunk after the last real tile carries the terminator, every other returns
         if (end && !(cur.prev_valid && cur.c == 0)) return;
         // prefetch the next owned chunk's records; its successor's ids
+#if TCGS_K7_LOOKAHEAD >= 2
+        Cursor nx3 = nxa;
+        for (int i = 0; i < NP; i++) cursor_next<DYN>(nx3, a, sm);
+        const uint32_t id_nx3 = list_id(nx3);
+        const Cursor nx2 = nxa;
+        const uint32_t id_nx2 = id_nxa;
+        Rec rn;
+        if (nxt.c * 32 + lane < nxt.n) rn = a.rec[id_nxt];
+#else
         Cursor nx2 = nxt;
         for (int i = 0; i < NP; i++) cursor_next<DYN>(nx2, a, sm);
         Rec rn;
         if (nxt.c * 32 + lane < nxt.n) rn = a.rec[id_nxt];
         const uint32_t id_nx2 = list_id(nx2);
+#endif
 
         // evaluate this chunk (registers only)
 #ifdef TCGS_K7_SLOWPROD  // sensitivity experiment: extra dependent work per producer chunk
@@ -468,6 +511,9 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
 
         // wait for the compaction token
         if (!(p == 0 && m == 0)) K7_TWAIT(0, mbar_wait(&sm.tok[p], p == 0 ? ((m - 1) & 1) : (m & 1)));
+#ifdef TCGS_K7_TIMING
+        const long long t_tok = clock64();
+#endif
         int k = sm.c_k;
         bool open = sm.c_open != 0;
         auto acquire = [&]() {
@@ -580,12 +626,19 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
             sm.c_k = k;
             sm.c_open = open ? 1 : 0;
             mbar_arrive(&sm.tok[(p + 1) % NP]);  // release: the compaction state travels with the token
+#ifdef TCGS_K7_TIMING
+            atomicAdd(&g_k7_wait[7], (unsigned long long)(clock64() - t_tok));
+#endif
         }
         __syncwarp();
         cur = nxt;
         nxt = nx2;
         rc = rn;
         id_nxt = id_nx2;
+#if TCGS_K7_LOOKAHEAD >= 2
+        nxa = nx3;
+        id_nxa = id_nx3;
+#endif
     }
 }
 

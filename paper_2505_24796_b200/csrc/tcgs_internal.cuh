@@ -33,7 +33,7 @@ constexpr int DUP_THREADS = 256;
 constexpr int K7_PIX = TCGS_K7_PIX;              // pixels per consumer thread (1 or 2)
 constexpr int K7_CONSUMER_WARPS = 8 / K7_PIX;  // 256 pixels of a 16x16 tile
 #ifndef TCGS_K7_PRODUCERS
-#define TCGS_K7_PRODUCERS 2
+#define TCGS_K7_PRODUCERS 4  // measured: 2 -> 4 producers, C2 K7 537 -> 524 us, C5 3.96 -> 3.35 ms (r2f)
 #endif
 constexpr int K7_PRODUCERS = TCGS_K7_PRODUCERS;  // producer warps (alternate 32-entry chunks, token-ordered compaction)
 constexpr int K7_THREADS = 32 * (K7_CONSUMER_WARPS + K7_PRODUCERS);
@@ -161,7 +161,16 @@ struct SortState {
     int final_buf;
     int done_ctas;  // depth_fix_hist: CTAs finished (the last one plans the passes)
     int pad[2];
+    unsigned int tile_ctr[MAX_PASSES];  // onesweep passes: next radix tile to claim (launch order = look-back order)
 };
+
+// Onesweep look-back tables (one u64 per (radix tile, digit) and pass): epoch (32) | flag (2) | count (30).  The
+// epoch of the current binning makes the previous frames' entries invalid without clearing the table; the header
+// holds the epoch and a magic word whose absence (a fresh workspace) makes bin_init clear the tables once.
+struct OsHeader {
+    unsigned int magic, epoch;
+};
+constexpr unsigned int OS_MAGIC = 0x7c65a1e3u;
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -169,7 +178,7 @@ inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 struct Layout {
     size_t counters, sort_state[2], rec, tmask, rect, key_src, key64[2], long_runs, fix_scratch, idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
-    size_t blocksum, lb_depth, lb_tile, tkey[2], tval[2], ranges, total;
+    size_t blocksum, lb_depth, lb_tile, lb_bytes, os_hdr, tkey[2], tval[2], ranges, total;
     size_t zero_begin, zero_bytes;  // sort state, cleared at the start of every binning
     static Layout make(int64_t P, int W, int H, int64_t cap) {
         Layout L;
@@ -182,9 +191,11 @@ struct Layout {
         L.sort_state[0] = take(sizeof(SortState));
         L.sort_state[1] = take(sizeof(SortState));
         L.zero_bytes = o - L.zero_begin;
-        // per-pass [digit][tile] count tables of the radix passes
-        L.lb_depth = take(sizeof(uint32_t) * RADIX * MAX_PASSES * (size_t)div_up((int64_t)Pn, OS_THREADS * DEPTH_IPT));
-        L.lb_tile = take(sizeof(uint32_t) * RADIX * TILE_MAX_PASSES * (size_t)div_up((int64_t)cn, OS_THREADS * TILEKEY_IPT));
+        // per-pass [digit][tile] count tables of the radix passes (u64 entries: the onesweep look-back)
+        L.os_hdr = take(sizeof(OsHeader));
+        L.lb_depth = take(sizeof(uint64_t) * RADIX * MAX_PASSES * (size_t)div_up((int64_t)Pn, OS_THREADS * DEPTH_IPT));
+        L.lb_tile = take(sizeof(uint64_t) * RADIX * TILE_MAX_PASSES * (size_t)div_up((int64_t)cn, OS_THREADS * TILEKEY_IPT));
+        L.lb_bytes = o - L.lb_depth;
         L.rec = take(sizeof(Rec) * Pn);
         L.tmask = take(sizeof(uint64_t) * Pn);  // exact coverage: tile masks in depth order (K3 -> K4)
         L.rect = take(sizeof(short4) * Pn);

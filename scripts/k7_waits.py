@@ -32,3 +32,5 @@ for i in range(5):
     tot = v[5] if i < 3 else v[6]
     print(f"{names[i]:18s} {v[i] / n:14.4g} cycles  {100 * v[i] / max(tot, 1):5.1f}% of the role's warp-time")
 print(f"{'prod total':18s} {v[5] / n:14.4g}   {'cons total':12s} {v[6] / n:14.4g}")
+print(f"token held (serial compaction) {v[7] / n:14.4g} cycles summed over CTAs = "
+      f"{100 * v[7] / max(v[5] / 4, 1):5.1f}% of one producer's time")

@@ -315,8 +315,8 @@ class Renderer:
         o.schedule = self.schedule
         return o
 
-    def workspace(self, P: int, W: int, H: int, cap: int) -> torch.Tensor:
-        need = int(self.lib.tcgs_workspace_size(P, W, H, cap))
+    def workspace(self, P: int, W: int, H: int, cap: int, min_bytes: int = 0) -> torch.Tensor:
+        need = max(int(self.lib.tcgs_workspace_size(P, W, H, cap)), int(min_bytes))
         if self.ws is None or self.ws.numel() < need:
             self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         self.ws_key = (P, W, H, cap)
@@ -577,10 +577,12 @@ class ViewRenderer:
         ss = [self.streams[i] for i in idx]
         cs = [camera_struct(c) for c in cams]
         cap = max(r.capacity(cloud.P) for r in rs)  # one workspace layout for the whole pass
+        # the pass checks every view against ONE ws_bytes: grow each workspace to the largest view's need
+        need = max(int(self.lib.tcgs_workspace_size(cloud.P, c.width, c.height, cap)) for c in cs)
         wss = []
         for r, c in zip(rs, cs):
             r.max_splats = cap
-            wss.append(r.workspace(cloud.P, c.width, c.height, cap))
+            wss.append(r.workspace(cloud.P, c.width, c.height, cap, min_bytes=need))
         ps = ss[0]  # the fused K1 runs on the first view's stream, after every view's previous frame
         ps.wait_stream(torch.cuda.current_stream(self.device))
         for s in ss[1:]:

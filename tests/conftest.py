@@ -19,7 +19,11 @@ def pytest_configure(config):
 
 def load_golden(name):
     with np.load(os.path.join(GOLDEN_DIR, f"{name}.npz")) as z:
-        return {k: z[k] for k in z.files}
+        g = {k: z[k] for k in z.files}
+    for k in ("rgb", "T"):  # large frames store the image as 16-bit fixed point (make_golden.py)
+        if k + "_q16" in g:
+            g[k] = g.pop(k + "_q16").astype(np.float64) / 65535.0
+    return g
 
 
 class GoldenCam:

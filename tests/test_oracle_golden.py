@@ -48,5 +48,6 @@ def test_oracle_render_matches_reference(golden):
     assert fr.stats.exp_calls == st[3]
     assert fr.stats.n_splats == st[4] and fr.stats.pixels_terminated == st[6]
     assert np.array_equal(fr.n_contrib, g["counts"])
-    assert np.max(np.abs(fr.rgb - g["rgb"])) <= 1e-12
-    assert np.max(np.abs(fr.T - g["T"])) <= 1e-12
+    tol = float(g.get("img_tol", 1e-12))  # float32-stored large frames: within the float32 rounding
+    assert np.max(np.abs(fr.rgb - g["rgb"].astype(np.float64))) <= tol
+    assert np.max(np.abs(fr.T - g["T"].astype(np.float64))) <= tol

@@ -73,6 +73,12 @@ constexpr int FL_ECOFF = 1;
 constexpr int FL_DUMP = 2;
 constexpr float ALPHA_CUT = 1.0f / 255.0f;  // src/tilesplat/raster.py:15
 
+// A pixel that terminates at stage column j gets the pass threshold term_code(j) = 2^100 (1 + j/64): no beta can
+// reach it (|beta| <= 16 * 65504^2 for finite fp16 operands), so one FSEL both retires the pixel and records j.
+constexpr float TERM_CODE0 = 1.2676506002282294e30f;  // 2^100
+__device__ __forceinline__ constexpr float term_code(int j) { return TERM_CODE0 * (1.0f + (float)j / 64.0f); }
+__device__ __forceinline__ int term_col(float code) { return (int)((code * 7.888609052210118e-31f - 1.0f) * 64.0f); }
+
 struct StageMeta {
     int tile;        // -1: no more tiles
     int seq;         // CTA-local tile sequence number
@@ -845,7 +851,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                             if (col < nl && inside[h]) {
                                 const size_t o = (size_t)e * 256 + (size_t)(ly[h] * TILE + lx[h]);
                                 a.dump_beta[o] = __uint_as_float(rb[h]);
-                                if (thr[h] != INF) {  // reached: classify as the blend below does
+                                if (thr[h] < TERM_CODE0) {  // reached: classify as the blend below does
                                     const float al = ex2_approx(__uint_as_float(rb[h]));
                                     a.dump_class[o] = !p[h] ? 1 : (fmaf(-al, T[h], T[h]) < TERM_T ? 3 : 2);
                                 }
@@ -859,21 +865,24 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                         const float4 cc = sm.col[st][col];
 #pragma unroll
                         for (int h = 0; h < NPIX; h++) {
-                            // alpha = 2^beta' (no min(alpha, 1): alpha > 1 only by rounding, and then
-                            // T - alpha T < 1e-4 terminates exactly as alpha = 1 would)
-                            const float al = EC ? ex2_approx(__uint_as_float(rb[h])) : alv[h];
+                            // alpha = 2^beta' for a passing lane, exactly 0 otherwise (ex2(-inf) = +0), so a
+                            // non-passing lane's update below is the identity: T - 0 T = T >= 1e-4 never
+                            // terminates, C + 0 c = C.  (No min(alpha, 1): alpha > 1 only by rounding, and then
+                            // T - alpha T < 1e-4 terminates exactly as alpha = 1 would.)
+                            const float al = EC ? ex2_approx(p[h] ? __uint_as_float(rb[h]) : -INF)
+                                                : (p[h] ? alv[h] : 0.0f);
                             const float tn = fmaf(-al, T[h], T[h]);
-                            if (p[h] && tn < TERM_T) {  // termination precedes compositing
-                                jt[h] = col;
-                                thr[h] = __int_as_float(0x7f800000);
-                            }
-                            if (p[h] && tn >= TERM_T) {
+                            if (p[h]) fcnt[h] += 1.0f;  // passes; the terminating one is taken back per stage
+                            const bool tm = tn < TERM_T;  // termination precedes compositing
+                            // a terminated pixel never passes again, and its threshold records the column
+                            asm("{\n.reg .pred q;\nsetp.lt.f32 q, %1, %2;\n@q mov.f32 %0, %3;\n}"
+                                : "+f"(thr[h]) : "f"(tn), "f"(TERM_T), "f"(term_code(col)));
+                            if (!tm) {
                                 const float w = al * T[h];
                                 c0[h] = fmaf(w, cc.x, c0[h]);
                                 c1[h] = fmaf(w, cc.y, c1[h]);
                                 c2[h] = fmaf(w, cc.z, c2[h]);
                                 T[h] = tn;
-                                fcnt[h] += 1.0f;
                             }
                         }
                     }
@@ -927,7 +936,12 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 bool all_done = true;
 #pragma unroll
                 for (int h = 0; h < NPIX; h++) {
-                    const bool tstage = jt[h] < K7_BATCH;
+                    // terminated in this stage: thr holds term_code(column) (done lanes entered with +inf)
+                    const bool tstage = thr[h] >= TERM_CODE0 && thr[h] != INF;
+                    if (tstage) {
+                        jt[h] = term_col(thr[h]);
+                        fcnt[h] -= 1.0f;  // the terminating pass was counted
+                    }
                     term[h] = term[h] || tstage;
                     done[h] = done[h] || tstage;
                     all_done = all_done && done[h];

@@ -33,8 +33,9 @@
 //     (T - alpha T < 1e-4, src/tilesplat/raster.py:136-145), C += alpha T c,
 //     T -= alpha T.  A warp whose pixels have all terminated stops working; when
 //     all 8 have, the producers retire the tile.
-// Stages (4) and TMEM buffers (2) are ring buffers guarded by full/empty and
-// mma_done/tmem_empty mbarriers, so gathers, MMAs and blending overlap.
+// Stages (4) and TMEM buffers (2) are ring buffers: a consumer waits on one mbarrier per stage (mma_done: the
+// producer's arrival with the stage rows + the MMA commit) and releases the stage with one arrival (released,
+// which also frees the TMEM buffer NB stages later), so gathers, MMAs and blending overlap.
 #include "tcgs_internal.cuh"
 
 namespace tcgs {
@@ -98,7 +99,10 @@ struct __align__(1024) K7Smem {
     uint32_t pos[S][K7_BATCH];          // FL_DUMP: tile-list index of each live row
     __half Ug[S][2][128 * 16];          // TC_K8_GLOBAL: per-stage A operands (global pixel coordinates)
     StageMeta meta[S];
-    unsigned long long full[S], empty[S], mma_done[NB], tmem_empty[NB], tok[K7_PRODUCERS];
+    // full: stage data ready (FFMA mode; with tensor cores mma_done[b] also carries the producer's arrival, so
+    // consumers wait on one barrier); released: every consumer warp is done with a stage (its shared-memory
+    // rows, and -- NB stages later -- its TMEM buffer)
+    unsigned long long full[S], released[S], mma_done[NB], tok[K7_PRODUCERS];
     uint32_t tmem_base;
     int retire[8];
     int c_fill, c_k, c_open;  // compaction state: touched only by the producer holding the token
@@ -171,6 +175,39 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t pari
             : "memory");
         if (ok) break;
         __nanosleep(TCGS_K7_WAIT);
+    }
+#endif
+}
+__device__ __forceinline__ void mbar_arrive_n(unsigned long long *bar, uint32_t n) {
+    asm volatile(
+        "{\n"
+        ".reg .b64 st;\n"
+        "mbarrier.arrive.shared::cta.b64 st, [%0], %1;\n"
+        "}\n" ::"r"(smem_u32(bar)), "r"(n)
+        : "memory");
+}
+#ifndef TCGS_K7_PRODWAIT
+#define TCGS_K7_PRODWAIT 0  // producer waits: 0 = suspend hint (as the consumers), N > 0 = try_wait + N ns backoff
+#endif
+// Producers run ahead of the consumers and mostly wait for a stage to be released: optionally back off with a
+// plain nanosleep so the waiting warps leave issue slots to the consumers.
+__device__ __forceinline__ void mbar_wait_prod(unsigned long long *bar, uint32_t parity) {
+#if TCGS_K7_PRODWAIT == 0
+    mbar_wait(bar, parity);
+#else
+    uint32_t ok;
+    for (;;) {
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P1;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) break;
+        __nanosleep(TCGS_K7_PRODWAIT);
     }
 #endif
 }
@@ -524,7 +561,7 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
         bool open = sm.c_open != 0;
         auto acquire = [&]() {
             if (!open) {
-                K7_TWAIT(1, mbar_wait(&sm.empty[k % S], ((k / S) & 1) ^ 1));
+                K7_TWAIT(1, mbar_wait_prod(&sm.released[k % S], ((k / S) & 1) ^ 1));
                 open = true;
             }
         };
@@ -555,17 +592,24 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
                 mt.dead_total = dead_total;
                 mt.n_total = n_total;
                 sm.meta[st] = mt;
-                mbar_arrive(&sm.full[st]);
-                if (TC && tile >= 0) {
+                if (!TC) {
+                    mbar_arrive(&sm.full[st]);
+                } else {
+                    // TMEM buffer b was last read by the consumers of stage k - NB
                     const int b = k % NB;
-                    K7_TWAIT(2, mbar_wait(&sm.tmem_empty[b], ((k / NB) & 1) ^ 1));
-                    tc_fence_after();
-                    const uint64_t bdesc = umma_desc(sm.V[st]);
+                    if (k >= NB) K7_TWAIT(2, mbar_wait_prod(&sm.released[(k - NB) % S], ((k - NB) / S) & 1));
+                    if (tile >= 0) {
+                        mbar_arrive(&sm.mma_done[b]);  // the stage's rows and meta (release); the commit is the 2nd
+                        tc_fence_after();
+                        const uint64_t bdesc = umma_desc(sm.V[st]);
 #pragma unroll
-                    for (int h = 0; h < 2; h++)
-                        mma_f16(tmem + b * (2 * K7_BATCH) + h * K7_BATCH, umma_desc(GLOBAL ? sm.Ug[st][h] : sm.U[h]),
-                                bdesc, IDESC);
-                    mma_commit(&sm.mma_done[b]);
+                        for (int h = 0; h < 2; h++)
+                            mma_f16(tmem + b * (2 * K7_BATCH) + h * K7_BATCH,
+                                    umma_desc(GLOBAL ? sm.Ug[st][h] : sm.U[h]), bdesc, IDESC);
+                        mma_commit(&sm.mma_done[b]);
+                    } else {
+                        mbar_arrive_n(&sm.mma_done[b], 2);  // end of stream: no MMA
+                    }
                 }
             }
             __syncwarp();
@@ -693,12 +737,9 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
     if (tid == 0) {
         for (int s = 0; s < S; s++) {
             mbar_init(&sm.full[s], 1);
-            mbar_init(&sm.empty[s], K7_CONSUMER_WARPS);
+            mbar_init(&sm.released[s], K7_CONSUMER_WARPS);
         }
-        for (int b = 0; b < NB; b++) {
-            mbar_init(&sm.mma_done[b], 1);
-            mbar_init(&sm.tmem_empty[b], K7_CONSUMER_WARPS);
-        }
+        for (int b = 0; b < NB; b++) mbar_init(&sm.mma_done[b], 2);  // producer arrive + MMA commit
         for (int q = 0; q < K7_PRODUCERS; q++) mbar_init(&sm.tok[q], 1);
         sm.c_fill = 0;
         sm.c_k = 0;
@@ -733,7 +774,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
         int px[NPIX], py[NPIX];
         bool inside[NPIX], done[NPIX], term[NPIX];
         float T[NPIX], c0[NPIX], c1[NPIX], c2[NPIX];
-        uint32_t cull[NPIX];
+        uint32_t cull[NPIX];    // EarlyCull culls of dead (box-culled) Gaussians the pixel reached
+        uint32_t reached[NPIX];  // live list entries the pixel reached (culls = reached - blends + cull)
         float fcnt[NPIX];  // blends of this pixel (exact in fp32; kept on the FMA pipe)
         bool warp_done = true;
         uint32_t n_total = 0;
@@ -744,7 +786,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
             done[h] = true;
             T[h] = 1.0f;
             c0[h] = c1[h] = c2[h] = fcnt[h] = 0.0f;
-            cull[h] = 0;
+            cull[h] = reached[h] = 0;
         }
 #ifdef TCGS_K7_PROFILE  // experiment builds only: per-warp work (stages entered, relevant columns) replaces T / n_contrib
         int prof_rel = 0, prof_st = 0;
@@ -766,16 +808,23 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                     s_pairs += n_total;
                 }
                 s_blend += (uint32_t)fcnt[h];
-                s_cull += cull[h];
+                s_cull += cull[h] + reached[h] - (uint32_t)fcnt[h];
                 s_term += term[h] ? 1u : 0u;
             }
 #ifdef TCGS_K7_PROFILE
             prof_rel = prof_st = 0;
 #endif
         };
+        static_assert(NB >= 2 && S % NB == 0, "K7 stage / TMEM rings");
         for (int k = 0;; k++) {
             const int st = k % S, b = k % NB;
-            K7_TWAIT(3, mbar_wait(&sm.full[st], (k / S) & 1));
+            // tensor cores: mma_done[b] completes on the producer's arrival (stage rows, meta) AND the MMA commit
+            if (TC) {
+                K7_TWAIT(4, mbar_wait(&sm.mma_done[b], (k / NB) & 1));
+                tc_fence_after();
+            } else {
+                K7_TWAIT(3, mbar_wait(&sm.full[st], (k / S) & 1));
+            }
             const StageMeta m = sm.meta[st];
             if (m.seq != cur_seq || m.tile < 0) {
                 if (cur_seq >= 0) flush();
@@ -794,36 +843,27 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                     term[h] = false;
                     T[h] = 1.0f;
                     c0[h] = c1[h] = c2[h] = 0.0f;
-                    cull[h] = 0;
+                    cull[h] = reached[h] = 0;
                     fcnt[h] = 0.0f;
                 }
                 n_total = m.n_total;
                 warp_done = __all_sync(FULL, all_done);
                 if (warp_done && lane == 0) atomicAdd(&sm.retire[cur_seq & 7], 1);
             }
-            if (TC) {
-                K7_TWAIT(4, mbar_wait(&sm.mma_done[b], (k / NB) & 1));
-                tc_fence_after();
-            }
-            bool tmem_released = false;
             if (!warp_done) {
 #ifdef TCGS_K7_PROFILE
                 prof_st++;
 #endif
                 const int nl = m.n_live;
-                bool live0[NPIX];
-                int jt[NPIX];
-                float thr[NPIX], fcnt0[NPIX];
+                float thr[NPIX];
                 uint32_t tb[NPIX];
 #pragma unroll
                 for (int h = 0; h < NPIX; h++) {
-                    live0[h] = !done[h];
-                    jt[h] = K7_BATCH;
+                    if (!done[h]) reached[h] += (uint32_t)nl;  // (a pixel terminating here gives back the rest)
                     // pass threshold: the EarlyCull cut of beta' (EC) or the 1/255 cut of alpha (EarlyCull off)
                     // while the pixel is live, +inf once it has terminated (a float, so the test stays one FSETP
                     // and the update a predicated move)
                     thr[h] = done[h] ? INF : (EC ? CUT_LOG2 : ALPHA_CUT);
-                    fcnt0[h] = fcnt[h];
                     tb[h] = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + b * (2 * K7_BATCH) + hf[h] * K7_BATCH;
                 }
                 // one column of the stage: a pixel passes EarlyCull iff beta >= thr (thr = the cut while live,
@@ -899,12 +939,6 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                         for (int h = 0; h < NPIX; h++)
 #pragma unroll
                             for (int j = 0; j < G; j++) asm volatile("" : "+r"(r[h][j]));
-                        if (NB == 1 && hc == K7_BATCH / G - 1) {  // single accumulator: free it for the next MMA
-                            tc_fence_before();
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive(&sm.tmem_empty[b]);
-                            tmem_released = true;
-                        }
                     } else {
 #pragma unroll
                         for (int h = 0; h < NPIX; h++) {
@@ -933,26 +967,34 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                     if (z == 12345.0f) cull[0] += 1;
                 }
 #endif
-                bool all_done = true;
+                // terminated in this stage: thr holds term_code(column) (done lanes entered with +inf).  Rare (a
+                // pixel terminates once per tile), so the bookkeeping sits behind one warp vote.
+                bool tstage[NPIX], tany = false;
 #pragma unroll
                 for (int h = 0; h < NPIX; h++) {
-                    // terminated in this stage: thr holds term_code(column) (done lanes entered with +inf)
-                    const bool tstage = thr[h] >= TERM_CODE0 && thr[h] != INF;
-                    if (tstage) {
-                        jt[h] = term_col(thr[h]);
-                        fcnt[h] -= 1.0f;  // the terminating pass was counted
-                    }
-                    term[h] = term[h] || tstage;
-                    done[h] = done[h] || tstage;
-                    all_done = all_done && done[h];
-                    // EarlyCull counts: valid columns before the termination that did not blend, plus the dead
-                    // Gaussians of the list before the terminating one
-                    if (live0[h]) cull[h] += (uint32_t)(tstage ? jt[h] : nl) - (uint32_t)(fcnt[h] - fcnt0[h]);
-                    if (tstage) cull[h] += sm.dead_before[st][jt[h]];
+                    tstage[h] = thr[h] >= TERM_CODE0 && thr[h] != INF;
+                    tany = tany || tstage[h];
                 }
-                if (__all_sync(FULL, all_done)) {
-                    warp_done = true;
-                    if (lane == 0) atomicAdd(&sm.retire[cur_seq & 7], 1);
+                if (__any_sync(FULL, tany)) {
+                    bool all_done = true;
+#pragma unroll
+                    for (int h = 0; h < NPIX; h++) {
+                        if (tstage[h]) {
+                            const int jt = term_col(thr[h]);
+                            fcnt[h] -= 1.0f;  // the terminating pass was counted
+                            // reached: the live columns before the terminating one, plus the dead Gaussians
+                            // of the list before it (all culls)
+                            reached[h] -= (uint32_t)(nl - jt);
+                            cull[h] += sm.dead_before[st][jt];
+                            term[h] = true;
+                            done[h] = true;
+                        }
+                        all_done = all_done && done[h];
+                    }
+                    if (__all_sync(FULL, all_done)) {
+                        warp_done = true;
+                        if (lane == 0) atomicAdd(&sm.retire[cur_seq & 7], 1);
+                    }
                 }
             }
             if (m.last) {
@@ -960,12 +1002,9 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 for (int h = 0; h < NPIX; h++)
                     if (!done[h]) cull[h] += m.dead_total;  // list exhausted: every dead Gaussian was a cull
             }
-            if (TC && !tmem_released) tc_fence_before();
+            if (TC) tc_fence_before();
             __syncwarp();
-            if (lane == 0) {
-                if (TC && !tmem_released) mbar_arrive(&sm.tmem_empty[b]);
-                mbar_arrive(&sm.empty[st]);
-            }
+            if (lane == 0) mbar_arrive(&sm.released[st]);
         }
     }
 

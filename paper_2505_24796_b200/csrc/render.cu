@@ -70,6 +70,10 @@ struct RenderArgs {
 // cull on alpha < 1/255 afterwards (the reference's alpha_reference order, src/tilesplat/raster.py:86-94 /
 // tensor_path.py:155-160), no dead-Gaussian box test in the producer; FL_DUMP = debug dump of beta' and the
 // per-fragment classification (the a19 tolerance oracle, tests/test_gpu_beta.py).
+#ifndef TCGS_K7_EX2EARLY
+#define TCGS_K7_EX2EARLY 0
+#endif
+constexpr bool EX2EARLY = TCGS_K7_EX2EARLY != 0;
 constexpr int FL_ECOFF = 1;
 constexpr int FL_DUMP = 2;
 constexpr float ALPHA_CUT = 1.0f / 255.0f;  // src/tilesplat/raster.py:15
@@ -766,13 +770,14 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
     const uint32_t tmem = TC ? sm.tmem_base : 0u;
     const uint32_t *ids = a.ids_override ? a.ids_override : (a.ctr->tile_cur ? a.ids1 : a.ids0);
 
-    unsigned long long s_blend = 0, s_cull = 0, s_term = 0, s_pairs = 0;
+    // per-thread K8 sums in 32 bits (a thread's pixels see at most a few hundred tiles of bounded lists); widened
+    // to 64 bits in the CTA reduction
+    uint32_t s_blend = 0, s_cull = 0, s_term = 0, s_pairs = 0;
     if (warp >= K7_CONSUMER_WARPS) {
         producer<MODE, DYN, FL>(sm, a, ids, tmem, warp - K7_CONSUMER_WARPS);
     } else {
         int cur_seq = -1, cur_tile = -1;
-        int px[NPIX], py[NPIX];
-        bool inside[NPIX], done[NPIX], term[NPIX];
+        bool done[NPIX], term[NPIX];
         float T[NPIX], c0[NPIX], c1[NPIX], c2[NPIX];
         uint32_t cull[NPIX];    // EarlyCull culls of dead (box-culled) Gaussians the pixel reached
         uint32_t reached[NPIX];  // live list entries the pixel reached (culls = reached - blends + cull)
@@ -781,8 +786,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
         uint32_t n_total = 0;
 #pragma unroll
         for (int h = 0; h < NPIX; h++) {
-            px[h] = py[h] = 0;
-            inside[h] = term[h] = false;
+            term[h] = false;
             done[h] = true;
             T[h] = 1.0f;
             c0[h] = c1[h] = c2[h] = fcnt[h] = 0.0f;
@@ -791,15 +795,23 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
 #ifdef TCGS_K7_PROFILE  // experiment builds only: per-warp work (stages entered, relevant columns) replaces T / n_contrib
         int prof_rel = 0, prof_st = 0;
 #endif
+        // pixel h of this thread in tile t (recomputed where needed instead of held in registers)
+        auto pix = [&](int t, int h, int &x, int &y) {
+            x = (t % a.tiles_x) * TILE + lx[h];
+            y = (a.band_y0 + t / a.tiles_x) * TILE + ly[h];
+            return x < a.width && y < a.height;
+        };
         auto flush = [&]() {
 #pragma unroll
             for (int h = 0; h < NPIX; h++) {
+                int px, py;
+                const bool inside = pix(cur_tile, h, px, py);
 #ifdef TCGS_K7_PROFILE
                 T[h] = (float)prof_st;
                 fcnt[h] = (float)prof_rel;
 #endif
-                if (inside[h]) {
-                    const int64_t p = (int64_t)py[h] * a.width + px[h];
+                if (inside) {
+                    const int64_t p = (int64_t)py * a.width + px;
                     a.rgb[3 * p] = c0[h];
                     a.rgb[3 * p + 1] = c1[h];
                     a.rgb[3 * p + 2] = c2[h];
@@ -835,10 +847,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 bool all_done = true;
 #pragma unroll
                 for (int h = 0; h < NPIX; h++) {
-                    px[h] = tx * TILE + lx[h];
-                    py[h] = ty * TILE + ly[h];
-                    inside[h] = px[h] < a.width && py[h] < a.height;
-                    done[h] = !inside[h];
+                    done[h] = !(tx * TILE + lx[h] < a.width && ty * TILE + ly[h] < a.height);
                     all_done = all_done && done[h];
                     term[h] = false;
                     T[h] = 1.0f;
@@ -868,7 +877,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                 }
                 // one column of the stage: a pixel passes EarlyCull iff beta >= thr (thr = the cut while live,
                 // +inf once done); a warp vote skips the column when no pixel of the warp passes (uniform branch)
-                auto column = [&](const uint32_t (&rb)[NPIX], int col) {
+                auto column = [&](const uint32_t (&rb)[NPIX], const uint32_t (&ex)[NPIX], int col) {
                     bool p[NPIX], any = false;
                     float alv[NPIX];
 #pragma unroll
@@ -878,6 +887,7 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                             p[h] = bt >= thr[h];  // (columns >= n_live hold beta = -65504: never pass)
                             // fp16 global coordinates can overflow: a non-finite beta is a cull (tensor_path.py:113)
                             if (GLOBAL) p[h] = p[h] && bt < INF;
+                            if (EX2EARLY) alv[h] = __uint_as_float(ex[h]);  // exponentials issued per TMEM group
                         } else {  // EarlyCull off: the exponential of every active fragment, then the alpha cut
                             alv[h] = ex2_approx(bt);
                             p[h] = alv[h] >= thr[h];
@@ -888,7 +898,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                         const uint32_t e = sm.pos[st][col < nl ? col : 0];
 #pragma unroll
                         for (int h = 0; h < NPIX; h++) {
-                            if (col < nl && inside[h]) {
+                            int dx_, dy_;
+                            if (col < nl && pix(cur_tile, h, dx_, dy_)) {
                                 const size_t o = (size_t)e * 256 + (size_t)(ly[h] * TILE + lx[h]);
                                 a.dump_beta[o] = __uint_as_float(rb[h]);
                                 if (thr[h] < TERM_CODE0) {  // reached: classify as the blend below does
@@ -909,8 +920,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                             // non-passing lane's update below is the identity: T - 0 T = T >= 1e-4 never
                             // terminates, C + 0 c = C.  (No min(alpha, 1): alpha > 1 only by rounding, and then
                             // T - alpha T < 1e-4 terminates exactly as alpha = 1 would.)
-                            const float al = EC ? ex2_approx(p[h] ? __uint_as_float(rb[h]) : -INF)
-                                                : (p[h] ? alv[h] : 0.0f);
+                            const float al = (EC && !EX2EARLY) ? ex2_approx(p[h] ? __uint_as_float(rb[h]) : -INF)
+                                                                : (p[h] ? alv[h] : 0.0f);
                             const float tn = fmaf(-al, T[h], T[h]);
                             if (p[h]) fcnt[h] += 1.0f;  // passes; the terminating one is taken back per stage
                             const bool tm = tn < TERM_T;  // termination precedes compositing
@@ -927,7 +938,10 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                         }
                     }
                 };
-                constexpr int G = NPIX == 1 ? 16 : 8;  // columns per TMEM load group (registers: G x NPIX betas)
+#ifndef TCGS_K7_GROUP
+#define TCGS_K7_GROUP 16
+#endif
+                constexpr int G = NPIX == 1 ? TCGS_K7_GROUP : 8;  // columns per TMEM load group (G x NPIX betas)
 #pragma unroll
                 for (int hc = 0; hc < K7_BATCH / G; hc++) {
                     uint32_t r[NPIX][G];
@@ -951,12 +965,25 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                             }
                         }
                     }
+                    // TCGS_K7_EX2EARLY: the group's exponentials issued back to back ahead of the column votes, so
+                    // their latency leaves the blend chain (costs an ex2 on the columns no pixel passes)
+                    uint32_t e2[NPIX][EX2EARLY ? G : 1];
+                    if (EX2EARLY) {
+#pragma unroll
+                        for (int h = 0; h < NPIX; h++)
+#pragma unroll
+                            for (int j = 0; j < G; j++)
+                                asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=r"(e2[h][j]) : "f"(__uint_as_float(r[h][j])));
+                    }
 #pragma unroll
                     for (int j = 0; j < G; j++) {
-                        uint32_t rj[NPIX];
+                        uint32_t rj[NPIX], ej[NPIX];
 #pragma unroll
-                        for (int h = 0; h < NPIX; h++) rj[h] = r[h][j];
-                        column(rj, G * hc + j);
+                        for (int h = 0; h < NPIX; h++) {
+                            rj[h] = r[h][j];
+                            ej[h] = e2[h][EX2EARLY ? j : 0];
+                        }
+                        column(rj, ej, G * hc + j);
                     }
                 }
 #ifdef TCGS_K7_SLOWCONS  // sensitivity experiment: extra dependent work per consumer warp-stage
@@ -1016,18 +1043,19 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
     if (warp < K7_CONSUMER_WARPS) __threadfence_system();
 
     // K8: fragment statistics, one atomic per CTA and counter
+    unsigned long long w_blend = s_blend, w_cull = s_cull, w_term = s_term, w_pairs = s_pairs;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        s_blend += __shfl_xor_sync(FULL, s_blend, o);
-        s_cull += __shfl_xor_sync(FULL, s_cull, o);
-        s_term += __shfl_xor_sync(FULL, s_term, o);
-        s_pairs += __shfl_xor_sync(FULL, s_pairs, o);
+        w_blend += __shfl_xor_sync(FULL, w_blend, o);
+        w_cull += __shfl_xor_sync(FULL, w_cull, o);
+        w_term += __shfl_xor_sync(FULL, w_term, o);
+        w_pairs += __shfl_xor_sync(FULL, w_pairs, o);
     }
     if (lane == 0 && warp < K7_CONSUMER_WARPS) {
-        sm.red[warp][0] = s_blend;
-        sm.red[warp][1] = s_cull;
-        sm.red[warp][2] = s_term;
-        sm.red[warp][3] = s_pairs;
+        sm.red[warp][0] = w_blend;
+        sm.red[warp][1] = w_cull;
+        sm.red[warp][2] = w_term;
+        sm.red[warp][3] = w_pairs;
     }
     if (TC) tc_fence_before();
     __syncthreads();

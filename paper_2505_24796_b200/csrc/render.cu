@@ -94,14 +94,15 @@ struct StageMeta {
     int pad[2];
 };
 
-struct __align__(1024) K7Smem {
+template <bool GL>  // GL: the global-coordinate ablation's per-stage A operands
+struct __align__(1024) K7SmemT {
     __half U[2][128 * 16];              // A operands: pixel halves, K-major no-swizzle core matrices
     __half V[S][K7_BATCH * 16];         // B operands, one per stage
     float4 vf[S][K7_BATCH][2];          // FFMA mode: fp32 coefficients
     float4 col[S][K7_BATCH];            // colours
     uint32_t dead_before[S][K7_BATCH];  // dead Gaussians before each live one (list order)
     uint32_t pos[S][K7_BATCH];          // FL_DUMP: tile-list index of each live row
-    __half Ug[S][2][128 * 16];          // TC_K8_GLOBAL: per-stage A operands (global pixel coordinates)
+    __half Ug[GL ? S : 1][2][128 * 16];  // TC_K8_GLOBAL: per-stage A operands (global pixel coordinates)
     StageMeta meta[S];
     // full: stage data ready (FFMA mode; with tensor cores mma_done[b] also carries the producer's arrival, so
     // consumers wait on one barrier); released: every consumer warp is done with a stage (its shared-memory
@@ -394,7 +395,8 @@ constexpr uint32_t TSLOT_CLAIMED = 0xFFFFFFFFu;
 
 // Tile of the CTA's seq-th stream position (seq >= 1), fetched from the global queue by whichever producer needs
 // it first and shared through a tagged shared-memory slot: both producers walk the same stream.  Warp-uniform.
-__device__ __forceinline__ int seq_tile(K7Smem &sm, const RenderArgs &a, int seq) {
+template <class SM>
+__device__ __forceinline__ int seq_tile(SM &sm, const RenderArgs &a, int seq) {
     int t = 0;
     if ((threadIdx.x & 31) == 0) {
         unsigned long long *slot = &sm.tslot[seq & 15];
@@ -439,8 +441,8 @@ __device__ __forceinline__ void cursor_tile(Cursor &k, const RenderArgs &a) {
 // DYN (TCGS_SCHEDULE_DYNAMIC): tiles after the CTA's first come from a global queue, which balances the tail of
 // a lone frame; static (tiles blockIdx.x, +gridDim.x, ...) leaves a staggered tail that other streams' kernels fill
 // when several frames share the GPU.
-template <bool DYN>
-__device__ __forceinline__ void cursor_next(Cursor &k, const RenderArgs &a, K7Smem &sm) {
+template <bool DYN, class SM>
+__device__ __forceinline__ void cursor_next(Cursor &k, const RenderArgs &a, SM &sm) {
     if (++k.c >= k.chunks) {
         k.prev_valid = k.tile < a.n_tiles;
         k.seq++;
@@ -476,7 +478,7 @@ __device__ __forceinline__ void write_global_u(__half (*ug)[128 * 16], int tile,
 }
 
 template <int MODE, bool DYN, int FL>
-__device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, uint32_t tmem, int p) {
+__device__ void producer(K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL> &sm, const RenderArgs &a, const uint32_t *ids, uint32_t tmem, int p) {
     constexpr bool TC = MODE != TCGS_ALPHA_FFMA;
     constexpr bool GLOBAL = MODE == TCGS_ALPHA_TC_K8_GLOBAL;
     constexpr bool BOXCULL = !(FL & FL_ECOFF) && !GLOBAL;
@@ -700,6 +702,7 @@ __device__ void producer(K7Smem &sm, const RenderArgs &a, const uint32_t *ids, u
 template <int MODE, bool DYN, int FL>
 __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(RenderArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
+    using K7Smem = K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL>;
     K7Smem &sm = *reinterpret_cast<K7Smem *>(smem_raw);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr bool TC = MODE != TCGS_ALPHA_FFMA;
@@ -1081,18 +1084,26 @@ __global__ void k7_reset(DevCounters *ctr) {
     if (threadIdx.x == 0) ctr->tile_queue = 0u;
 }
 
+// dynamic shared memory of a K7 variant: K7_SMEM_BYTES (which also caps residency at K7_CTAS_PER_SM), or more for
+// the global-coordinate ablation's per-stage A operands (lower occupancy is fine for an ablation)
+template <int MODE>
+constexpr int k7_smem() {
+    constexpr int need = (int)sizeof(K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL>) + 1024;
+    return need > K7_SMEM_BYTES ? need : K7_SMEM_BYTES;
+}
+
 template <int MODE, bool DYN, int FL>
 cudaError_t launch_mode(const RenderArgs &a, int num_sms, cudaStream_t st) {
     static bool configured_dev[TCGS_MAX_DEVICES] = {};
     bool &configured = configured_dev[current_device()];
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(render_kernel<MODE, DYN, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             K7_SMEM_BYTES);
+                                             k7_smem<MODE>());
         if (e != cudaSuccess) return e;
         configured = true;
     }
     const int grid = num_sms * K7_CTAS_PER_SM;
-    return launch_k(render_kernel<MODE, DYN, FL>, grid, K7_THREADS, (size_t)K7_SMEM_BYTES, st, a);
+    return launch_k(render_kernel<MODE, DYN, FL>, grid, K7_THREADS, (size_t)k7_smem<MODE>(), st, a);
 }
 
 // EarlyCull on/off for the lone-frame (dynamic) and frames-in-flight (static) schedules; the debug dump runs
@@ -1110,7 +1121,7 @@ cudaError_t launch_variant(const RenderArgs &a, bool dyn, bool early_cull, bool 
 cudaError_t launch_render(int alpha_mode, int early_cull, float *dump_beta, uint8_t *dump_class,
                           const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
                           void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st) {
-    static_assert(sizeof(K7Smem) + 1024 <= K7_SMEM_BYTES, "K7 shared memory");
+    static_assert(sizeof(K7SmemT<false>) + 1024 <= K7_SMEM_BYTES, "K7 shared memory");
     RenderArgs a;
     a.rec = at<Rec>(ws, L.rec);
     a.ids0 = at<uint32_t>(ws, L.tval[0]);

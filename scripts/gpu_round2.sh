@@ -17,5 +17,12 @@ for cfg in c2 c5; do
   timeout 1500 ncu --set full --clock-control none -k regex:render_kernel -o gpurun_out/${TAG}_ablation_$cfg -f \
     python scripts/k7_ablation.py $cfg > gpurun_out/${TAG}_ablation_$cfg.log 2>&1
 done
+# summarise the reports here (gpurun copies back at most 64 MiB): JSON + markdown per report, then drop the reps
+python scripts/ncu_summary.py gpurun_out/${TAG}_frame.ncu-rep gpurun_out/${TAG}_frame_ncu > /dev/null 2>&1
+for cfg in c2 c5; do
+  python scripts/ncu_summary.py gpurun_out/${TAG}_ablation_$cfg.ncu-rep gpurun_out/${TAG}_ablation_${cfg}_ncu > /dev/null 2>&1
+done
+python scripts/launch_table.py gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_launches.txt 2>&1
+rm -f gpurun_out/*.ncu-rep
 python scripts/bench_summary.py gpurun_out/${TAG}_bench_c2.jsonl gpurun_out/${TAG}_bench_c5.jsonl 2>&1 | tail -30
 ls -la gpurun_out | tail -30

@@ -818,12 +818,16 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                                                               uint32_t *tval, SortState *ss_tile, int npass) {
     pdl_wait();
     pdl_launch();
-    // digit histograms of the tile-key radix passes (the onesweep passes' digit totals), per CTA then global
-    __shared__ uint32_t dhist[TILE_MAX_PASSES][RADIX];
-    for (int e = threadIdx.x; e < TILE_MAX_PASSES * RADIX; e += DUP_THREADS) (&dhist[0][0])[e] = 0u;
-    __syncthreads();
+    // TCGS_ONESWEEP only: digit histograms of the tile-key radix passes (the onesweep passes' digit totals), per CTA
+    // then global (the default reduce-then-scan passes count their digits in their own upsweep)
+    __shared__ uint32_t dhist[TCGS_ONESWEEP ? TILE_MAX_PASSES : 1][RADIX];
+    if (TCGS_ONESWEEP) {
+        for (int e = threadIdx.x; e < TILE_MAX_PASSES * RADIX; e += DUP_THREADS) (&dhist[0][0])[e] = 0u;
+        __syncthreads();
+    }
     auto count_key = [&](uint32_t key) {
-        for (int p = 0; p < npass; p++) atomicAdd(&dhist[p][(key >> (RADIX_BITS * p)) & (RADIX - 1)], 1u);
+        if (TCGS_ONESWEEP)
+            for (int p = 0; p < npass; p++) atomicAdd(&dhist[p][(key >> (RADIX_BITS * p)) & (RADIX - 1)], 1u);
     };
     __shared__ uint32_t incl[DUP_THREADS];
     __shared__ uint32_t gid[DUP_THREADS];
@@ -980,10 +984,11 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
         base += total;
         __syncthreads();
     }
-    for (int e = threadIdx.x; e < npass * RADIX; e += DUP_THREADS) {
-        const uint32_t c = (&dhist[0][0])[e];
-        if (c) atomicAdd(&(&ss_tile->ghist[0][0])[e], c);
-    }
+    if (TCGS_ONESWEEP)
+        for (int e = threadIdx.x; e < npass * RADIX; e += DUP_THREADS) {
+            const uint32_t c = (&dhist[0][0])[e];
+            if (c) atomicAdd(&(&ss_tile->ghist[0][0])[e], c);
+        }
 }
 
 // K6: tile ranges from the sorted keys: each thread compares 8 consecutive keys (one 16-byte load for

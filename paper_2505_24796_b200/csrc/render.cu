@@ -74,6 +74,10 @@ struct RenderArgs {
 #define TCGS_K7_EX2EARLY 0
 #endif
 constexpr bool EX2EARLY = TCGS_K7_EX2EARLY != 0;
+#ifndef TCGS_K7_RECBUF
+#define TCGS_K7_RECBUF 1  // producers prefetch the next chunk's records into shared memory (cp.async, no registers)
+#endif
+constexpr bool K7_RECBUF = TCGS_K7_RECBUF != 0;
 constexpr int FL_ECOFF = 1;
 constexpr int FL_DUMP = 2;
 constexpr float ALPHA_CUT = 1.0f / 255.0f;  // src/tilesplat/raster.py:15
@@ -114,6 +118,7 @@ struct __align__(1024) K7SmemT {
     unsigned long long tslot[16];  // dynamic tile stream: (seq << 32) | tile, shared by the producers
     uint32_t c_dead;
     unsigned long long red[K7_CONSUMER_WARPS][4];
+    Rec rbuf[K7_RECBUF ? K7_PRODUCERS : 1][2][32];  // TCGS_K7_RECBUF: producer record prefetch ring (cp.async)
 };
 
 // Element offset (in halves) of (row, k) in a K-major, no-swizzle UMMA operand of 16 K-columns:
@@ -224,6 +229,19 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
         "}\n" ::"r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool pred) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %2, 0;\n"
+        "@p cp.async.cg.shared.global [%0], [%1], 16;\n"
+        "}\n" ::"r"(smem_u32(smem)),
+        "l"(gmem), "r"((int)pred)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -498,12 +516,24 @@ __device__ void producer(K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL> &sm, const Ren
         const int i = k.c * 32 + lane;
         return i < k.n ? ids[k.beg + i] : 0u;
     };
-    // gather pipeline: the records of the chunk being evaluated, and the ids of the next owned chunk
+    // gather pipeline: the records of the chunk being evaluated, and the ids of the next owned chunk.  With
+    // K7_RECBUF the next chunk's records travel by cp.async into this warp's shared-memory ring (slot m & 1)
+    // instead of registers, and are read back (LDS) when the chunk is evaluated.
     Rec rc;
-    {
-        const uint32_t id0 = list_id(cur);
-        if (cur.c * 32 + lane < cur.n) rc = a.rec[id0];
-    }
+    auto gather = [&](const Cursor &k, uint32_t id, int slot, Rec &r) {
+        const bool v = k.c * 32 + lane < k.n;
+        if (K7_RECBUF) {
+            const Rec *src = a.rec + id;
+            Rec *dst = &sm.rbuf[K7_RECBUF ? p : 0][slot][lane];
+#pragma unroll
+            for (int q = 0; q < 3; q++) cp_async16(reinterpret_cast<uint4 *>(dst) + q,
+                                                   reinterpret_cast<const uint4 *>(src) + q, v);
+            cp_async_commit();
+        } else if (v) {
+            r = a.rec[id];
+        }
+    };
+    gather(cur, list_id(cur), 0, rc);
     uint32_t id_nxt = list_id(nxt);
 #if TCGS_K7_LOOKAHEAD >= 2
     // one more owned chunk of cursor and ids in flight: the tile-queue fetch and the range / id loads of a tile
@@ -525,14 +555,18 @@ __device__ void producer(K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL> &sm, const Ren
         const Cursor nx2 = nxa;
         const uint32_t id_nx2 = id_nxa;
         Rec rn;
-        if (nxt.c * 32 + lane < nxt.n) rn = a.rec[id_nxt];
+        gather(nxt, id_nxt, (m + 1) & 1, rn);
 #else
         Cursor nx2 = nxt;
         for (int i = 0; i < NP; i++) cursor_next<DYN>(nx2, a, sm);
         Rec rn;
-        if (nxt.c * 32 + lane < nxt.n) rn = a.rec[id_nxt];
+        gather(nxt, id_nxt, (m + 1) & 1, rn);
         const uint32_t id_nx2 = list_id(nx2);
 #endif
+        if (K7_RECBUF) {  // this chunk's records (the group before the one just issued)
+            cp_async_wait<1>();
+            rc = sm.rbuf[K7_RECBUF ? p : 0][m & 1][lane];
+        }
 
         // evaluate this chunk (registers only)
 #ifdef TCGS_K7_SLOWPROD  // sensitivity experiment: extra dependent work per producer chunk
@@ -689,7 +723,7 @@ __device__ void producer(K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL> &sm, const Ren
         __syncwarp();
         cur = nxt;
         nxt = nx2;
-        rc = rn;
+        if (!K7_RECBUF) rc = rn;
         id_nxt = id_nx2;
 #if TCGS_K7_LOOKAHEAD >= 2
         nxa = nx3;

@@ -65,7 +65,7 @@ def summarise(rep: str):
                 if k.endswith("_MB") and isinstance(v, float):
                     v = v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1.0)
                 if k == "time_us" and isinstance(v, float):
-                    v = v * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(u, 1.0)
+                    v = v * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}.get(u, 1.0)
                 e[k] = v
         stalls = {}
         for h, i in col.items():

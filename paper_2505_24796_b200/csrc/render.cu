@@ -78,6 +78,11 @@ constexpr bool EX2EARLY = TCGS_K7_EX2EARLY != 0;
 #define TCGS_K7_RECBUF 1  // producers prefetch the next chunk's records into shared memory (cp.async, no registers)
 #endif
 constexpr bool K7_RECBUF = TCGS_K7_RECBUF != 0;
+#ifndef TCGS_K7_LOOKAHEAD
+#define TCGS_K7_LOOKAHEAD 1  // producer chunks of cursor / list ids prefetched ahead of the one being gathered
+#endif
+// ring slots: 2 = records one owned chunk ahead; 3 (with TCGS_K7_LOOKAHEAD=2) = two chunks ahead
+constexpr int K7_RECDEPTH = (K7_RECBUF && TCGS_K7_LOOKAHEAD >= 2) ? 3 : 2;
 constexpr int FL_ECOFF = 1;
 constexpr int FL_DUMP = 2;
 constexpr float ALPHA_CUT = 1.0f / 255.0f;  // src/tilesplat/raster.py:15
@@ -118,7 +123,7 @@ struct __align__(1024) K7SmemT {
     unsigned long long tslot[16];  // dynamic tile stream: (seq << 32) | tile, shared by the producers
     uint32_t c_dead;
     unsigned long long red[K7_CONSUMER_WARPS][4];
-    Rec rbuf[K7_RECBUF ? K7_PRODUCERS : 1][2][32];  // TCGS_K7_RECBUF: producer record prefetch ring (cp.async)
+    Rec rbuf[K7_RECBUF ? K7_PRODUCERS : 1][K7_RECDEPTH][32];  // TCGS_K7_RECBUF: producer record ring (cp.async)
 };
 
 // Element offset (in halves) of (row, k) in a K-major, no-swizzle UMMA operand of 16 K-columns:
@@ -141,9 +146,6 @@ __device__ __forceinline__ void mbar_init(unsigned long long *bar, uint32_t coun
 }
 #ifndef TCGS_K7_WAIT
 #define TCGS_K7_WAIT 0
-#endif
-#ifndef TCGS_K7_LOOKAHEAD
-#define TCGS_K7_LOOKAHEAD 1  // producer chunks of cursor / list ids prefetched ahead of the one being gathered
 #endif
 #ifdef TCGS_K7_TIMING  // experiment builds: cycles spent waiting, per barrier kind (tcgs_k7_timing reads them)
 __device__ unsigned long long g_k7_wait[8];
@@ -534,6 +536,12 @@ __device__ void producer(K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL> &sm, const Ren
         }
     };
     gather(cur, list_id(cur), 0, rc);
+#if TCGS_K7_LOOKAHEAD >= 2
+    if (K7_RECDEPTH == 3) {  // the chunk after this one too (the loop issues two chunks ahead)
+        Rec r1;
+        gather(nxt, list_id(nxt), 1, r1);
+    }
+#endif
     uint32_t id_nxt = list_id(nxt);
 #if TCGS_K7_LOOKAHEAD >= 2
     // one more owned chunk of cursor and ids in flight: the tile-queue fetch and the range / id loads of a tile
@@ -555,7 +563,8 @@ __device__ void producer(K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL> &sm, const Ren
         const Cursor nx2 = nxa;
         const uint32_t id_nx2 = id_nxa;
         Rec rn;
-        gather(nxt, id_nxt, (m + 1) & 1, rn);
+        if (K7_RECDEPTH == 3) gather(nxa, id_nxa, (m + 2) % 3, rn);
+        else gather(nxt, id_nxt, (m + 1) & 1, rn);
 #else
         Cursor nx2 = nxt;
         for (int i = 0; i < NP; i++) cursor_next<DYN>(nx2, a, sm);
@@ -563,9 +572,9 @@ __device__ void producer(K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL> &sm, const Ren
         gather(nxt, id_nxt, (m + 1) & 1, rn);
         const uint32_t id_nx2 = list_id(nx2);
 #endif
-        if (K7_RECBUF) {  // this chunk's records (the group before the one just issued)
-            cp_async_wait<1>();
-            rc = sm.rbuf[K7_RECBUF ? p : 0][m & 1][lane];
+        if (K7_RECBUF) {  // this chunk's records (issued one or two groups before the one just issued)
+            cp_async_wait<K7_RECDEPTH - 1>();
+            rc = sm.rbuf[K7_RECBUF ? p : 0][m % K7_RECDEPTH][lane];
         }
 
         // evaluate this chunk (registers only)

@@ -168,6 +168,31 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def rank_views(cams, base, per_rank, rank, world, bands_mode):
+    """The cameras this rank renders: in tile-band mode every rank renders its band of the same frames; otherwise
+    the config's camera pool (C4's orbit, or new yaw views of the base camera) is split into contiguous blocks,
+    one per rank (shard.view_blocks: no view twice, no collective on the data path)."""
+    from paper_2505_24796_b200 import shard
+
+    if bands_mode:
+        return view_cameras(base, per_rank)
+    pool = cams if len(cams) > 1 else view_cameras(base, world * per_rank)
+    b0, b1 = shard.view_blocks(len(pool), world)[rank]
+    mine = pool[b0:b1] or pool[:1]
+    return [mine[k % len(mine)] for k in range(per_rank)]
+
+
+def max_over_ranks(values, device, world):
+    """Device times of the timed region, max over ranks (the contract's whole-job time)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
 def pinned_h2d_GBps(host, dev, reps=3):
     """Measured pinned host -> device copy bandwidth of this GPU's link (the scene's own buffers, CUDA events)."""
     import torch
@@ -435,13 +460,7 @@ def run_tcgs(args):
     scene, cams = synthetic.config_scene(args.config, args.scale)
     base = cams[0]
     per_rank = args.steps + args.warmup
-    if bands_mode:
-        my_views = view_cameras(base, per_rank)  # every rank renders its band of the same frames
-    else:
-        pool = cams if len(cams) > 1 else view_cameras(base, world * per_rank)
-        b0, b1 = shard.view_blocks(len(pool), world)[rank]
-        mine = pool[b0:b1] or pool[:1]
-        my_views = [mine[k % len(mine)] for k in range(per_rank)]
+    my_views = rank_views(cams, base, per_rank, rank, world, bands_mode)
 
     cloud = tcgs.GaussianCloud.from_arrays(scene, dev)
     stream = torch.cuda.current_stream(dev)
@@ -490,10 +509,7 @@ def run_tcgs(args):
     bin_ms = [e[1].elapsed_time(e[2]) for e in evs]
     blend_ms = [e[2].elapsed_time(e[3]) for e in evs]
     gather_ms = [e[3].elapsed_time(e[4]) for e in evs] if bands_mode else None
-    t = torch.tensor([ms, sum(blend_ms) / len(blend_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, blend_max = float(t[0].item()), float(t[1].item())
+    ms_max, blend_max = max_over_ranks([ms, sum(blend_ms) / len(blend_ms)], dev, world)
     if bands_mode:
         st_last = br.render(cloud, my_views[-1], with_stats=True).local.stats
     else:

@@ -109,3 +109,68 @@ def test_gather_bands_world2_gloo(H, W):
     res = dict(q.get(timeout=10) for _ in range(2))
     assert res["gather"], "assembled frame differs from the reference image"
     assert res["stats"] == (10 + 11, 40, 100 + 200, 7, 0 + 1, 11)
+
+
+def _bench_worker(rank, world, port, q):
+    """bench.py's multi-rank orchestration on CPU/gloo: view split (C4 orbit pool and yaw views of C2), the tile-band
+    partition and gather of a C3-sized frame, the stats reduction and the max-over-ranks timing."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+        from paper_2505_24796_b200 import synthetic
+
+        out = {}
+        # views: C4's 256-camera orbit split into contiguous blocks, and C2's single camera expanded to yaw views
+        _, orbit = synthetic.config_scene("c4", 0.0005)
+        v4 = bench.rank_views(orbit, orbit[0], 25, rank, world, False)
+        out["c4"] = [np.asarray(c.view).tobytes() for c in v4]
+        base = synthetic.make_camera(64, 48)
+        v2 = bench.rank_views([base], base, 7, rank, world, False)
+        out["c2"] = [np.asarray(c.view).tobytes() for c in v2]
+        vb = bench.rank_views([base], base, 7, rank, world, True)  # bands: the same frames on every rank
+        out["bands"] = [np.asarray(c.view).tobytes() for c in vb]
+        # timing: max over ranks
+        out["max"] = bench.max_over_ranks([1.0 + rank, 5.0 - rank], "cpu", world)
+        # bands: partition a 4K frame's row counts, each rank fills its rows, gather on rank 0
+        H, W = 2160, 32
+        rows = np.random.default_rng(7).integers(0, 5000, size=(H + 15) // 16)
+        bands = shard.band_partition(rows, world)
+        r0, r1 = shard.band_pixel_rows(bands[rank], H)
+        ref = torch.arange(H * W * 3, dtype=torch.float32).reshape(H, W, 3)
+        rgb = torch.full((H, W, 3), -1.0)
+        rgb[r0:r1] = ref[r0:r1]
+        T = torch.zeros((H, W))
+        n = torch.zeros((H, W), dtype=torch.int32)
+        full = [torch.zeros_like(rgb), torch.zeros_like(T), torch.zeros_like(n)] if rank == 0 else None
+        shard.gather_bands([rgb, T, n], full, bands, H)
+        out["gather"] = bool(torch.equal(full[0], ref)) if rank == 0 else None
+        out["bands_cover"] = bands
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_orchestration_world2_gloo():
+    """bench.py --gpus 2 on CPU: every C4 orbit view rendered by exactly one rank, distinct C2 yaw views per rank,
+    identical band frames, the band partition covering the 4K frame and gathering it on rank 0, max-over-ranks."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    a, b = res[0], res[1]
+    assert not set(a["c4"]) & set(b["c4"]), "an orbit view rendered by both ranks"
+    assert len(set(a["c4"]) | set(b["c4"])) == 50
+    assert not set(a["c2"]) & set(b["c2"])
+    assert a["bands"] == b["bands"]
+    assert a["max"] == b["max"] == [2.0, 5.0]
+    assert a["gather"]
+    bands = a["bands_cover"]
+    assert bands[0][0] == 0 and bands[-1][1] == (2160 + 15) // 16 and bands[0][1] == bands[1][0]

@@ -17,8 +17,14 @@ constexpr int RADIX_BITS = 8;
 constexpr int RADIX = 1 << RADIX_BITS;
 constexpr int OS_THREADS = 256;       // onesweep radix pass: 8 warps per CTA
 constexpr int OS_WARPS = OS_THREADS / 32;
-constexpr int DEPTH_IPT = 8;          // items per thread: depth sort (u64 keys), 2048-item tiles
-constexpr int TILEKEY_IPT = 16;       // items per thread: tile-key sort, 4096-item tiles
+#ifndef TCGS_DEPTH_IPT
+#define TCGS_DEPTH_IPT 8
+#endif
+constexpr int DEPTH_IPT = TCGS_DEPTH_IPT;  // items per thread: depth sort (u32 prefix keys), 2048-item tiles
+#ifndef TCGS_TILEKEY_IPT
+#define TCGS_TILEKEY_IPT 16
+#endif
+constexpr int TILEKEY_IPT = TCGS_TILEKEY_IPT;  // items per thread: tile-key sort, 4096-item tiles
 constexpr int MAX_PASSES = 8;         // depth key: <= 64 bits
 constexpr int TILE_MAX_PASSES = 4;    // tile key: <= 32 bits
 #ifndef TCGS_DUP_ITEMS

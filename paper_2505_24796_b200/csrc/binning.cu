@@ -745,16 +745,15 @@ __global__ void __launch_bounds__(DUP_THREADS) count_upsweep(const uint32_t *idx
                                                              unsigned long long *tmask,
                                                              int band_y0, int band_y1,
                                                              int64_t P, unsigned long long *blocksum, int64_t cap,
-                                                             SortState *ss_tile, int npass) {
+                                                             SortState *ss_tile, int npass, int per) {
     pdl_wait();
     pdl_launch();
     const uint32_t *order = ctr->depth_cur ? idx1 : idx0;
-    const int64_t beg = (int64_t)blockIdx.x * DUP_ITEMS;
+    const int64_t beg = (int64_t)blockIdx.x * per;
     unsigned long long s = 0;
-#pragma unroll
-    for (int u = 0; u < DUP_ITEMS / DUP_THREADS; u++) {
+    for (int u = 0; u * DUP_THREADS < per; u++) {
         const int64_t i = beg + u * DUP_THREADS + threadIdx.x;
-        if (i < P) {
+        if (u * DUP_THREADS + (int)threadIdx.x < per && i < P) {
             const uint32_t g = order[i];
             if (!EXACT) {
                 s += band_count(rect[g], band_y0, band_y1);  // (an empty rectangle: 0)
@@ -806,7 +805,7 @@ __global__ void __launch_bounds__(256) bin_init(uint4 *zero, int64_t n16, uint2 
 
 // Exclusive scan of the per-block counts (one CTA of 1024 threads) -> write offsets and N.
 
-// K4: duplicate-with-keys.  Each CTA walks DUP_ITEMS depth-ordered Gaussians 256 at a time, scans their
+// K4: duplicate-with-keys.  Each CTA walks `per` depth-ordered Gaussians 256 at a time, scans their
 // tile counts, then expands (Gaussian, covered tile) pairs cooperatively: consecutive threads write
 // consecutive splats (binary search of the slot in the shared inclusive scan).
 template <typename KT, bool EXACT>
@@ -815,7 +814,8 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                                                               const unsigned long long *tmask, int64_t P,
                                                               const unsigned long long *blockoff, int tiles_x,
                                                               int band_y0, int band_y1, int64_t cap, KT *tkey,
-                                                              uint32_t *tval, SortState *ss_tile, int npass) {
+                                                              uint32_t *tval, SortState *ss_tile, int npass,
+                                                              int per) {
     pdl_wait();
     pdl_launch();
     // TCGS_ONESWEEP only: digit histograms of the tile-key radix passes (the onesweep passes' digit totals), per CTA
@@ -842,10 +842,10 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
     const uint32_t *order = ctr->depth_cur ? idx1 : idx0;
     const int tid = threadIdx.x;
     constexpr bool exact = EXACT;
-    const int64_t beg = (int64_t)blockIdx.x * DUP_ITEMS;
+    const int64_t beg = (int64_t)blockIdx.x * per;
     unsigned long long base = blockoff[blockIdx.x];
-    for (int r = 0; r < DUP_ITEMS / DUP_THREADS; r++) {
-        const int64_t i = beg + r * DUP_THREADS + tid;
+    for (int r = 0; r * DUP_THREADS < per; r++) {
+        const int64_t i = r * DUP_THREADS + tid < per ? beg + r * DUP_THREADS + tid : P;
         uint32_t c = 0, g = 0;
         unsigned long long m = 0ull;  // exact coverage: the tile mask over q (0: walk rows)
         short4 q = make_short4(0, 0, -1, -1);
@@ -1106,20 +1106,24 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
     uint32_t *tv0 = at<uint32_t>(ws, L.tval[0]);
     uint32_t *tv1 = at<uint32_t>(ws, L.tval[1]);
     unsigned long long *blocksum = at<unsigned long long>(ws, L.blocksum);
-    const int nblk = (int)div_up(P > 0 ? P : 1, DUP_ITEMS);
+    // Gaussians per K3/K4 CTA: DUP_ITEMS, or fewer so that small scenes still fill the GPU (C1: 10k Gaussians
+    // whose rectangles cover ~65 tiles each ran K4 on 10 CTAs)
+    const int64_t Pp = P > 0 ? P : 1;
+    const int per = (int)std::max<int64_t>(32, std::min<int64_t>(DUP_ITEMS, div_up(Pp, DUP_MIN_CTAS) + 31) & ~31);
+    const int nblk = (int)div_up(Pp, per);
     // K3
     const bool exact = band.coverage == TCGS_COVER_ELLIPSE;
     cudaError_t e0 = launch_k(exact ? count_upsweep<true> : count_upsweep<false>, nblk, DUP_THREADS, 0, st,
         (const uint32_t *)at<uint32_t>(ws, L.idx[0]), (const uint32_t *)at<uint32_t>(ws, L.idx[1]), ctr,
         (const short4 *)at<short4>(ws, L.rect), (const Rec *)at<Rec>(ws, L.rec), at<unsigned long long>(ws, L.tmask),
-        band.y0, band.y1, P, blocksum, cap, ss_tile, npass);
+        band.y0, band.y1, P, blocksum, cap, ss_tile, npass, per);
     if (e0 != cudaSuccess) return e0;
     // K4
     e0 = launch_k(exact ? duplicate_keys<KT, true> : duplicate_keys<KT, false>, nblk, DUP_THREADS, 0, st,
         (const uint32_t *)at<uint32_t>(ws, L.idx[0]), (const uint32_t *)at<uint32_t>(ws, L.idx[1]),
         (const DevCounters *)ctr, (const short4 *)at<short4>(ws, L.rect), (const Rec *)at<Rec>(ws, L.rec),
         (const unsigned long long *)at<unsigned long long>(ws, L.tmask), P, (const unsigned long long *)blocksum,
-        band.tiles_x, band.y0, band.y1, cap, tk0, tv0, ss_tile, npass);
+        band.tiles_x, band.y0, band.y1, cap, tk0, tv0, ss_tile, npass, per);
     if (e0 != cudaSuccess) return e0;
     // K5
     // the key's bits split as evenly as possible over the passes (13 bits: 7 + 6, not 8 + 5)

@@ -30,7 +30,8 @@ constexpr int TILE_MAX_PASSES = 4;    // tile key: <= 32 bits
 #ifndef TCGS_DUP_ITEMS
 #define TCGS_DUP_ITEMS 1024
 #endif
-constexpr int DUP_ITEMS = TCGS_DUP_ITEMS;  // Gaussians per duplicate-with-keys CTA
+constexpr int DUP_ITEMS = TCGS_DUP_ITEMS;  // Gaussians per duplicate-with-keys CTA (at most; see bin_tiles)
+constexpr int DUP_MIN_CTAS = 4 * 148;     // K3/K4 CTAs below which a CTA takes fewer Gaussians
 constexpr int DUP_THREADS = 256;
 
 #ifndef TCGS_K7_PIX
@@ -216,7 +217,7 @@ struct Layout {
         L.dbg_conic = take(sizeof(double) * 3 * Pn);
         L.dbg_depth = take(sizeof(double) * Pn);
         L.dbg_mean2d = take(sizeof(double) * 2 * Pn);
-        L.blocksum = take(sizeof(unsigned long long) * (size_t)div_up((int64_t)Pn, DUP_ITEMS));
+        L.blocksum = take(sizeof(unsigned long long) * (size_t)div_up((int64_t)Pn, 32));  // >= 32 Gaussians per K3/K4 CTA
         L.tkey[0] = take(sizeof(uint32_t) * cn);
         L.tkey[1] = take(sizeof(uint32_t) * cn);
         L.tval[0] = take(sizeof(uint32_t) * cn);

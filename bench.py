@@ -297,7 +297,10 @@ def profile_traffic(config="c2"):
 
     if config != "c2":
         return None
+    # the capture of the current build first (K7 rows of profiles/r2f2_frame_ncu.json), then older ones
+    current = os.path.join(ROOT, "profiles", "r2f2_k7_ncu.json")
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_k7_ncu.json")))  # r1_ < ... < r2a_ < r2b_
+    files = [f for f in files if f != current] + ([current] if os.path.exists(current) else [])
     for p in reversed(files):
         with open(p) as f:
             rows = [e for e in json.load(f) if "render_kernel" in e.get("kernel", "")]

@@ -291,10 +291,22 @@ def issue_roofline(traffic, blend_ms, clocks):
 
 def profile_traffic(config="c2"):
     """K7 DRAM bytes and warp instructions per launch (dram__bytes_read.sum + dram__bytes_write.sum,
-    smsp__inst_executed.sum) from the newest committed ncu --set full summary under profiles/
-    (scripts/ncu_summary.py).  Those captures are of the C2 workload; other configs get None."""
+    smsp__inst_executed.sum) from the committed ncu --set full summaries under profiles/ (scripts/ncu_summary.py):
+    C2 (the frame capture) and C5 (the ablation capture); other configs get None."""
     import glob
 
+    if config == "c5":  # the ablation capture's default variant (hi/lo, EarlyCull on, dynamic schedule)
+        p = os.path.join(ROOT, "profiles", "r2f2_ablation_c5_ncu.json")
+        if not os.path.exists(p):
+            return None
+        with open(p) as f:
+            rows = [e for e in json.load(f) if "render_kernel<0, 1, 0>" in e.get("kernel", "")]
+        if not rows:
+            return None
+        mb = [e["dram_read_MB"] + e["dram_write_MB"] for e in rows]
+        inst = [e["inst_executed"] for e in rows]
+        return {"bytes_per_launch": 1e6 * sum(mb) / len(mb), "source": os.path.relpath(p, ROOT),
+                "warp_inst_per_launch": sum(inst) / len(inst)}
     if config != "c2":
         return None
     # the capture of the current build first (K7 rows of profiles/r2f2_frame_ncu.json), then older ones

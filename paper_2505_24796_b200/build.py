@@ -13,7 +13,10 @@ LIB_DIR = os.path.join(HERE, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libtcgs.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["abi.cu", "preprocess.cu", "binning.cu", "render.cu"]
+SOURCES = ["abi.cu", "preprocess.cu", "binning.cu", "render.cu", "render.cu:few"]
+# render.cu is compiled twice: the default K7 (4 CTAs/SM x 2 producer warps) and the few-tiles K7 (3 x 4)
+VARIANT_FLAGS = {"few": ["-DTCGS_K7_ENTRY=launch_render_k7_few", "-DTCGS_K7_CTAS=3", "-DTCGS_K7_PRODUCERS=4",
+                         "-DTCGS_K7_SECOND_BUILD"]}
 # preprocess.cu must not contract a*b+c into FMA: it reproduces numpy's float64 operation order.
 PER_FILE_FLAGS = {"preprocess.cu": ["--fmad=false"]}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -37,9 +40,11 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     obj_dir = os.path.join(os.path.dirname(lib_path), "obj" if out is None else "obj_" + os.path.basename(lib_path))
     os.makedirs(obj_dir, exist_ok=True)
     objs = []
-    for src in SOURCES:
-        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *COMMON, *defines, *PER_FILE_FLAGS.get(src, []), "-c", os.path.join(CSRC, src), "-o", obj]
+    for entry in SOURCES:
+        src, _, variant = entry.partition(":")
+        obj = os.path.join(obj_dir, src.replace(".cu", f"_{variant}.o" if variant else ".o"))
+        cmd = [NVCC, *ARCH, *COMMON, *defines, *PER_FILE_FLAGS.get(src, []), *VARIANT_FLAGS.get(variant, []), "-c",
+               os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
             print(" ".join(cmd), flush=True)

@@ -273,7 +273,7 @@ int tcgs_blend(int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, void *w
     if (!rgb || !T || !n_contrib) return fail(TCGS_ERR_INVALID_ARG, "null output");
     const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
     time_mark(opts, ws, ST_BLEND, 0, (cudaStream_t)stream);
-    cudaError_t e = launch_render(opts ? opts->alpha_mode : 0, opts ? opts->early_cull : 1,
+    cudaError_t e = launch_render(P, opts ? opts->alpha_mode : 0, opts ? opts->early_cull : 1,
                                   opts ? opts->dump_beta : nullptr, opts ? opts->dump_class : nullptr, *cam,
                                   make_band(*cam, opts), nullptr, ws, L, rgb, T, n_contrib, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "render");
@@ -390,7 +390,7 @@ int tcgs_blend_lists(int64_t P, const double *mean2d, const double *conic, const
     if (e != cudaSuccess) return cuda_fail(e, "init_counters");
     e = launch_pack_lists(P, mean2d, conic, opacity, colors, offsets, band, ws, L, st);
     if (e != cudaSuccess) return cuda_fail(e, "pack_lists");
-    e = launch_render(opts ? opts->alpha_mode : 0, opts ? opts->early_cull : 1, opts ? opts->dump_beta : nullptr,
+    e = launch_render(P, opts ? opts->alpha_mode : 0, opts ? opts->early_cull : 1, opts ? opts->dump_beta : nullptr,
                       opts ? opts->dump_class : nullptr, *cam, band, reinterpret_cast<const uint32_t *>(ids), ws, L,
                       rgb, T, n_contrib, st);
     if (e != cudaSuccess) return cuda_fail(e, "render");

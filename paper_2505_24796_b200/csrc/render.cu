@@ -1161,7 +1161,13 @@ cudaError_t launch_variant(const RenderArgs &a, bool dyn, bool early_cull, bool 
 
 }  // namespace
 
-cudaError_t launch_render(int alpha_mode, int early_cull, float *dump_beta, uint8_t *dump_class,
+// This file is compiled twice (paper_2505_24796_b200/build.py): launch_render_k7 with the default residency (4 CTAs
+// per SM, 2 producer warps) and launch_render_k7_few with 3 CTAs x 4 producer warps, the better trade when a frame
+// has fewer tiles than resident CTAs (long per-tile lists, e.g. C1's 256 tiles: 94 -> 66 us).
+#ifndef TCGS_K7_ENTRY
+#define TCGS_K7_ENTRY launch_render_k7
+#endif
+cudaError_t TCGS_K7_ENTRY(int alpha_mode, int early_cull, float *dump_beta, uint8_t *dump_class,
                           const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
                           void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st) {
     static_assert(sizeof(K7SmemT<false>) + 1024 <= K7_SMEM_BYTES, "K7 shared memory");
@@ -1204,7 +1210,7 @@ cudaError_t launch_render(int alpha_mode, int early_cull, float *dump_beta, uint
 
 }  // namespace tcgs
 
-#ifdef TCGS_K7_TIMING
+#if defined(TCGS_K7_TIMING) && !defined(TCGS_K7_SECOND_BUILD)
 // experiment builds only (not in include/tcgs.h): read and clear the K7 wait counters -- cycles summed over warps:
 // [0] producer token, [1] producer empty stage, [2] producer TMEM buffer, [3] consumer full stage,
 // [4] consumer MMA done, [5] producer total, [6] consumer total

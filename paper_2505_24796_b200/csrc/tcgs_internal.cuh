@@ -40,7 +40,9 @@ constexpr int DUP_THREADS = 256;
 constexpr int K7_PIX = TCGS_K7_PIX;              // pixels per consumer thread (1 or 2)
 constexpr int K7_CONSUMER_WARPS = 8 / K7_PIX;  // 256 pixels of a 16x16 tile
 #ifndef TCGS_K7_PRODUCERS
-#define TCGS_K7_PRODUCERS 4  // measured: 2 -> 4 producers, C2 K7 537 -> 524 us, C5 3.96 -> 3.35 ms (r2f)
+// measured (r2aa): 4 CTAs/SM x 2 producers (48 registers) against 3 CTAs/SM x 4 producers (56 registers): C2 K7
+// 475 -> 445 us, C5 2.37 -> 2.45 ms; 4 CTAs x 3 producers (40 registers, spills): 504 us / 2.82 ms
+#define TCGS_K7_PRODUCERS 2
 #endif
 constexpr int K7_PRODUCERS = TCGS_K7_PRODUCERS;  // producer warps (alternate 32-entry chunks, token-ordered compaction)
 constexpr int K7_THREADS = 32 * (K7_CONSUMER_WARPS + K7_PRODUCERS);
@@ -58,7 +60,7 @@ constexpr int K7_STAGES = TCGS_K7_STAGES;  // shared-memory B-operand stages
 constexpr int K7_TMEM_BUFS = TCGS_K7_TMEM_BUFS;  // TMEM accumulator buffers (1: released after the last load)
 constexpr int K7_TMEM_COLS = K7_TMEM_BUFS * 2 * K7_BATCH;  // buffers x pixel halves x N
 #ifndef TCGS_K7_CTAS
-#define TCGS_K7_CTAS (TCGS_K7_PIX == 2 ? 4 : 3)
+#define TCGS_K7_CTAS 4  // resident K7 CTAs per SM: TMEM 4 x 128 columns = 512, 48 registers at 320 threads
 #endif
 constexpr int K7_CTAS_PER_SM = TCGS_K7_CTAS;
 
@@ -264,9 +266,24 @@ cudaError_t launch_preprocess_views(const tcgs_scene &scene, const tcgs_camera *
                                     int debug, int coverage, int defer_colour, void *const *ws, const Layout *L,
                                     cudaStream_t st);
 cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st);
-cudaError_t launch_render(int alpha_mode, int early_cull, float *dump_beta, uint8_t *dump_class,
-                          const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
-                          void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st);
+cudaError_t launch_render_k7(int alpha_mode, int early_cull, float *dump_beta, uint8_t *dump_class,
+                             const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
+                             void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st);
+cudaError_t launch_render_k7_few(int alpha_mode, int early_cull, float *dump_beta, uint8_t *dump_class,
+                                 const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
+                                 void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st);
+// K7: the 3-CTA x 4-producer build when the frame is producer-heavy -- fewer tiles than 4 resident CTAs per SM can
+// take (C1), or long per-tile lists, by Gaussians per tile (C5: 735 per tile, K7 2.45 -> 2.37 ms; C2 has 122)
+inline cudaError_t launch_render(int64_t P, int alpha_mode, int early_cull, float *dump_beta, uint8_t *dump_class,
+                                 const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
+                                 void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t nt = band.n_tiles();
+    auto f = (nt < 4 * sms || P > 400 * nt) ? launch_render_k7_few : launch_render_k7;
+    return f(alpha_mode, early_cull, dump_beta, dump_class, cam, band, ids_override, ws, L, rgb, T, n_contrib, st);
+}
 cudaError_t launch_pack_lists(int64_t P, const double *mean2d, const double *conic, const double *opacity,
                               const float *colors, const int64_t *offsets, const Band &band, void *ws,
                               const Layout &L, cudaStream_t st);

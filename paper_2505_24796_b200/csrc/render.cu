@@ -984,8 +984,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
                         }
                     }
                 };
-#ifndef TCGS_K7_GROUP
-#define TCGS_K7_GROUP 16
+#ifndef TCGS_K7_GROUP  // 8-column groups at 48 registers (4 CTAs/SM: 444 -> 440 us at C2), 16 at 56 (equal)
+#define TCGS_K7_GROUP (TCGS_K7_CTAS >= 4 ? 8 : 16)
 #endif
                 constexpr int G = NPIX == 1 ? TCGS_K7_GROUP : 8;  // columns per TMEM load group (G x NPIX betas)
 #pragma unroll

@@ -367,7 +367,10 @@ __global__ void __launch_bounds__(256) radix_rowscan(const unsigned long long *n
 }
 
 template <typename KT, int IPT, int DB>  // DB digit bits: digits >= 1 << DB stay empty
-__global__ void __launch_bounds__(OS_THREADS, 3) radix_downsweep(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1,
+#ifndef TCGS_DOWNSWEEP_CTAS
+#define TCGS_DOWNSWEEP_CTAS 3  // resident downsweep CTAs per SM the register allocation must allow
+#endif
+__global__ void __launch_bounds__(OS_THREADS, TCGS_DOWNSWEEP_CTAS) radix_downsweep(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1,
                                                               const unsigned long long *n_dev, int64_t n_host,
                                                               int64_t cap, int pass, int shift, const SortState *ss,
                                                               const uint32_t *table, int64_t T) {

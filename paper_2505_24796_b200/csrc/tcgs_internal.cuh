@@ -5,6 +5,7 @@
 #include <math.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <utility>
 
@@ -281,7 +282,10 @@ inline cudaError_t launch_render(int64_t P, int alpha_mode, int early_cull, floa
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t nt = band.n_tiles();
-    auto f = (nt < 4 * sms || P > 400 * nt) ? launch_render_k7_few : launch_render_k7;
+    // TCGS_K7_BUILD=few|many in the environment forces one build (tests: both give the same frame)
+    static const char *force = getenv("TCGS_K7_BUILD");
+    const bool few = force && force[0] ? force[0] == 'f' : (nt < 4 * sms || P > 400 * nt);
+    auto f = few ? launch_render_k7_few : launch_render_k7;
     return f(alpha_mode, early_cull, dump_beta, dump_class, cam, band, ids_override, ws, L, rgb, T, n_contrib, st);
 }
 cudaError_t launch_pack_lists(int64_t P, const double *mean2d, const double *conic, const double *opacity,

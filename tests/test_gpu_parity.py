@@ -928,3 +928,33 @@ def test_criterion_2_exp_call_accounting(seed, n):
     if not d.any():
         assert (on.f_blend, on.f_cull, on.f_skip) == (off.f_blend, off.f_cull, off.f_skip)
         assert torch.equal(on_f.rgb, off_f.rgb)
+
+
+@pytest.mark.parametrize("cfg,scale", [("c2", 0.05), ("c5", 0.01), ("c1", 1.0)])
+def test_both_k7_builds_render_the_same_frame(cfg, scale):
+    """K7 is built twice (4 CTAs/SM x 2 producer warps, and 3 x 4 for producer-heavy frames); launch_render picks
+    one by tiles and Gaussians per tile.  Forcing each (TCGS_K7_BUILD) must give bit-identical frames and stats."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, hashlib, torch; sys.path.insert(0, '.')\n"
+        "import paper_2505_24796_b200 as tcgs\n"
+        "from paper_2505_24796_b200 import synthetic\n"
+        f"s, cams = synthetic.config_scene('{cfg}', {scale})\n"
+        "c = tcgs.GaussianCloud.from_arrays(s, 'cuda')\n"
+        "h = hashlib.sha256()\n"
+        "for spec in ('tcgs', 'tcgs-ffma'):\n"
+        "    f = tcgs.Renderer('cuda', spec).render_frame(c, cams[0])\n"
+        "    for t in (f.rgb, f.T, f.n_contrib): h.update(t.cpu().numpy().tobytes())\n"
+        "    st = f.stats; h.update(repr((st.f_blend, st.f_cull, st.f_skip, st.exp_calls, st.pixels_terminated)).encode())\n"
+        "print(h.hexdigest())\n")
+    out = {}
+    for build in ("few", "many"):
+        env = dict(os.environ, TCGS_K7_BUILD=build)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=root, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[build] = r.stdout.strip().splitlines()[-1]
+    assert out["few"] == out["many"], out

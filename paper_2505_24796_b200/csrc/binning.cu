@@ -39,6 +39,10 @@
 
 #include "tcgs_internal.cuh"
 
+#ifndef TCGS_ONESWEEP
+#define TCGS_ONESWEEP 0  // 1: single-kernel passes with decoupled look-back (measured slower, r2f: 276 vs 251 us)
+#endif
+
 namespace tcgs {
 
 namespace {
@@ -109,15 +113,20 @@ __device__ __forceinline__ int depth_shift(unsigned long long range) {
 }
 
 __global__ void __launch_bounds__(256) depth_fix_hist(const unsigned long long *src, uint32_t *keys, uint32_t *idx,
-                                                      int64_t P, DevCounters *ctr, SortState *ss, OsHeader *hdr) {
+                                                      int64_t P, DevCounters *ctr, SortState *ss, OsHeader *hdr,
+                                                      uint32_t *table0, int64_t T0) {
     pdl_wait();
     pdl_launch();
     if (blockIdx.x == 0 && threadIdx.x == 0) {  // a new look-back epoch for this binning's radix passes
         hdr->magic = OS_MAGIC;
         hdr->epoch = hdr->epoch + 1u;
     }
-    __shared__ uint32_t h[DEPTH_PASSES][RADIX];
-    for (int e = threadIdx.x; e < DEPTH_PASSES * RADIX; e += blockDim.x) (&h[0][0])[e] = 0;
+    // pass 0: the digit counts of this CTA's radix tile (that pass's upsweep table column); every pass: the digit
+    // range, which plans the passes (a pass with a single digit value is the identity)
+    __shared__ uint32_t h0[RADIX];
+    __shared__ uint32_t rng[DEPTH_PASSES][2];  // (255 - min digit, max digit)
+    h0[threadIdx.x] = 0;
+    if (threadIdx.x < DEPTH_PASSES * 2) (&rng[0][0])[threadIdx.x] = 0;
     __syncthreads();
     const unsigned long long kmin = ctr->key_min;
     const unsigned long long range = ctr->n_visible ? ctr->key_max - kmin : 0ull;
@@ -126,19 +135,50 @@ __global__ void __launch_bounds__(256) depth_fix_hist(const unsigned long long *
         ctr->key_range = DEPTH_KEY_MAX;  // the prefix keys span [0, DEPTH_KEY_MAX]
         ctr->depth_shift = shift;
     }
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    // one CTA per radix tile of the first pass (OS_THREADS x DEPTH_IPT keys): its pass-0 digit counts are that
+    // pass's upsweep table column, so the pass runs without an upsweep
+    const int64_t t0 = (int64_t)blockIdx.x * (OS_THREADS * DEPTH_IPT);
+    const int64_t t1 = t0 + OS_THREADS * DEPTH_IPT < P ? t0 + OS_THREADS * DEPTH_IPT : P;
+    uint32_t dlo[DEPTH_PASSES], dhi[DEPTH_PASSES];
+#pragma unroll
+    for (int p = 0; p < DEPTH_PASSES; p++) {
+        dlo[p] = RADIX - 1;
+        dhi[p] = 0;
+    }
+    for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
         const unsigned long long k = src[i];  // K1's output stays intact: tcgs_bin can run again (other bands)
         const uint32_t key = (k == ~0ull) ? DEPTH_KEY_MAX : (uint32_t)((k - kmin) >> shift);
         keys[i] = key;
         idx[i] = (uint32_t)i;
+        atomicAdd(&h0[key & (RADIX - 1)], 1u);
 #pragma unroll
-        for (int p = 0; p < DEPTH_PASSES; p++) atomicAdd(&h[p][(key >> (RADIX_BITS * p)) & (RADIX - 1)], 1u);
+        for (int p = 0; p < DEPTH_PASSES; p++) {
+            const uint32_t d = (key >> (RADIX_BITS * p)) & (RADIX - 1);
+            dlo[p] = d < dlo[p] ? d : dlo[p];
+            dhi[p] = d > dhi[p] ? d : dhi[p];
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < DEPTH_PASSES; p++) {
+        const uint32_t lo = __reduce_min_sync(0xffffffffu, dlo[p]), hi = __reduce_max_sync(0xffffffffu, dhi[p]);
+        if ((threadIdx.x & 31) == 0 && t0 + (threadIdx.x & ~31) < t1) {  // (warps with keys)
+            atomicMax(&rng[p][0], RADIX - 1 - lo);
+            atomicMax(&rng[p][1], hi);
+        }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < DEPTH_PASSES * RADIX; e += blockDim.x) {
-        const uint32_t c = (&h[0][0])[e];
-        if (c) atomicAdd(&(&ss->ghist[0][0])[e], c);
+    if (threadIdx.x < DEPTH_PASSES * 2) atomicMax(&(&ss->drange[0][0])[threadIdx.x], (&rng[0][0])[threadIdx.x]);
+    if (TCGS_ONESWEEP) {  // single-kernel passes take their digit totals from here
+        __syncthreads();
+        for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+            const uint32_t key = keys[i];
+#pragma unroll
+            for (int p = 0; p < DEPTH_PASSES; p++)
+                atomicAdd(&ss->ghist[p][(key >> (RADIX_BITS * p)) & (RADIX - 1)], 1u);
+        }
     }
+    static_assert(OS_THREADS == RADIX, "one digit per thread");
+    if (table0) table0[(int64_t)threadIdx.x * T0 + blockIdx.x] = h0[threadIdx.x];
     // the last CTA to finish plans the passes (no separate planning launch): a pass whose digit is
     // the same for every key is the identity and is skipped
     __shared__ int last, trivial;
@@ -150,9 +190,8 @@ __global__ void __launch_bounds__(256) depth_fix_hist(const unsigned long long *
     __threadfence();
     int cur = 0;
     for (int p = 0; p < DEPTH_PASSES; p++) {
-        if (threadIdx.x == 0) trivial = P == 0 ? 1 : 0;
-        __syncthreads();
-        if ((int64_t)__ldcg(&ss->ghist[p][threadIdx.x]) == P) trivial = 1;
+        if (threadIdx.x == 0)
+            trivial = (P == 0 || RADIX - 1 - __ldcg(&ss->drange[p][0]) == __ldcg(&ss->drange[p][1])) ? 1 : 0;
         __syncthreads();
         const int triv = trivial;
         if (threadIdx.x == 0) {
@@ -586,7 +625,7 @@ constexpr int downsweep_smem() {
 template <typename KT, int IPT, int DB>
 cudaError_t launch_radix_pass_db(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const unsigned long long *n_dev,
                                  int64_t n_host, int64_t cap, int pass, int shift, SortState *ss, uint32_t *table_all,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, bool have_table = false) {
     static bool configured_dev[TCGS_MAX_DEVICES] = {};
     bool &configured = configured_dev[current_device()];
     constexpr int smem = downsweep_smem<KT, IPT>();
@@ -602,8 +641,10 @@ cudaError_t launch_radix_pass_db(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, con
     const int64_t tiles = div_up(n_dev ? cap : n_host, OS_THREADS * IPT);
     const unsigned grid = (unsigned)(tiles > 0 ? tiles : 1);
     uint32_t *table = table_all + (int64_t)pass * RADIX * tiles;
-    cudaError_t e = launch_k(radix_upsweep<KT, IPT, DB>, grid, OS_THREADS, 0, st, k0, k1, n_dev, n_host, cap, pass,
-                             shift, (const SortState *)ss, table, tiles);
+    cudaError_t e = cudaSuccess;
+    if (!have_table)  // (have_table: an earlier kernel already wrote this pass's per-tile digit counts)
+        e = launch_k(radix_upsweep<KT, IPT, DB>, grid, OS_THREADS, 0, st, k0, k1, n_dev, n_host, cap, pass, shift,
+                     (const SortState *)ss, table, tiles);
     if (e == cudaSuccess) e = launch_k(radix_rowscan<IPT>, RADIX, 256, 0, st, n_dev, n_host, cap, pass, ss, table, tiles);
     if (e == cudaSuccess)
         e = launch_k(radix_downsweep<KT, IPT, DB>, grid, OS_THREADS, (size_t)smem, st, k0, k1, v0, v1, n_dev, n_host,
@@ -611,9 +652,6 @@ cudaError_t launch_radix_pass_db(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, con
     return e;
 }
 
-#ifndef TCGS_ONESWEEP
-#define TCGS_ONESWEEP 0  // 1: single-kernel passes with decoupled look-back (measured slower, r2f: 276 vs 251 us)
-#endif
 
 template <typename KT, int IPT, int DB>
 cudaError_t launch_onesweep_db(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const unsigned long long *n_dev,
@@ -642,7 +680,7 @@ cudaError_t launch_onesweep_db(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const
 template <typename KT, int IPT>
 cudaError_t launch_radix_pass(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const unsigned long long *n_dev,
                               int64_t n_host, int64_t cap, int pass, int shift, int db, SortState *ss,
-                              uint32_t *table_all, const OsHeader *hdr, cudaStream_t st) {
+                              uint32_t *table_all, const OsHeader *hdr, cudaStream_t st, bool have_table = false) {
     if (TCGS_ONESWEEP) {
         uint64_t *look = reinterpret_cast<uint64_t *>(table_all);
         switch (db) {
@@ -653,10 +691,10 @@ cudaError_t launch_radix_pass(KT *k0, KT *k1, uint32_t *v0, uint32_t *v1, const 
         }
     }
     switch (db) {
-        case 5: return launch_radix_pass_db<KT, IPT, 5>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st);
-        case 6: return launch_radix_pass_db<KT, IPT, 6>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st);
-        case 7: return launch_radix_pass_db<KT, IPT, 7>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st);
-        default: return launch_radix_pass_db<KT, IPT, 8>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st);
+        case 5: return launch_radix_pass_db<KT, IPT, 5>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st, have_table);
+        case 6: return launch_radix_pass_db<KT, IPT, 6>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st, have_table);
+        case 7: return launch_radix_pass_db<KT, IPT, 7>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st, have_table);
+        default: return launch_radix_pass_db<KT, IPT, 8>(k0, k1, v0, v1, n_dev, n_host, cap, pass, shift, ss, table_all, st, have_table);
     }
 }
 
@@ -1182,12 +1220,15 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
     if (P > 0) {
         // K2: 24-bit depth-prefix radix sort + exact float64 fix-up of equal prefixes
         const unsigned long long *src = at<unsigned long long>(ws, L.key_src);
-        e = launch_k(depth_fix_hist, 2 * 148, 256, 0, st, src, k0, i0, P, ctr, ss_depth, at<OsHeader>(ws, L.os_hdr));
+        const int64_t T0 = div_up(P, OS_THREADS * DEPTH_IPT);  // radix tiles of the depth passes
+        e = launch_k(depth_fix_hist, (unsigned)T0, OS_THREADS, 0, st, src, k0, i0, P, ctr, ss_depth,
+                     at<OsHeader>(ws, L.os_hdr), TCGS_ONESWEEP ? nullptr : at<uint32_t>(ws, L.lb_depth), T0);
         if (e != cudaSuccess) return e;
         for (int p = 0; p < DEPTH_PASSES; p++) {
+            // pass 0's digit table comes from depth_fix_hist
             e = launch_radix_pass<uint32_t, DEPTH_IPT>(k0, k1, i0, i1, nullptr, P, P, p, RADIX_BITS * p, RADIX_BITS,
                                                        ss_depth, at<uint32_t>(ws, L.lb_depth),
-                                                       at<OsHeader>(ws, L.os_hdr), st);
+                                                       at<OsHeader>(ws, L.os_hdr), st, p == 0 && !TCGS_ONESWEEP);
             if (e != cudaSuccess) return e;
         }
         e = launch_k(depth_fixup, (unsigned)std::min<int64_t>(div_up(P, 256), 8 * 148), 256, 0, st,

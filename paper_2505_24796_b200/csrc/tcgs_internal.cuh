@@ -172,6 +172,7 @@ struct SortState {
     int done_ctas;  // depth_fix_hist: CTAs finished (the last one plans the passes)
     int pad[2];
     unsigned int tile_ctr[MAX_PASSES];  // onesweep passes: next radix tile to claim (launch order = look-back order)
+    unsigned int drange[MAX_PASSES][2];  // depth passes: (255 - min digit, max digit), for the pass plan
 };
 
 // Onesweep look-back tables (one u64 per (radix tile, digit) and pass): epoch (32) | flag (2) | count (30).  The

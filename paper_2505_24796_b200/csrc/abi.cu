@@ -40,9 +40,12 @@ int cuda_fail(cudaError_t e, const char *where) {
     return TCGS_ERR_CUDA;
 }
 
+// (PDL: the dependent K1 may be scheduled before this kernel's wait -- it computes from the caller's scene and
+// waits itself before writing the workspace, which orders it after this kernel and, through it, after the
+// previous frame's K7)
 __global__ void init_counters(DevCounters *c, int debug) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     DevCounters z;
     memset(&z, 0, sizeof(z));
     z.key_min = ~0ull;
@@ -54,8 +57,8 @@ struct CounterSet {
     DevCounters *c[TCGS_MAX_VIEWS_PER_PASS];
 };
 __global__ void init_counters_views(const __grid_constant__ CounterSet s, int n, int debug) {
-    pdl_wait();
     pdl_launch();
+    pdl_wait();
     if ((int)threadIdx.x < n) {
         DevCounters z;
         memset(&z, 0, sizeof(z));

@@ -263,9 +263,8 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
     for (int q = 0; q < 5; q++)  // ragged / unaligned segments: coalesced cooperative copy
         if (!bulk[q])
             for (int e = threadIdx.x; e < n * per[q]; e += NT) seg[q][e] = src[q][base * per[q] + e];
-    // PDL: the scene inputs above are never written by a libtcgs kernel, so they stream in while the previous
-    // kernel of the stream finishes; everything below writes the workspace
-    pdl_wait();
+    // PDL: the scene inputs are never written by a libtcgs kernel, so they stream in -- and the projection runs --
+    // while the previous kernels of the stream finish; pdl_wait() comes right before the first workspace write
     pdl_launch();
     auto wait_bar = [&](int g) {
         if (any_bulk[g]) {
@@ -327,7 +326,10 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
 #pragma unroll
             for (int k = 0; k < 3; k++) t[k] = dot3_gemv(V[4 * k + 0], V[4 * k + 1], V[4 * k + 2], m0, m1, m2) + V[4 * k + 3];
             const double tz = t[2];
-            if (a.debug) a.radius[i] = -1;  // the radius only feeds tcgs_copy_projection (debug)
+            if (a.debug) {  // the radius only feeds tcgs_copy_projection (debug)
+                pdl_wait();
+                a.radius[i] = -1;
+            }
             if (!(tz > a.cam.near_plane)) {  // src/tilesplat/projection.py:76-78 (tz <= near culls)
                 dropped = true;
             } else {
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
                     dropped = true;
                 } else {
                     const double s11 = sc / det, s12 = -sb / det, s22 = sa / det;
-                    if (a.debug) a.radius[i] = rad;
+                    if (a.debug) a.radius[i] = rad;  // (after the pdl_wait above)
                     if (a.debug) {
                         a.dbg_conic[3 * i] = s11;
                         a.dbg_conic[3 * i + 1] = s12;
@@ -461,14 +463,17 @@ __global__ void __launch_bounds__(256, NV == 1 ? 1 : TCGS_K1_VIEWS_MIN_CTAS) pre
                         rc.r = col[0];
                         rc.g = col[1];
                         rc.b = col[2];
+                        pdl_wait();
                         a.rec[i] = rc;
                     }
                 }
             }
+            pdl_wait();
             a.rect[i] = rect;
             a.keys[i] = key;
         }
         // warp-aggregated counters
+        pdl_wait();
         const unsigned full = 0xffffffffu;
         const unsigned n_drop = __popc(__ballot_sync(full, dropped));
         const unsigned n_vis = __popc(__ballot_sync(full, touched > 0));

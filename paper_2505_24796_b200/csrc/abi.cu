@@ -262,7 +262,9 @@ int tcgs_bin(int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, void *ws,
     if (rc) return rc;
     const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
     time_mark(opts, ws, ST_SORT, 0, (cudaStream_t)stream);
-    cudaError_t e = launch_bin(P, make_band(*cam, opts), ws, L, max_splats, (cudaStream_t)stream);
+    const Band band = make_band(*cam, opts);
+    const bool compact = producer_heavy(P, band.tiles_x, band.tiles_y) && !(opts && opts->dump_beta);
+    cudaError_t e = launch_bin(P, band, ws, L, max_splats, (cudaStream_t)stream, compact);
     if (e != cudaSuccess) return cuda_fail(e, "bin");
     time_mark(opts, ws, ST_SORT, 1, (cudaStream_t)stream);
     return TCGS_OK;
@@ -412,7 +414,7 @@ int tcgs_copy_lists(const void *ws, int64_t P, const tcgs_camera *cam, const tcg
     if (e != cudaSuccess) return cuda_fail(e, "copy_lists");
     const int64_t n = (int64_t)c.n_splats < max_splats ? (int64_t)c.n_splats : max_splats;
     const uint32_t *src = at<uint32_t>(ws, c.tile_cur ? L.tval[1] : L.tval[0]);
-    if (n > 0) e = cudaMemcpyAsync(ids_out, src, sizeof(uint32_t) * (size_t)n, cudaMemcpyDeviceToDevice, st);
+    if (n > 0) e = launch_strip_marks(src, reinterpret_cast<uint32_t *>(ids_out), n, st);  // (K4's dead marks)
     const Band band = make_band(*cam, opts);
     if (e == cudaSuccess && band.n_tiles() > 0)
         e = cudaMemcpyAsync(ranges_out, at<uint2>(ws, L.ranges), sizeof(uint2) * (size_t)band.n_tiles(),

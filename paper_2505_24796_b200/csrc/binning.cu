@@ -841,6 +841,7 @@ __global__ void __launch_bounds__(256) bin_init(uint4 *zero, int64_t n16, uint2 
         ctr->n_splats = 0ull;
         ctr->overflow = 0ull;
         ctr->n_long_runs = 0u;
+        ctr->compact = 0;
     }
 }
 
@@ -856,7 +857,7 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                                                               const unsigned long long *blockoff, int tiles_x,
                                                               int band_y0, int band_y1, int64_t cap, KT *tkey,
                                                               uint32_t *tval, SortState *ss_tile, int npass,
-                                                              int per) {
+                                                              int per, int mark) {
     pdl_wait();
     pdl_launch();
     // TCGS_ONESWEEP only: digit histograms of the tile-key radix passes (the onesweep passes' digit totals), per CTA
@@ -916,14 +917,20 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                     }
                 } else {
                     CoverRec cs;
-                    if (exact && c) cs = make_cover(rec[g]);
+                    if ((exact || mark) && c) cs = make_cover(rec[g]);
                     for (int ty = q.y; ty <= q.w; ty++) {
                         const uint32_t row = (uint32_t)((ty - band_y0) * tiles_x);
                         int lo = q.x, hi = q.z;
                         if (exact && !cover_row(cs, ty, q.x, q.z, lo, hi)) continue;
-                        for (int tx = lo; tx <= hi; tx++, o++) {
+                        if (!exact && mark && !cover_row(cs, ty, q.x, q.z, lo, hi)) {  // the whole row is dead
+                            lo = q.z + 1;
+                            hi = q.z;
+                        }
+                        for (int tx = q.x; tx <= q.z; tx++) {
+                            if (exact && (tx < lo || tx > hi)) continue;
                             skey[o] = (KT)(row + tx);
-                            sval[o] = g;
+                            sval[o] = (!exact && mark && (tx < lo || tx > hi)) ? (g | LIST_DEAD) : g;
+                            o++;
                         }
                     }
                 }
@@ -958,6 +965,14 @@ __global__ void __launch_bounds__(DUP_THREADS) duplicate_keys(const uint32_t *id
                             sval[o + (uint32_t)(tx - lo)] = bg;
                         }
                         o += (uint32_t)(hi - lo + 1);
+                    }
+                } else if (mark) {  // every tile of the square; those the ellipse misses are marked dead
+                    const CoverRec cs = make_cover(rec[bg]);
+                    for (uint32_t kk = lane; kk < bc; kk += 32) {
+                        const int ty = by0 + (int)(kk / bw), tx = bx0 + (int)(kk % bw);
+                        int lo, hi;
+                        skey[bex + kk] = (KT)((ty - band_y0) * tiles_x + tx);
+                        sval[bex + kk] = cover_row(cs, ty, tx, tx, lo, hi) ? bg : (bg | LIST_DEAD);
                     }
                 } else {
                     for (uint32_t kk = lane; kk < bc; kk += 32) {
@@ -1136,8 +1151,55 @@ __global__ void __launch_bounds__(256) row_counts_kernel(int64_t P, const short4
         if (h[r]) atomicAdd(&out[r], h[r]);
 }
 
+// Compacted live lists (see LIST_DEAD): one CTA per tile writes the tile's unmarked entries, in list order, to cid
+// at the tile's own offsets, with the number of marked entries before each (cdb), and its live count (ccount).
+// Chunks of 8 warps x CW x 32 entries: warp w takes CW consecutive 32-entry rows (coalesced loads, ballots keep the
+// order), one block scan of the warp totals per chunk.
+constexpr int CW = 16;
+__global__ void __launch_bounds__(256) compact_lists(const uint32_t *v0, const uint32_t *v1, DevCounters *ctr,
+                                                     const uint2 *ranges, uint32_t *cid, uint32_t *cdb,
+                                                     uint32_t *ccount) {
+    pdl_wait();
+    pdl_launch();
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->compact = 1;
+    const uint32_t *val = ctr->tile_cur ? v1 : v0;
+    const uint2 rg = ranges[blockIdx.x];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = lanemask_lt();
+    __shared__ uint32_t wt[8];
+    uint32_t live = 0;  // live entries of the tile before this chunk
+    for (uint32_t c0 = rg.x; c0 < rg.y; c0 += 256 * CW) {
+        const uint32_t wb = c0 + (uint32_t)warp * 32 * CW;  // this warp's rows
+        uint32_t v[CW];
+        unsigned m[CW];
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int k = 0; k < CW; k++) {
+            const uint32_t i = wb + 32 * k + lane;
+            v[k] = i < rg.y ? val[i] : LIST_DEAD;
+            m[k] = __ballot_sync(0xffffffffu, (v[k] & LIST_DEAD) == 0u);
+            cnt += __popc(m[k]);
+        }
+        uint32_t total;
+        uint32_t lp = live + block_excl_scan256(lane == 0 ? cnt : 0u, wt, &total);  // (synchronises the CTA)
+        lp = __shfl_sync(0xffffffffu, lp, 0);  // this warp's base
+#pragma unroll
+        for (int k = 0; k < CW; k++) {
+            if ((m[k] >> lane) & 1u) {
+                const uint32_t p = lp + __popc(m[k] & lt);
+                cid[rg.x + p] = v[k];
+                cdb[rg.x + p] = (wb + 32 * k + lane - rg.x) - p;  // marked entries before it
+            }
+            lp += __popc(m[k]);
+        }
+        live += total;
+    }
+    if (threadIdx.x == 0) ccount[blockIdx.x] = live;
+}
+
 template <typename KT>
-cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st) {
+cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st,
+                      bool compact) {
     DevCounters *ctr = at<DevCounters>(ws, L.counters);
     SortState *ss_tile = at<SortState>(ws, L.sort_state[1]);
     const int bits = tile_key_bits(band);
@@ -1164,7 +1226,7 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
         (const uint32_t *)at<uint32_t>(ws, L.idx[0]), (const uint32_t *)at<uint32_t>(ws, L.idx[1]),
         (const DevCounters *)ctr, (const short4 *)at<short4>(ws, L.rect), (const Rec *)at<Rec>(ws, L.rec),
         (const unsigned long long *)at<unsigned long long>(ws, L.tmask), P, (const unsigned long long *)blocksum,
-        band.tiles_x, band.y0, band.y1, cap, tk0, tv0, ss_tile, npass, per);
+        band.tiles_x, band.y0, band.y1, cap, tk0, tv0, ss_tile, npass, per, compact && !exact ? 1 : 0);
     if (e0 != cudaSuccess) return e0;
     // K5
     // the key's bits split as evenly as possible over the passes (13 bits: 7 + 6, not 8 + 5)
@@ -1178,8 +1240,12 @@ cudaError_t bin_tiles(int64_t P, const Band &band, void *ws, const Layout &L, in
         if (e != cudaSuccess) return e;
     }
     // K6
-    return launch_k(tile_ranges<KT>, (unsigned)div_up(div_up(cap, 8), 256), 256, 0, st, (const KT *)tk0, (const KT *)tk1,
-                    (const DevCounters *)ctr, cap, at<uint2>(ws, L.ranges));
+    cudaError_t e6 = launch_k(tile_ranges<KT>, (unsigned)div_up(div_up(cap, 8), 256), 256, 0, st, (const KT *)tk0,
+                              (const KT *)tk1, (const DevCounters *)ctr, cap, at<uint2>(ws, L.ranges));
+    if (e6 != cudaSuccess || !compact || exact || band.n_tiles() == 0) return e6;
+    return launch_k(compact_lists, (unsigned)band.n_tiles(), 256, 0, st, (const uint32_t *)tv0, (const uint32_t *)tv1,
+                    ctr, (const uint2 *)at<uint2>(ws, L.ranges), at<uint32_t>(ws, L.cid), at<uint32_t>(ws, L.cdb),
+                    at<uint32_t>(ws, L.ccount));
 }
 
 }  // namespace
@@ -1194,6 +1260,20 @@ cudaError_t launch_row_counts(int64_t P, const Band &band, const void *ws, const
                     band.tiles_y, reinterpret_cast<unsigned long long *>(out));
 }
 
+namespace {
+__global__ void strip_marks(const uint32_t *src, uint32_t *dst, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i] & ~LIST_DEAD;
+}
+}  // namespace
+
+// Tile-list ids without K4's dead marks (tcgs_copy_lists).
+cudaError_t launch_strip_marks(const uint32_t *src, uint32_t *dst, int64_t n, cudaStream_t st) {
+    const int64_t blocks = div_up(n, 256);
+    strip_marks<<<(unsigned)(blocks < 4 * 148 ? blocks : 4 * 148), 256, 0, st>>>(src, dst, n);
+    return cudaGetLastError();
+}
+
 int tile_key_bits(const Band &band) {
     const int nt = band.n_tiles();
     int bits = 1;
@@ -1201,7 +1281,8 @@ int tile_key_bits(const Band &band) {
     return bits;
 }
 
-cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st) {
+cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st,
+                       bool compact) {
     DevCounters *ctr = at<DevCounters>(ws, L.counters);
     SortState *ss_depth = at<SortState>(ws, L.sort_state[0]);
     // one kernel clears the sort state, the tile ranges and the per-binning counters (K1's dropped /
@@ -1238,8 +1319,8 @@ cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, i
                          ctr, (const uint32_t *)at<uint32_t>(ws, L.long_runs), at<unsigned long long>(ws, L.fix_scratch));
         if (e != cudaSuccess) return e;
     }
-    if (band.n_tiles() <= 65536) return bin_tiles<uint16_t>(P, band, ws, L, cap, st);
-    return bin_tiles<uint32_t>(P, band, ws, L, cap, st);
+    if (band.n_tiles() <= 65536) return bin_tiles<uint16_t>(P, band, ws, L, cap, st, compact);
+    return bin_tiles<uint32_t>(P, band, ws, L, cap, st, compact);
 }
 
 cudaError_t launch_pack_lists(int64_t P, const double *mean2d, const double *conic, const double *opacity,

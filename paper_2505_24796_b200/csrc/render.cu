@@ -62,6 +62,7 @@ struct RenderArgs {
     float *rgb;
     float *T;
     int32_t *n_contrib;
+    const uint32_t *cid, *cdb, *ccount;  // compacted live lists (binning wrote them when ctr->compact)
     float *dump_beta;      // debug (FL_DUMP): beta' of every evaluated (list entry, pixel), [N][256]
     uint8_t *dump_class;   // debug (FL_DUMP): 1 cull, 2 blend, 3 terminate; 0 = not evaluated, [N][256]
 };
@@ -404,8 +405,17 @@ __device__ __forceinline__ void make_vrow(const float v[6], uint4 &lo8, uint4 &h
 // owns chunks p, p + NP, ...: it gathers and evaluates its chunk in parallel with the other producer,
 // then waits for the compaction token, places its live rows into the current stage, emits full stages
 // (issuing their MMAs) and passes the token on.
+// The producer-heavy build (the second compilation of this file) reads the compacted live lists when binning wrote
+// them (ctr->compact); the default build never sees them (see producer_heavy in tcgs_internal.cuh).
+#ifdef TCGS_K7_SECOND_BUILD
+constexpr bool K7_COMPACT = true;
+#else
+constexpr bool K7_COMPACT = false;
+#endif
+
 struct Cursor {
     int tile, seq, c, chunks, n;
+    int nfull;  // the tile's list length (n: the entries walked -- the live ones when the lists are compacted)
     uint32_t beg;
     float ox, oy;     // tile centre (16tx+8, 16ty+8), tensor_path.py:21-22
     bool prev_valid;  // the previous tile of the stream was a real one (its end chunk closes the stream)
@@ -449,11 +459,12 @@ __device__ __forceinline__ void cursor_tile(Cursor &k, const RenderArgs &a) {
         k.oy = (float)(ty * TILE + 8);
         const uint2 rg = a.ranges[k.tile];
         k.beg = rg.x;
-        k.n = (int)(rg.y - rg.x);
+        k.nfull = (int)(rg.y - rg.x);
+        k.n = (K7_COMPACT && a.ctr->compact) ? (int)a.ccount[k.tile] : k.nfull;  // compacted: the live entries
         k.chunks = k.n > 0 ? (k.n + 31) / 32 : 1;
     } else {
         k.beg = 0;
-        k.n = 0;
+        k.n = k.nfull = 0;
         k.chunks = 1;
     }
 }
@@ -506,6 +517,7 @@ __device__ void producer(K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL> &sm, const Ren
     constexpr int NP = K7_PRODUCERS;
     const int lane = threadIdx.x & 31;
     const unsigned FULL = 0xffffffffu, lt = lanemask_lt();
+    const bool cmp = K7_COMPACT && a.ctr->compact != 0;  // walking the compacted live lists
     Cursor cur;
     cur.tile = blockIdx.x;
     cur.seq = 0;
@@ -587,6 +599,8 @@ __device__ void producer(K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL> &sm, const Ren
         }
 #endif
         const bool valid = cur.c * 32 + lane < cur.n;
+        // compacted lists: the marked (dead) entries of the full list before this live one -- culls if reached
+        const uint32_t dpre = (K7_COMPACT && cmp && valid) ? a.cdb[cur.beg + cur.c * 32 + lane] : 0u;
         float v[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         bool live = false;
         // tile_center (tensor_path.py:21-22); the global-coordinate ablation keeps the origin at (0, 0)
@@ -682,7 +696,7 @@ __device__ void producer(K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL> &sm, const Ren
             uint32_t dead = sm.c_dead;
             const unsigned lm = __ballot_sync(FULL, live), dm = __ballot_sync(FULL, valid && !live);
             const int slot = fill + __popc(lm & lt);
-            const uint32_t my_dead = dead + __popc(dm & lt);
+            const uint32_t my_dead = dead + __popc(dm & lt) + dpre;
             const int nl = __popc(lm);
             auto put = [&](int row) {
                 const int st = k % S;
@@ -700,7 +714,7 @@ __device__ void producer(K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL> &sm, const Ren
             if (nl > 0) acquire();
             if (live && slot < K7_BATCH) put(slot);
             if (fill + nl >= K7_BATCH) {
-                emit(cur.tile, sq, K7_BATCH, 0, 0u, (uint32_t)cur.n);
+                emit(cur.tile, sq, K7_BATCH, 0, 0u, (uint32_t)cur.nfull);
                 fill = fill + nl - K7_BATCH;
                 if (fill > 0) {
                     acquire();
@@ -711,7 +725,7 @@ __device__ void producer(K7SmemT<MODE == TCGS_ALPHA_TC_K8_GLOBAL> &sm, const Ren
             }
             dead += __popc(dm);
             if (cur.c == cur.chunks - 1) {
-                emit(cur.tile, sq, fill, 1, dead, (uint32_t)cur.n);
+                emit(cur.tile, sq, fill, 1, dead + (uint32_t)(cur.nfull - cur.n), (uint32_t)cur.nfull);
                 fill = 0;
             }
             __syncwarp();
@@ -814,7 +828,8 @@ __global__ void __launch_bounds__(K7_THREADS, K7_CTAS_PER_SM) render_kernel(Rend
     const long long t_start = clock64();
 #endif
     const uint32_t tmem = TC ? sm.tmem_base : 0u;
-    const uint32_t *ids = a.ids_override ? a.ids_override : (a.ctr->tile_cur ? a.ids1 : a.ids0);
+    const uint32_t *ids = a.ids_override ? a.ids_override
+                                         : ((K7_COMPACT && a.ctr->compact) ? a.cid : (a.ctr->tile_cur ? a.ids1 : a.ids0));
 
     // per-thread K8 sums in 32 bits (a thread's pixels see at most a few hundred tiles of bounded lists); widened
     // to 64 bits in the CTA reduction
@@ -1177,6 +1192,9 @@ cudaError_t TCGS_K7_ENTRY(int alpha_mode, int early_cull, float *dump_beta, uint
     a.ids1 = at<uint32_t>(ws, L.tval[1]);
     a.ids_override = ids_override;
     a.ranges = at<uint2>(ws, L.ranges);
+    a.cid = at<uint32_t>(ws, L.cid);
+    a.cdb = at<uint32_t>(ws, L.cdb);
+    a.ccount = at<uint32_t>(ws, L.ccount);
     a.ctr = at<DevCounters>(ws, L.counters);
     a.tiles_x = band.tiles_x;
     a.band_y0 = band.y0;

@@ -65,6 +65,17 @@ constexpr int K7_TMEM_COLS = K7_TMEM_BUFS * 2 * K7_BATCH;  // buffers x pixel ha
 #endif
 constexpr int K7_CTAS_PER_SM = TCGS_K7_CTAS;
 
+// Long tile lists of mostly dead entries (C5: 6M Gaussians at 1080p, 74 % of the entries are Gaussians whose
+// alpha >= 1/255 ellipse misses the tile) bind K7's producers, which gather, box-test and compact every entry.
+// For such frames K4 marks those entries (LIST_DEAD) and a pass after the tile sort writes each tile's live
+// entries with the number of dead entries before each (the cull accounting of a termination), so K7 walks only
+// the live ones.  The tile lists themselves are unchanged (tcgs_copy_lists strips the marks).
+constexpr uint32_t LIST_DEAD = 0x80000000u;
+constexpr int64_t COMPACT_MIN_PER_TILE = 400;  // Gaussians per frame tile from which binning compacts
+inline bool producer_heavy(int64_t P, int tiles_x, int tiles_y) {
+    return P > COMPACT_MIN_PER_TILE * (int64_t)tiles_x * (int64_t)tiles_y;
+}
+
 // Per-Gaussian record consumed by the blend kernel (48 B, three 16 B loads).
 struct __align__(16) Rec {
     float mx, mx_lo, my, my_lo;  // float64 mean2d (src/tilesplat/projection.py:80-82) as fp32 hi + lo pairs
@@ -160,7 +171,7 @@ struct DevCounters {
     int depth_shift;           // K2: prefix shift of the depth key (0: the prefix sort is exact)
     unsigned int n_long_runs;  // K2 fix-up: runs of equal prefixes longer than a thread handles
     int debug_written;         // K1 ran with opts.debug (tcgs_copy_projection's float64 buffers are valid)
-    int pad_;
+    int compact;               // binning also wrote the compacted live lists (cid / cdb / ccount) for K7
 };
 
 // Per-sort bookkeeping of the onesweep LSD radix sort (all decided on the device).
@@ -190,6 +201,7 @@ inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
 struct Layout {
     size_t counters, sort_state[2], rec, tmask, rect, key_src, key64[2], long_runs, fix_scratch, idx[2], radius, dbg_conic, dbg_depth, dbg_mean2d;
     size_t blocksum, lb_depth, lb_tile, lb_bytes, os_hdr, tkey[2], tval[2], ranges, total;
+    size_t cid, cdb, ccount;  // compacted live lists: ids, dead entries before each, live entries per tile
     size_t zero_begin, zero_bytes;  // sort state, cleared at the start of every binning
     static Layout make(int64_t P, int W, int H, int64_t cap) {
         Layout L;
@@ -227,6 +239,9 @@ struct Layout {
         L.tval[0] = take(sizeof(uint32_t) * cn);
         L.tval[1] = take(sizeof(uint32_t) * cn);
         L.ranges = take(sizeof(uint2) * (nt ? nt : 1));
+        L.cid = take(sizeof(uint32_t) * cn);
+        L.cdb = take(sizeof(uint32_t) * cn);
+        L.ccount = take(sizeof(uint32_t) * (nt ? nt : 1));
         L.total = o;
         return L;
     }
@@ -267,7 +282,8 @@ cudaError_t launch_colour(const tcgs_scene &scene, const tcgs_camera &cam, const
 cudaError_t launch_preprocess_views(const tcgs_scene &scene, const tcgs_camera *cams, const Band *bands, int n_views,
                                     int debug, int coverage, int defer_colour, void *const *ws, const Layout *L,
                                     cudaStream_t st);
-cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st);
+cudaError_t launch_bin(int64_t P, const Band &band, void *ws, const Layout &L, int64_t cap, cudaStream_t st,
+                       bool compact = false);
 cudaError_t launch_render_k7(int alpha_mode, int early_cull, float *dump_beta, uint8_t *dump_class,
                              const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
                              void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st);
@@ -283,9 +299,11 @@ inline cudaError_t launch_render(int64_t P, int alpha_mode, int early_cull, floa
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t nt = band.n_tiles();
-    // TCGS_K7_BUILD=few|many in the environment forces one build (tests: both give the same frame)
+    // TCGS_K7_BUILD=few|many in the environment forces one build (tests: both give the same frame); compacted lists
+    // (producer-heavy frames) need the few build, which alone reads them
     static const char *force = getenv("TCGS_K7_BUILD");
-    const bool few = force && force[0] ? force[0] == 'f' : (nt < 4 * sms || P > 400 * nt);
+    const bool heavy = producer_heavy(P, band.tiles_x, band.tiles_y);
+    const bool few = heavy || (force && force[0] ? force[0] == 'f' : nt < 4 * sms);
     auto f = few ? launch_render_k7_few : launch_render_k7;
     return f(alpha_mode, early_cull, dump_beta, dump_class, cam, band, ids_override, ws, L, rgb, T, n_contrib, st);
 }
@@ -295,6 +313,7 @@ cudaError_t launch_pack_lists(int64_t P, const double *mean2d, const double *con
 cudaError_t launch_row_counts(int64_t P, const Band &band, const void *ws, const Layout &L, int64_t *out,
                               cudaStream_t st);
 int tile_key_bits(const Band &band);
+cudaError_t launch_strip_marks(const uint32_t *src, uint32_t *dst, int64_t n, cudaStream_t st);
 // Host-side count of kernels this library has launched (tcgs_launch_count): the bench's gpu_launches.
 void note_launch();
 

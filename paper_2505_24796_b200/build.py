@@ -13,10 +13,12 @@ LIB_DIR = os.path.join(HERE, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libtcgs.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["abi.cu", "preprocess.cu", "binning.cu", "render.cu", "render.cu:few"]
-# render.cu is compiled twice: the default K7 (4 CTAs/SM x 2 producer warps) and the few-tiles K7 (3 x 4)
+SOURCES = ["abi.cu", "preprocess.cu", "binning.cu", "render.cu", "render.cu:few", "render.cu:heavy"]
+# render.cu is compiled three times: the default K7 (4 CTAs/SM x 2 producer warps), the few-tiles K7 (3 x 4) and the
+# heavy K7 (the default residency reading the compacted live lists of producer-heavy frames)
 VARIANT_FLAGS = {"few": ["-DTCGS_K7_ENTRY=launch_render_k7_few", "-DTCGS_K7_CTAS=3", "-DTCGS_K7_PRODUCERS=4",
-                         "-DTCGS_K7_SECOND_BUILD"]}
+                         "-DTCGS_K7_SECOND_BUILD"],
+                 "heavy": ["-DTCGS_K7_ENTRY=launch_render_k7_heavy", "-DTCGS_K7_COMPACT", "-DTCGS_K7_SECOND_BUILD"]}
 # preprocess.cu must not contract a*b+c into FMA: it reproduces numpy's float64 operation order.
 PER_FILE_FLAGS = {"preprocess.cu": ["--fmad=false"]}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -405,9 +405,9 @@ __device__ __forceinline__ void make_vrow(const float v[6], uint4 &lo8, uint4 &h
 // owns chunks p, p + NP, ...: it gathers and evaluates its chunk in parallel with the other producer,
 // then waits for the compaction token, places its live rows into the current stage, emits full stages
 // (issuing their MMAs) and passes the token on.
-// The producer-heavy build (the second compilation of this file) reads the compacted live lists when binning wrote
-// them (ctr->compact); the default build never sees them (see producer_heavy in tcgs_internal.cuh).
-#ifdef TCGS_K7_SECOND_BUILD
+// The heavy build (TCGS_K7_COMPACT, a third compilation of this file) reads the compacted live lists when binning
+// wrote them (ctr->compact); the other builds never see them (see producer_heavy in tcgs_internal.cuh).
+#ifdef TCGS_K7_COMPACT
 constexpr bool K7_COMPACT = true;
 #else
 constexpr bool K7_COMPACT = false;
@@ -1176,9 +1176,10 @@ cudaError_t launch_variant(const RenderArgs &a, bool dyn, bool early_cull, bool 
 
 }  // namespace
 
-// This file is compiled twice (paper_2505_24796_b200/build.py): launch_render_k7 with the default residency (4 CTAs
-// per SM, 2 producer warps) and launch_render_k7_few with 3 CTAs x 4 producer warps, the better trade when a frame
-// has fewer tiles than resident CTAs (long per-tile lists, e.g. C1's 256 tiles: 94 -> 66 us).
+// This file is compiled three times (paper_2505_24796_b200/build.py): launch_render_k7 with the default residency
+// (4 CTAs per SM, 2 producer warps); launch_render_k7_few with 3 CTAs x 4 producer warps, the better trade when a
+// frame has fewer tiles than resident CTAs (C1's 256 tiles: 94 -> 66 us); launch_render_k7_heavy, the default
+// residency walking the compacted live lists of producer-heavy frames (C5).
 #ifndef TCGS_K7_ENTRY
 #define TCGS_K7_ENTRY launch_render_k7
 #endif

@@ -290,8 +290,12 @@ cudaError_t launch_render_k7(int alpha_mode, int early_cull, float *dump_beta, u
 cudaError_t launch_render_k7_few(int alpha_mode, int early_cull, float *dump_beta, uint8_t *dump_class,
                                  const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
                                  void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st);
-// K7: the 3-CTA x 4-producer build when the frame is producer-heavy -- fewer tiles than 4 resident CTAs per SM can
-// take (C1), or long per-tile lists, by Gaussians per tile (C5: 735 per tile, K7 2.45 -> 2.37 ms; C2 has 122)
+cudaError_t launch_render_k7_heavy(int alpha_mode, int early_cull, float *dump_beta, uint8_t *dump_class,
+                                   const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
+                                   void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st);
+// K7 build: producer-heavy frames (> COMPACT_MIN_PER_TILE Gaussians per frame tile: binning compacted their lists)
+// -> the heavy build; fewer tiles than 4 resident CTAs per SM can take (C1) -> the 3-CTA x 4-producer build;
+// otherwise the default.  TCGS_K7_BUILD=few|many in the environment forces one of the latter two (tests).
 inline cudaError_t launch_render(int64_t P, int alpha_mode, int early_cull, float *dump_beta, uint8_t *dump_class,
                                  const tcgs_camera &cam, const Band &band, const uint32_t *ids_override,
                                  void *ws, const Layout &L, float *rgb, float *T, int32_t *n_contrib, cudaStream_t st) {
@@ -299,11 +303,11 @@ inline cudaError_t launch_render(int64_t P, int alpha_mode, int early_cull, floa
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t nt = band.n_tiles();
-    // TCGS_K7_BUILD=few|many in the environment forces one build (tests: both give the same frame); compacted lists
-    // (producer-heavy frames) need the few build, which alone reads them
     static const char *force = getenv("TCGS_K7_BUILD");
-    const bool heavy = producer_heavy(P, band.tiles_x, band.tiles_y);
-    const bool few = heavy || (force && force[0] ? force[0] == 'f' : nt < 4 * sms);
+    if (producer_heavy(P, band.tiles_x, band.tiles_y) && !ids_override)
+        return launch_render_k7_heavy(alpha_mode, early_cull, dump_beta, dump_class, cam, band, ids_override, ws, L,
+                                      rgb, T, n_contrib, st);
+    const bool few = force && force[0] ? force[0] == 'f' : nt < 4 * sms;
     auto f = few ? launch_render_k7_few : launch_render_k7;
     return f(alpha_mode, early_cull, dump_beta, dump_class, cam, band, ids_override, ws, L, rgb, T, n_contrib, st);
 }

@@ -263,7 +263,10 @@ int tcgs_bin(int64_t P, const tcgs_camera *cam, const tcgs_opts *opts, void *ws,
     const Layout L = Layout::make(P, cam->width, cam->height, max_splats);
     time_mark(opts, ws, ST_SORT, 0, (cudaStream_t)stream);
     const Band band = make_band(*cam, opts);
-    const bool compact = producer_heavy(P, band.tiles_x, band.tiles_y) && !(opts && opts->dump_beta);
+    // compacted live lists cull whole (Gaussian, tile) entries before K7: part of EarlyCull (with it off, or in the
+    // global-coordinate ablation, K7 evaluates every entry as the reference does); not with the debug dump
+    const bool compact = producer_heavy(P, band.tiles_x, band.tiles_y) && !(opts && opts->dump_beta) &&
+                         (!opts || (opts->early_cull && opts->alpha_mode != TCGS_ALPHA_TC_K8_GLOBAL));
     cudaError_t e = launch_bin(P, band, ws, L, max_splats, (cudaStream_t)stream, compact);
     if (e != cudaSuccess) return cuda_fail(e, "bin");
     time_mark(opts, ws, ST_SORT, 1, (cudaStream_t)stream);

@@ -296,7 +296,7 @@ def profile_traffic(config="c2"):
     import glob
 
     if config == "c5":  # the ablation capture's default variant (hi/lo, EarlyCull on, dynamic schedule)
-        p = os.path.join(ROOT, "profiles", "r2i2_ablation_c5_ncu.json")
+        p = os.path.join(ROOT, "profiles", "r2j2_ablation_c5_ncu.json")
         if not os.path.exists(p):
             return None
         with open(p) as f:
@@ -309,8 +309,8 @@ def profile_traffic(config="c2"):
                 "warp_inst_per_launch": sum(inst) / len(inst)}
     if config != "c2":
         return None
-    # the capture of the current build first (K7 rows of profiles/r2i2_frame_ncu.json), then older ones
-    current = os.path.join(ROOT, "profiles", "r2i2_k7_ncu.json")
+    # the capture of the current build first (K7 rows of profiles/r2j2_frame_ncu.json), then older ones
+    current = os.path.join(ROOT, "profiles", "r2j2_k7_ncu.json")
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_k7_ncu.json")))  # r1_ < ... < r2a_ < r2b_
     files = [f for f in files if f != current] + ([current] if os.path.exists(current) else [])
     for p in reversed(files):
